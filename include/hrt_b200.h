@@ -1,0 +1,188 @@
+/*
+ * hrt_b200.h — C ABI of libhrt_b200.so, the B200 (sm_100a) backend for the
+ * Jacobi / halo-exchange / device-message hot path of the reference `hrt`
+ * runtime (arXiv 2303.02543, /root/reference/pkg/src/hrt).
+ *
+ * Plain C types only (pointers, sizes, integers); no torch types.  Every
+ * function returns 0 (HRT_OK) on success or a negative HRT_E_* code; the
+ * message for the calling thread is in hrt_last_error().  Error codes map
+ * onto the reference's exception tree (errors.py:4-65) — see
+ * paper_2303_02543_b200/errors.py.
+ *
+ * The reference has no native ABI: its seams are Python classes.  Each
+ * entry point below names the reference interface it replaces.  The ctypes
+ * binding a maintainer would add to the reference is shown in
+ * INTEGRATION.md; paper_2303_02543_b200/_native.py is this repo's binding.
+ */
+#ifndef HRT_B200_H
+#define HRT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HRT_ABI_VERSION 1
+#define HRT_ALIGNMENT 256      /* devices.py:35 ALIGNMENT */
+#define HRT_BOUNDARY 1.0       /* bench/jacobi.py:38 BOUNDARY */
+
+/* error codes */
+#define HRT_OK 0
+#define HRT_E_INVALID (-1)        /* HrtError */
+#define HRT_E_OOM (-2)            /* OutOfDeviceMemory   devices.py:122 */
+#define HRT_E_DOUBLE_FREE (-3)    /* DoubleFree          devices.py:127 */
+#define HRT_E_LOCATION (-4)       /* InvalidLocation     devices.py:423-457 */
+#define HRT_E_UNKNOWN_TOKEN (-5)  /* UnknownToken        devices.py:564 */
+#define HRT_E_CUDA (-6)           /* failed launch/copy -> FAILED token -> TaskFailed runtime.py:507 */
+#define HRT_E_NCCL (-7)           /* transport failure   (TransportClosed / ProtocolError) */
+#define HRT_E_UNSUPPORTED (-8)
+
+const char *hrt_last_error(void);
+int hrt_version(void);
+
+/* ---- devices (DeviceRegistry.register_device devices.py:364-380) ---- */
+int hrt_device_count(int *n);
+int hrt_device_info(int gpu, char *name, int name_len, int *sm_count, uint64_t *hbm_bytes,
+                    int *cc_major, int *cc_minor);
+/* enable NVLink peer access gpu -> peer (lifts devices.py:456-457) */
+int hrt_enable_peer_access(int gpu, int peer);
+int hrt_device_synchronize(int gpu);
+int hrt_pointer_device(const void *ptr, int *gpu);
+
+/* ---- first-fit free list: FreeListAllocator devices.py:89-154 (host logic) ---- */
+int hrt_fl_create(uint64_t capacity, uint64_t alignment, void **fl);
+int hrt_fl_alloc(void *fl, uint64_t size, uint64_t *offset, uint64_t *granted);   /* alloc 108-122 */
+int hrt_fl_free(void *fl, uint64_t offset, uint64_t *size);                       /* free 124-137 */
+int hrt_fl_stats(void *fl, uint64_t *live_bytes, uint64_t *free_bytes, uint64_t *free_blocks);
+int hrt_fl_check(void *fl);                                                       /* check 147-154 */
+void hrt_fl_destroy(void *fl);
+
+/* ---- device pools: DeviceBackend.attach/region devices.py:299-305 +
+ *      DeviceRegistry.pool_alloc/pool_free devices.py:398-404 ---- */
+int hrt_pool_create(int gpu, uint64_t capacity, void **pool);
+int hrt_pool_alloc(void *pool, uint64_t size, uint64_t *offset, uint64_t *granted, void **dptr);
+int hrt_pool_free(void *pool, uint64_t offset);
+int hrt_pool_stats(void *pool, uint64_t *live_bytes, uint64_t *free_bytes);
+int hrt_pool_base(void *pool, void **base);
+int hrt_pool_destroy(void *pool);
+
+/* ---- streams (_Device.compute_streams/h2d/d2h devices.py:322-329) ---- */
+int hrt_stream_create(int gpu, int priority, void **stream);
+int hrt_stream_wrap(int gpu, void *cuda_stream, void **stream);   /* adopt an external cudaStream_t */
+void *hrt_stream_handle(void *stream);                              /* the cudaStream_t */
+int hrt_stream_destroy(void *stream, int owned);
+int hrt_stream_synchronize(void *stream);
+
+/* ---- completion tokens: CompletionToken devices.py:199-222, poll 560-567 ---- */
+int hrt_token_record(void *stream, uint64_t *token);
+int hrt_token_query(uint64_t token);              /* 0 pending, 1 complete, 2 failed, <0 error */
+int hrt_token_wait(uint64_t token);
+int hrt_stream_wait_token(void *stream, uint64_t token);   /* GPU-side dependency edge */
+int hrt_token_elapsed_ms(uint64_t start, uint64_t end, float *ms);
+int hrt_token_release(uint64_t token);
+
+/* ---- transfers: DeviceRegistry.enqueue_transfer devices.py:446-496,
+ *      HostPinnedPool devices.py:167-196 ---- */
+int hrt_host_alloc(uint64_t bytes, void **ptr);     /* page-locked */
+int hrt_host_free(void *ptr);
+int hrt_host_register(void *ptr, uint64_t bytes);
+int hrt_host_unregister(void *ptr);
+int hrt_copy_async(void *stream, void *dst, const void *src, uint64_t bytes);   /* H2D/D2H/D2D (UVA) */
+int hrt_copy_peer_async(void *stream, void *dst, int dst_gpu, const void *src, int src_gpu,
+                        uint64_t bytes);                                         /* NVLink peer copy */
+int hrt_copy2d_async(void *stream, void *dst, uint64_t dpitch, const void *src, uint64_t spitch,
+                     uint64_t width, uint64_t height);
+int hrt_memset_async(void *stream, void *dst, int value, uint64_t bytes);
+
+/* ---- Jacobi hot path: bench/jacobi.py ---- */
+
+/* Ghosted chunk layout.  Element (i,j,k) of the ghosted (ex+2, ey+2, ez+2)
+ * chunk (jacobi.py:383) lives at base + origin + i*stride[0] + j*stride[1]
+ * + k*stride[2] (float64 elements).  ndim 2 is the (X,Y,1) slab: no z ghosts
+ * are stored, the two z neighbours are the constant BOUNDARY. */
+typedef struct hrt_chunk_layout {
+    int32_t ndim;
+    int32_t pad_;
+    int64_t ext[3];
+    int64_t stride[3];
+    int64_t origin;
+    int64_t elems;
+} hrt_chunk_layout_t;
+
+/* One face copy (pack+send+unpack fused, jacobi.py:102-124 + 237):
+ * dst[o*ds0 + i*ds1] = src[o*ss0 + i*ss1] for o < n0, i < n1, with separate
+ * addresses for step parity 0 and 1 (the alternating buffers, jacobi.py:213-217). */
+typedef struct hrt_halo_seg {
+    uint64_t src[2];
+    uint64_t dst[2];
+    int64_t n0, n1;
+    int64_t ss0, ss1;
+    int64_t ds0, ds1;
+} hrt_halo_seg_t;
+
+/* One half of a face crossing a process boundary: `count` contiguous
+ * float64 at buf[parity] sent to (kind 0) or received from (kind 1) NCCL
+ * rank `peer`.  Both ranks list their ops in one canonical global order
+ * (destination chunk, face), so NCCL's in-order pairing matches them. */
+typedef struct hrt_remote_seg {
+    uint64_t buf[2];
+    int64_t count;
+    int32_t peer;
+    int32_t kind;
+} hrt_remote_seg_t;
+
+/* Step engine for all chunks of one GPU (replaces the per-chunk task chain
+ * of _RankDriver.start_step/_try_finish_step jacobi.py:219-273).
+ * bufs: 2*nchunks device addresses (buffer 0, buffer 1 per chunk).
+ * segs: same-GPU / peer faces, executed before every update. */
+int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t *layout, int nchunks,
+                           const uint64_t *bufs, const hrt_halo_seg_t *segs, int nsegs,
+                           void **plan);
+/* faces that cross ranks: NCCL exchange, then `post` (unpack) copies */
+int hrt_jacobi_plan_set_remote(void *plan, void *comm, const hrt_remote_seg_t *remote,
+                               int nremote, const hrt_halo_seg_t *post, int npost);
+int hrt_jacobi_plan_set_rows(void *plan, int64_t rows);
+/* one step: halo faces, then the 7-point update of every chunk (_update_body
+ * jacobi.py:70-79); resid (nullable, device, uint64 bit patterns of float64)
+ * receives max|u'-u| at index `step` via atomicMax (must start zeroed). */
+int hrt_jacobi_plan_step(void *plan, void *stream, int64_t step, uint64_t *resid);
+int hrt_jacobi_plan_update(void *plan, void *stream, int parity, uint64_t *resid_slot);
+int hrt_jacobi_plan_halo(void *plan, void *stream, int parity);
+/* steps [first, first+n); mode 0 direct launches, 1 CUDA-graph replay */
+int hrt_jacobi_plan_run(void *plan, void *stream, int64_t first, int64_t n, uint64_t *resid,
+                        int mode);
+/* as run(mode 0) with events around every launch; synchronises */
+int hrt_jacobi_plan_run_timed(void *plan, void *stream, int64_t first, int64_t n, uint64_t *resid,
+                              double *update_ms, double *halo_ms, double *total_ms);
+int hrt_jacobi_plan_destroy(void *plan);
+
+/* standalone plane copies (halo_pack_f / halo_unpack_f bodies); segs on device */
+int hrt_halo_copy(void *stream, const hrt_halo_seg_t *segs_dev, int nsegs, int parity,
+                  int64_t max_elems);
+/* ghost shell of one chunk buffer: faces in `mask` (bit f = FACES[f],
+ * jacobi.py:41) get `value` (Dirichlet, jacobi.py:386-393), others 0 */
+int hrt_jacobi_ghost_fill(void *stream, double *base, const hrt_chunk_layout_t *layout,
+                          int mask, double value);
+/* float(np.sum(a)) bit-exact (jacobi.py:436): numpy pairwise summation on
+ * the GPU; synchronises the stream */
+int hrt_np_sum(void *stream, const double *a, int64_t n, double *out);
+/* self-check of the Markstein division used by the update kernel against
+ * IEEE division: n hashed samples (mode 0 uniform [0,6), 1 near 1/2/3/6,
+ * 2 random finite bit patterns); synchronises */
+int hrt_div6_sweep(void *stream, uint64_t seed, int64_t n, int mode, uint64_t *mismatches,
+                   double *first_bad);
+
+/* ---- NCCL (cross-process faces; replaces Transport transport.py:40-278
+ *      for payloads) ---- */
+int hrt_nccl_unique_id(uint8_t *out128);
+int hrt_nccl_init(int gpu, int rank, int world, const uint8_t *id128, void **comm);
+int hrt_nccl_destroy(void *comm);
+int hrt_nccl_exchange(void *comm, void *stream, const hrt_remote_seg_t *segs, int n, int parity);
+int hrt_nccl_allreduce_max_u64(void *comm, void *stream, uint64_t *buf, int64_t count);
+int hrt_nccl_allreduce_sum_f64(void *comm, void *stream, double *buf, int64_t count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HRT_B200_H */

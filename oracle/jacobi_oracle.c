@@ -1,0 +1,189 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * CPU restatement (plain C, optional OpenMP) of the reference's Jacobi
+ * result oracle and of the checksum it reports.  Only tests/, the
+ * __graft_entry__.smoke() checker and bench.py's cpu_baseline /
+ * `--impl reference` legs may load this library; the product path never
+ * does (it fails loudly when its CUDA library is missing instead).
+ *
+ * Parity pin: tests/test_oracle.py checks every entry point here against
+ * golden vectors produced by the reference itself (tests/golden/, made by
+ * tests/golden/make_golden.py running /root/reference/pkg/src/hrt).
+ *
+ * Restated reference behaviour (paths relative to /root/reference):
+ *   - oracle_jacobi3d: pkg/src/hrt/bench/jacobi.py:49-67 (jacobi_reference).
+ *     Ghosted (X+2, Y+2, Z+2) float64 C-order array, every ghost face = 1.0
+ *     (BOUNDARY, jacobi.py:38, 53-55), interior 0.0; each step
+ *     nxt = (((((xm + xp) + ym) + yp) + zm) + zp) / 6.0 with IEEE division
+ *     (jacobi.py:58-65; the per-chunk body _update_body jacobi.py:70-79 uses
+ *     the identical expression, so the decomposed run is bitwise equal).
+ *   - residual history (builder-defined, the reference has none — see
+ *     SURVEY.md §0.7): r_s = max over interior |u_{s+1} - u_s|.  Max is exact
+ *     under any reduction order, so the GPU result must match bitwise.
+ *   - oracle_np_sum: numpy's float64 add.reduce over a contiguous array, i.e.
+ *     0.0 + pairwise_sum(a, n) (numpy umath loops_utils pairwise summation,
+ *     PW_BLOCKSIZE 128, 8 partial accumulators).  This is the checksum the
+ *     reference computes with float(np.sum(assembled)) at jacobi.py:436.
+ *
+ * Build: oracle/Makefile (gcc -O2 -fopenmp -ffp-contract=off -fno-fast-math).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define BOUNDARY 1.0
+
+static inline size_t gidx(int64_t i, int64_t j, int64_t k, int64_t Y2, int64_t Z2) {
+    return (size_t)((i * Y2 + j) * Z2 + k);
+}
+
+/* Single-array Jacobi, jacobi.py:49-67.  out_interior receives X*Y*Z
+ * doubles (C order); resid (may be NULL) receives `steps` residuals.
+ * Returns 0, or -1 on allocation failure. */
+int oracle_jacobi3d(int64_t X, int64_t Y, int64_t Z, int64_t steps,
+                    double *out_interior, double *resid) {
+    const int64_t X2 = X + 2, Y2 = Y + 2, Z2 = Z + 2;
+    const size_t n = (size_t)X2 * Y2 * Z2;
+    double *u = (double *)malloc(n * sizeof(double));
+    double *v = (double *)malloc(n * sizeof(double));
+    if (!u || !v) { free(u); free(v); return -1; }
+    /* interior 0.0, every ghost face 1.0 (jacobi.py:52-55) */
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < X2; ++i)
+        for (int64_t j = 0; j < Y2; ++j)
+            for (int64_t k = 0; k < Z2; ++k) {
+                int ghost = (i == 0 || i == X2 - 1 || j == 0 || j == Y2 - 1 ||
+                             k == 0 || k == Z2 - 1);
+                u[gidx(i, j, k, Y2, Z2)] = ghost ? BOUNDARY : 0.0;
+            }
+    memcpy(v, u, n * sizeof(double)); /* nxt = u.copy() keeps the ghosts */
+    for (int64_t s = 0; s < steps; ++s) {
+        double rmax = 0.0;
+        #pragma omp parallel for schedule(static) reduction(max : rmax)
+        for (int64_t i = 1; i <= X; ++i) {
+            for (int64_t j = 1; j <= Y; ++j) {
+                for (int64_t k = 1; k <= Z; ++k) {
+                    double xm = u[gidx(i - 1, j, k, Y2, Z2)];
+                    double xp = u[gidx(i + 1, j, k, Y2, Z2)];
+                    double ym = u[gidx(i, j - 1, k, Y2, Z2)];
+                    double yp = u[gidx(i, j + 1, k, Y2, Z2)];
+                    double zm = u[gidx(i, j, k - 1, Y2, Z2)];
+                    double zp = u[gidx(i, j, k + 1, Y2, Z2)];
+                    double acc = xm + xp;  /* left-associative, jacobi.py:59-64 */
+                    acc = acc + ym;
+                    acc = acc + yp;
+                    acc = acc + zm;
+                    acc = acc + zp;
+                    double nv = acc / 6.0; /* IEEE division, jacobi.py:65 */
+                    double d = fabs(nv - u[gidx(i, j, k, Y2, Z2)]);
+                    if (d > rmax) rmax = d;
+                    v[gidx(i, j, k, Y2, Z2)] = nv;
+                }
+            }
+        }
+        if (resid) resid[s] = rmax;
+        double *t = u; u = v; v = t;
+    }
+    if (out_interior) {
+        #pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < X; ++i)
+            for (int64_t j = 0; j < Y; ++j)
+                memcpy(out_interior + (size_t)(i * Y + j) * Z,
+                       u + gidx(i + 1, j + 1, 1, Y2, Z2), (size_t)Z * sizeof(double));
+    }
+    free(u);
+    free(v);
+    return 0;
+}
+
+/* Same arithmetic specialised to the (X, Y, 1) slab the BASELINE "2D"
+ * configs map onto: the two z ghosts are the constant
+ * 1.0, so u' = (((((xm+xp)+ym)+yp)+1.0)+1.0)/6.0.  A 2D (X+2)x(Y+2) array
+ * instead of (X+2)x(Y+2)x3 — identical results, a third of the memory, so
+ * the bounded CPU baseline can reach the large configs. */
+int oracle_jacobi2d(int64_t X, int64_t Y, int64_t steps, double *out_interior,
+                    double *resid) {
+    const int64_t X2 = X + 2, Y2 = Y + 2;
+    const size_t n = (size_t)X2 * Y2;
+    double *u = (double *)malloc(n * sizeof(double));
+    double *v = (double *)malloc(n * sizeof(double));
+    if (!u || !v) { free(u); free(v); return -1; }
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < X2; ++i)
+        for (int64_t j = 0; j < Y2; ++j) {
+            int ghost = (i == 0 || i == X2 - 1 || j == 0 || j == Y2 - 1);
+            u[i * Y2 + j] = ghost ? BOUNDARY : 0.0;
+        }
+    memcpy(v, u, n * sizeof(double));
+    for (int64_t s = 0; s < steps; ++s) {
+        double rmax = 0.0;
+        #pragma omp parallel for schedule(static) reduction(max : rmax)
+        for (int64_t i = 1; i <= X; ++i) {
+            const double *up = u + (i - 1) * Y2, *mid = u + i * Y2, *dn = u + (i + 1) * Y2;
+            double *out = v + i * Y2;
+            for (int64_t j = 1; j <= Y; ++j) {
+                double acc = up[j] + dn[j];
+                acc = acc + mid[j - 1];
+                acc = acc + mid[j + 1];
+                acc = acc + BOUNDARY;
+                acc = acc + BOUNDARY;
+                double nv = acc / 6.0;
+                double d = fabs(nv - mid[j]);
+                if (d > rmax) rmax = d;
+                out[j] = nv;
+            }
+        }
+        if (resid) resid[s] = rmax;
+        double *t = u; u = v; v = t;
+    }
+    if (out_interior) {
+        #pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < X; ++i)
+            memcpy(out_interior + (size_t)i * Y, u + (i + 1) * Y2 + 1, (size_t)Y * sizeof(double));
+    }
+    free(u);
+    free(v);
+    return 0;
+}
+
+/* numpy pairwise summation (float64, contiguous). */
+static double pairwise(const double *a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        int64_t i;
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return pairwise(a, n2) + pairwise(a + n2, n - n2);
+    }
+}
+
+/* float(np.sum(a)) for a contiguous float64 array (jacobi.py:436). */
+double oracle_np_sum(const double *a, int64_t n) { return 0.0 + pairwise(a, n); }
+
+/* Largest single step of the cfg1/cfg2 sweep, timed by bench.py's CPU leg:
+ * `steps` sweeps of the slab, interior written to nowhere.  Returns 0. */
+int oracle_jacobi2d_sweeps(int64_t X, int64_t Y, int64_t steps) {
+    return oracle_jacobi2d(X, Y, steps, NULL, NULL);
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    extern int omp_get_max_threads(void);
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

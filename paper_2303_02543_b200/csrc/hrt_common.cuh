@@ -1,0 +1,39 @@
+// Shared helpers for libhrt_b200: error plumbing and handle types.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+
+#include "../../include/hrt_b200.h"
+
+namespace hrt {
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+struct Stream {
+    cudaStream_t s = nullptr;
+    int gpu = 0;
+};
+
+inline Stream* as_stream(void* h) { return reinterpret_cast<Stream*>(h); }
+
+// Make `gpu` current for the calling thread (cheap when already current).
+int use_device(int gpu);
+
+}  // namespace hrt
+
+#define HRT_CUDA(call)                                              \
+    do {                                                            \
+        cudaError_t _e = (call);                                    \
+        if (_e != cudaSuccess) return hrt::cuda_fail(_e, #call);    \
+    } while (0)
+
+#define HRT_CHECK_ARG(cond, msg)                                    \
+    do {                                                            \
+        if (!(cond)) {                                              \
+            hrt::set_error("%s", msg);                              \
+            return HRT_E_INVALID;                                   \
+        }                                                           \
+    } while (0)

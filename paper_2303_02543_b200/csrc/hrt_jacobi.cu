@@ -1,0 +1,896 @@
+// libhrt_b200 — the Jacobi hot path on sm_100a.
+//
+// Reference behaviour (paths under /root/reference/pkg/src/hrt):
+//   bench/jacobi.py:70-79   _update_body: 7-point update, sum order
+//                           (((((xm+xp)+ym)+yp)+zm)+zp) and IEEE /6.0
+//   bench/jacobi.py:102-124 halo pack/unpack bodies (plane copies)
+//   bench/jacobi.py:219-273 per-step protocol: pack, send, unpack, update
+//   bench/jacobi.py:425-436 gather and checksum float(np.sum(assembled))
+//
+// B200 design:
+//   * every chunk lives in HBM as two ghosted float64 buffers; same-GPU halo
+//     exchange is one launch of `halo_copy_kernel` that reads the neighbour's
+//     boundary plane in place and writes this chunk's ghost plane (pack +
+//     message + unpack fused into one plane copy; cross-GPU planes are read
+//     over NVLink by the same kernel or exchanged with NCCL send/recv);
+//   * one `slab_update_kernel` launch per step covers every chunk on the GPU
+//     (block table), marching rows with a register window, 128-bit loads and
+//     warp shuffles for the y neighbours, a fused L-inf residual
+//     (warp-shuffle max + one 64-bit atomicMax per CTA);
+//   * the division is Markstein's correction q=s*r; e=fma(-q,6,s); q=fma(e,r,q)
+//     with r=RN(1/6), which is correctly rounded (== IEEE s/6.0) whenever
+//     s/6 is normal; tiny/special inputs take the IEEE path.  Parity tests
+//     check it bitwise against IEEE division on the GPU.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "hrt_common.cuh"
+
+namespace hrt {
+
+// ---------------------------------------------------------------------------
+// arithmetic
+
+__device__ __forceinline__ double div6(double s) {
+#if HRT_IEEE_DIV
+    return __ddiv_rn(s, 6.0);
+#else
+    const double r = 0x1.5555555555555p-3;  // RN(1/6)
+    double q = __dmul_rn(s, r);
+    const double e = __fma_rn(-q, 6.0, s);  // exact remainder
+    q = __fma_rn(e, r, q);
+    const double a = fabs(s);
+    if ((a < 0x1p-1019 && a != 0.0) || !(a <= 0x1p1000)) q = __ddiv_rn(s, 6.0);
+    return q;
+#endif
+}
+
+__device__ __forceinline__ double sum6(double xm, double xp, double ym, double yp, double zm,
+                                       double zp) {
+    double acc = __dadd_rn(xm, xp);
+    acc = __dadd_rn(acc, ym);
+    acc = __dadd_rn(acc, yp);
+    acc = __dadd_rn(acc, zm);
+    return __dadd_rn(acc, zp);
+}
+
+// non-negative doubles order like their bit patterns
+__device__ __forceinline__ void resid_max(unsigned long long* slot, double v) {
+    atomicMax(slot, (unsigned long long)__double_as_longlong(v));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+struct ChunkBufs {
+    double* b[2];
+};
+
+// ---------------------------------------------------------------------------
+// slab update: (X,Y,1) domains.  Chunk layout: element (i,j) of the ghosted
+// (ex+2, ey+2) chunk at base + origin + i*sx + j, with (1,1) 16-byte aligned
+// and sx even, so every interior row starts 16-byte aligned.
+//
+// CTA = SLAB_THREADS threads covering 2*SLAB_THREADS columns; each thread owns
+// two adjacent columns (one double2) and marches `rows` rows keeping the row
+// above/at/below in registers; rows are fetched SLAB_U at a time.
+
+constexpr int SLAB_THREADS = 128;
+constexpr int SLAB_COLS = 2 * SLAB_THREADS;
+constexpr int SLAB_U = 4;
+
+struct SlabArgs {
+    const ChunkBufs* chunks;
+    int parity;
+    int64_t ex, ey, sx, origin;
+    int64_t rows;          // rows per CTA tile
+    int64_t tiles_r, tiles_c;
+    unsigned long long* resid;  // nullable: L-inf residual slot for this step
+    double zghost;         // the two constant z ghosts (BOUNDARY)
+};
+
+__global__ void __launch_bounds__(SLAB_THREADS)
+slab_update_kernel(SlabArgs a) {
+    const int64_t per_chunk = a.tiles_r * a.tiles_c;
+    const int64_t t = blockIdx.x;
+    const int64_t c = t / per_chunk;
+    const int64_t rem = t - c * per_chunk;
+    const int64_t rb = rem / a.tiles_c;
+    const int64_t cb = rem - rb * a.tiles_c;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+
+    const double* __restrict__ u = a.chunks[c].b[a.parity] + a.origin;
+    double* __restrict__ w = a.chunks[c].b[a.parity ^ 1] + a.origin;
+
+    const int64_t j = 1 + cb * SLAB_COLS + 2 * tid;   // ghosted column of .x
+    const bool act = j <= a.ey;                       // .x is interior
+    const bool both = j + 1 <= a.ey;                  // .y is interior
+    const bool right_mem = (lane == 31) || (j + 2 > a.ey);  // next lane idle
+    const int64_t i0 = 1 + rb * a.rows;
+    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+    const double zg = a.zghost;
+
+    auto ld2 = [&](int64_t i) -> double2 {
+        return act ? __ldg(reinterpret_cast<const double2*>(u + i * a.sx + j))
+                   : make_double2(0.0, 0.0);
+    };
+    auto ldl = [&](int64_t i) -> double {
+        return (act && lane == 0) ? __ldg(u + i * a.sx + j - 1) : 0.0;
+    };
+    auto ldr = [&](int64_t i) -> double {
+        return (both && right_mem) ? __ldg(u + i * a.sx + j + 2) : 0.0;
+    };
+    // y-neighbours of a row: left of .x and right of .y
+    auto nbrs = [&](double2 v, double el, double er, double& lx, double& ry) {
+        double l = __shfl_up_sync(0xffffffffu, v.y, 1);
+        double r = __shfl_down_sync(0xffffffffu, v.x, 1);
+        lx = (lane == 0) ? el : l;
+        ry = right_mem ? er : r;
+    };
+
+    double2 up = ld2(i0 - 1);
+    double2 mid = ld2(i0);
+    double lx, ry;
+    {
+        double el = ldl(i0), er = ldr(i0);
+        nbrs(mid, el, er, lx, ry);
+    }
+    double rmax = 0.0;
+
+    for (int64_t i = i0; i <= i1; i += SLAB_U) {
+        double2 nb[SLAB_U];
+        double el[SLAB_U], er[SLAB_U];
+#pragma unroll
+        for (int k = 0; k < SLAB_U; ++k) {
+            const int64_t r = i + 1 + k;
+            if (r <= i1 + 1) {
+                nb[k] = ld2(r);
+                el[k] = ldl(r);
+                er[k] = ldr(r);
+            } else {
+                nb[k] = make_double2(0.0, 0.0);
+                el[k] = er[k] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SLAB_U; ++k) {
+            const int64_t r = i + k;
+            if (r > i1) break;  // uniform across the CTA
+            const double2 dn = nb[k];
+            if (act) {
+                double2 o;
+                o.x = div6(sum6(up.x, dn.x, lx, mid.y, zg, zg));
+                o.y = div6(sum6(up.y, dn.y, mid.x, ry, zg, zg));
+                double* dst = w + r * a.sx + j;
+                if (both) {
+                    *reinterpret_cast<double2*>(dst) = o;
+                    rmax = fmax(rmax, fmax(fabs(__dsub_rn(o.x, mid.x)), fabs(__dsub_rn(o.y, mid.y))));
+                } else {
+                    dst[0] = o.x;
+                    rmax = fmax(rmax, fabs(__dsub_rn(o.x, mid.x)));
+                }
+            }
+            double nlx, nry;
+            nbrs(dn, el[k], er[k], nlx, nry);
+            up = mid;
+            mid = dn;
+            lx = nlx;
+            ry = nry;
+        }
+    }
+
+    if (a.resid) {
+        __shared__ double red[SLAB_THREADS / 32];
+        rmax = warp_max(rmax);
+        if (lane == 0) red[tid >> 5] = rmax;
+        __syncthreads();
+        if (tid == 0) {
+            double m = red[0];
+#pragma unroll
+            for (int k = 1; k < SLAB_THREADS / 32; ++k) m = fmax(m, red[k]);
+            resid_max(a.resid, m);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// volume update: general (X,Y,Z) domains; element (i,j,k) at
+// base + origin + i*sx + j*sy + k.  Threads tile (j,k), march i.
+
+constexpr int VOL_TX = 32, VOL_TY = 4;
+
+struct VolArgs {
+    const ChunkBufs* chunks;
+    int parity;
+    int64_t ex, ey, ez, sx, sy, origin;
+    int64_t rows;
+    int64_t tiles_i, tiles_j, tiles_k;
+    unsigned long long* resid;
+};
+
+__global__ void __launch_bounds__(VOL_TX * VOL_TY)
+volume_update_kernel(VolArgs a) {
+    const int64_t per_chunk = a.tiles_i * a.tiles_j * a.tiles_k;
+    const int64_t t = blockIdx.x;
+    const int64_t c = t / per_chunk;
+    int64_t rem = t - c * per_chunk;
+    const int64_t ti = rem / (a.tiles_j * a.tiles_k);
+    rem -= ti * a.tiles_j * a.tiles_k;
+    const int64_t tj = rem / a.tiles_k;
+    const int64_t tk = rem - tj * a.tiles_k;
+
+    const double* __restrict__ u = a.chunks[c].b[a.parity] + a.origin;
+    double* __restrict__ w = a.chunks[c].b[a.parity ^ 1] + a.origin;
+    const int64_t k = 1 + tk * VOL_TX + threadIdx.x;
+    const int64_t j = 1 + tj * VOL_TY + threadIdx.y;
+    const bool act = (k <= a.ez) && (j <= a.ey);
+    const int64_t i0 = 1 + ti * a.rows;
+    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+    double rmax = 0.0;
+    if (act) {
+        const int64_t col = j * a.sy + k;
+        double up = __ldg(u + (i0 - 1) * a.sx + col);
+        double mid = __ldg(u + i0 * a.sx + col);
+        for (int64_t i = i0; i <= i1; ++i) {
+            const double* p = u + i * a.sx + col;
+            const double dn = __ldg(p + a.sx);
+            const double nv = div6(sum6(up, dn, __ldg(p - a.sy), __ldg(p + a.sy), __ldg(p - 1),
+                                        __ldg(p + 1)));
+            w[i * a.sx + col] = nv;
+            rmax = fmax(rmax, fabs(__dsub_rn(nv, mid)));
+            up = mid;
+            mid = dn;
+        }
+    }
+    if (a.resid) {
+        __shared__ double red[VOL_TX * VOL_TY / 32];
+        const int tid = threadIdx.y * VOL_TX + threadIdx.x;
+        rmax = warp_max(rmax);
+        if ((tid & 31) == 0) red[tid >> 5] = rmax;
+        __syncthreads();
+        if (tid == 0) {
+            double m = red[0];
+            for (int q = 1; q < VOL_TX * VOL_TY / 32; ++q) m = fmax(m, red[q]);
+            resid_max(a.resid, m);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// halo plane copies: dst[o*ds0 + i*ds1] = src[o*ss0 + i*ss1] for every
+// segment.  One launch per step moves every face of every chunk on the GPU:
+// same-GPU faces read the neighbour's boundary plane in place, peer faces
+// read it over NVLink, remote (NCCL) faces pack/unpack staging buffers.
+
+constexpr int HALO_THREADS = 256;
+constexpr int HALO_PER_THREAD = 4;
+
+__global__ void __launch_bounds__(HALO_THREADS)
+halo_copy_kernel(const hrt_halo_seg_t* __restrict__ segs, int parity, int64_t blocks_per_seg) {
+    const int64_t s = blockIdx.x / blocks_per_seg;
+    const int64_t b = blockIdx.x - s * blocks_per_seg;
+    const hrt_halo_seg_t g = segs[s];
+    const double* __restrict__ src = reinterpret_cast<const double*>(g.src[parity]);
+    double* __restrict__ dst = reinterpret_cast<double*>(g.dst[parity]);
+    const int64_t n = g.n0 * g.n1;
+    const int64_t stride = blocks_per_seg * HALO_THREADS;
+    for (int64_t e = b * HALO_THREADS + threadIdx.x; e < n; e += stride) {
+        const int64_t o = e / g.n1, i = e - o * g.n1;
+        dst[o * g.ds0 + i * g.ds1] = src[o * g.ss0 + i * g.ss1];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ghost initialisation: set the ghost shell of a chunk buffer to `value`
+// for faces in `mask` (bit f = face f of jacobi.py:41 FACES) and 0 elsewhere.
+
+__global__ void ghost_fill_kernel(double* __restrict__ base, int64_t origin, int64_t ex,
+                                  int64_t ey, int64_t ez, int64_t sx, int64_t sy, int ndim,
+                                  int mask, double value) {
+    // iterate over the full ghosted box; write only ghost cells
+    const int64_t gx = ex + 2, gy = ey + 2, gz = (ndim == 3) ? ez + 2 : 1;
+    const int64_t n = gx * gy * gz;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / (gy * gz);
+        const int64_t r = e - i * gy * gz;
+        const int64_t jj = r / gz;
+        const int64_t kk = r - jj * gz;
+        int face = -1;
+        if (i == 0) face = 0;
+        else if (i == gx - 1) face = 1;
+        else if (jj == 0) face = 2;
+        else if (jj == gy - 1) face = 3;
+        else if (ndim == 3 && kk == 0) face = 4;
+        else if (ndim == 3 && kk == gz - 1) face = 5;
+        if (face < 0) continue;
+        // a ghost cell on several faces (edges/corners) is never read by the
+        // 7-point stencil; give it the value of any domain face it touches
+        bool dom = (mask >> face) & 1;
+        if (!dom) {
+            dom = ((i == 0) && (mask & 1)) || ((i == gx - 1) && (mask & 2)) ||
+                  ((jj == 0) && (mask & 4)) || ((jj == gy - 1) && (mask & 8)) ||
+                  (ndim == 3 && kk == 0 && (mask & 16)) ||
+                  (ndim == 3 && kk == gz - 1 && (mask & 32));
+        }
+        base[origin + i * sx + jj * sy + kk] = dom ? value : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact float(np.sum(a)): numpy's pairwise summation (PW_BLOCKSIZE 128, eight
+// partial sums), evaluated as one CTA per subtree of <= SEG elements; the top
+// of the recursion tree is combined on the host in the same order.
+
+constexpr int PW_SEG = 16384;
+constexpr int PW_THREADS = 256;
+constexpr int PW_MAX_LEAVES = 512;
+
+__device__ double pw_leaf(const double* a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = a[q];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], a[i + q]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+// enumerate leaves (n <= 128) of the subtree rooted at (off, n) in order
+__device__ void pw_leaves(int64_t off, int64_t n, int64_t* lo, int64_t* ln, int* cnt) {
+    // explicit stack: depth <= log2(PW_SEG/64)+1
+    int64_t so[32], sn[32];
+    int sp = 0;
+    so[sp] = off;
+    sn[sp] = n;
+    ++sp;
+    while (sp) {
+        --sp;
+        int64_t o = so[sp], m = sn[sp];
+        if (m <= 128) {
+            lo[*cnt] = o;
+            ln[*cnt] = m;
+            ++*cnt;
+        } else {
+            int64_t m2 = m / 2;
+            m2 -= m2 % 8;
+            // push right first so the left subtree is visited first
+            so[sp] = o + m2; sn[sp] = m - m2; ++sp;
+            so[sp] = o; sn[sp] = m2; ++sp;
+        }
+    }
+}
+
+__device__ double pw_combine(int64_t n, const double* leaf, int* next) {
+    if (n <= 128) return leaf[(*next)++];
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    double l = pw_combine(n2, leaf, next);
+    double r = pw_combine(n - n2, leaf, next);
+    return __dadd_rn(l, r);
+}
+
+__global__ void __launch_bounds__(PW_THREADS)
+pairwise_seg_kernel(const double* __restrict__ a, const int64_t* __restrict__ seg_off,
+                    const int64_t* __restrict__ seg_len, double* __restrict__ out) {
+    __shared__ int64_t lo[PW_MAX_LEAVES], ln[PW_MAX_LEAVES];
+    __shared__ double leaf[PW_MAX_LEAVES];
+    __shared__ int cnt;
+    const int64_t off = seg_off[blockIdx.x], n = seg_len[blockIdx.x];
+    if (threadIdx.x == 0) {
+        cnt = 0;
+        pw_leaves(off, n, lo, ln, &cnt);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < cnt; q += PW_THREADS) leaf[q] = pw_leaf(a + lo[q], ln[q]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int next = 0;
+        out[blockIdx.x] = pw_combine(n, leaf, &next);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// division self-check: Markstein div6 vs IEEE on a counter-hashed sweep
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return x;
+}
+
+__global__ void div6_sweep_kernel(uint64_t seed, int64_t n, int mode,
+                                  unsigned long long* mismatches, double* first_bad) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t h = mix64(seed + (uint64_t)e * 0x9e3779b97f4a7c15ULL);
+        double x;
+        if (mode == 0) {  // uniform [0, 6): the Jacobi range of a six-term sum
+            x = (double)(h >> 11) * 0x1p-53 * 6.0;
+        } else if (mode == 1) {  // doubles within 2^-40 of 1.0 and of 6.0, 3.0
+            const double centre = (h & 3) == 0 ? 1.0 : ((h & 3) == 1 ? 6.0 : ((h & 3) == 2 ? 3.0 : 2.0));
+            x = centre + ((double)((int64_t)(h >> 24) - (int64_t)(1ULL << 39)) * 0x1p-80);
+        } else {  // random finite bit patterns, positive
+            uint64_t bits = h & 0x7fffffffffffffffULL;
+            x = __longlong_as_double((long long)bits);
+            if (!(fabs(x) <= 0x1p1000)) x = 1.0;
+        }
+        const double q = div6(x);
+        const double ref = __ddiv_rn(x, 6.0);
+        if (__double_as_longlong(q) != __double_as_longlong(ref)) {
+            unsigned long long k = atomicAdd(mismatches, 1ULL);
+            if (k == 0) *first_bad = x;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// plan: the per-GPU step engine
+
+struct Plan {
+    int gpu;
+    hrt_chunk_layout_t L;
+    int nchunks;
+    ChunkBufs* d_chunks = nullptr;
+    std::vector<ChunkBufs> h_chunks;
+    hrt_halo_seg_t* d_segs = nullptr;
+    int nsegs = 0;
+    int64_t seg_blocks = 1;
+    hrt_halo_seg_t* d_post = nullptr;
+    int npost = 0;
+    int64_t post_blocks = 1;
+    std::vector<hrt_remote_seg_t> remote;
+    void* comm = nullptr;
+    int64_t rows = 64;
+    // graph of two steps (parity 0 then 1) per residual base pointer
+    cudaGraphExec_t graph = nullptr;
+    unsigned long long* graph_resid = nullptr;
+    cudaStream_t graph_stream = nullptr;
+};
+
+static int64_t blocks_for(const hrt_halo_seg_t* segs, int n) {
+    int64_t mx = 1;
+    for (int i = 0; i < n; ++i) mx = std::max<int64_t>(mx, segs[i].n0 * segs[i].n1);
+    return std::max<int64_t>(1, (mx + HALO_THREADS * HALO_PER_THREAD - 1) /
+                                    (HALO_THREADS * HALO_PER_THREAD));
+}
+
+}  // namespace hrt
+
+using namespace hrt;
+
+// NCCL hooks (hrt_nccl.cu)
+extern "C" int hrt_nccl_exchange(void* comm, void* stream, const hrt_remote_seg_t* segs, int n,
+                                 int parity);
+
+static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long* resid) {
+    const hrt_chunk_layout_t& L = p->L;
+    if (L.ndim == 2) {
+        SlabArgs a;
+        a.chunks = p->d_chunks;
+        a.parity = parity;
+        a.ex = L.ext[0];
+        a.ey = L.ext[1];
+        a.sx = L.stride[0];
+        a.origin = L.origin;
+        a.rows = p->rows;
+        a.tiles_r = (a.ex + a.rows - 1) / a.rows;
+        a.tiles_c = (a.ey + SLAB_COLS - 1) / SLAB_COLS;
+        a.resid = resid;
+        a.zghost = HRT_BOUNDARY;
+        const int64_t grid = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
+        if (grid == 0) return HRT_OK;
+        slab_update_kernel<<<(unsigned)grid, SLAB_THREADS, 0, s>>>(a);
+    } else {
+        VolArgs a;
+        a.chunks = p->d_chunks;
+        a.parity = parity;
+        a.ex = L.ext[0];
+        a.ey = L.ext[1];
+        a.ez = L.ext[2];
+        a.sx = L.stride[0];
+        a.sy = L.stride[1];
+        a.origin = L.origin;
+        a.rows = p->rows;
+        a.tiles_i = (a.ex + a.rows - 1) / a.rows;
+        a.tiles_j = (a.ey + VOL_TY - 1) / VOL_TY;
+        a.tiles_k = (a.ez + VOL_TX - 1) / VOL_TX;
+        a.resid = resid;
+        const int64_t grid = (int64_t)p->nchunks * a.tiles_i * a.tiles_j * a.tiles_k;
+        if (grid == 0) return HRT_OK;
+        volume_update_kernel<<<(unsigned)grid, dim3(VOL_TX, VOL_TY), 0, s>>>(a);
+    }
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
+static int launch_halo(Plan* p, cudaStream_t s, int parity) {
+    if (p->nsegs > 0) {
+        halo_copy_kernel<<<(unsigned)(p->nsegs * p->seg_blocks), HALO_THREADS, 0, s>>>(
+            p->d_segs, parity, p->seg_blocks);
+        HRT_CUDA(cudaGetLastError());
+    }
+    if (!p->remote.empty()) {
+        Stream tmp;
+        tmp.s = s;
+        tmp.gpu = p->gpu;
+        int rc = hrt_nccl_exchange(p->comm, &tmp, p->remote.data(), (int)p->remote.size(), parity);
+        if (rc) return rc;
+        if (p->npost > 0) {
+            halo_copy_kernel<<<(unsigned)(p->npost * p->post_blocks), HALO_THREADS, 0, s>>>(
+                p->d_post, parity, p->post_blocks);
+            HRT_CUDA(cudaGetLastError());
+        }
+    }
+    return HRT_OK;
+}
+
+static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
+    const int parity = (int)(step & 1);
+    int rc = launch_halo(p, s, parity);
+    if (rc) return rc;
+    return launch_update(p, s, parity, resid_base ? resid_base + step : nullptr);
+}
+
+extern "C" {
+
+int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunks,
+                           const uint64_t* bufs, const hrt_halo_seg_t* segs, int nsegs,
+                           void** plan) {
+    HRT_CHECK_ARG(layout && plan && (nchunks == 0 || bufs) && (nsegs == 0 || segs),
+                  "null plan argument");
+    HRT_CHECK_ARG(layout->ndim == 2 || layout->ndim == 3, "layout.ndim must be 2 or 3");
+    if (layout->ndim == 2) {
+        HRT_CHECK_ARG(layout->stride[1] == 1, "slab layout needs unit y stride");
+        HRT_CHECK_ARG(layout->stride[0] % 2 == 0 && (layout->origin + 1) % 2 == 0,
+                      "slab layout: interior rows must start 16-byte aligned");
+        for (int c = 0; c < nchunks; ++c)
+            for (int b = 0; b < 2; ++b)
+                HRT_CHECK_ARG(bufs[2 * c + b] % 16 == 0, "chunk buffers must be 16-byte aligned");
+    } else {
+        HRT_CHECK_ARG(layout->stride[2] == 1, "volume layout needs unit z stride");
+    }
+    int rc = use_device(gpu);
+    if (rc) return rc;
+    Plan* p = new Plan();
+    p->gpu = gpu;
+    p->L = *layout;
+    p->nchunks = nchunks;
+    p->h_chunks.resize(nchunks);
+    for (int c = 0; c < nchunks; ++c) {
+        p->h_chunks[c].b[0] = reinterpret_cast<double*>(bufs[2 * c]);
+        p->h_chunks[c].b[1] = reinterpret_cast<double*>(bufs[2 * c + 1]);
+    }
+    cudaError_t e = cudaSuccess;
+    if (nchunks) {
+        e = cudaMalloc(&p->d_chunks, sizeof(ChunkBufs) * nchunks);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p->d_chunks, p->h_chunks.data(), sizeof(ChunkBufs) * nchunks,
+                           cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess && nsegs) {
+        e = cudaMalloc(&p->d_segs, sizeof(hrt_halo_seg_t) * nsegs);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p->d_segs, segs, sizeof(hrt_halo_seg_t) * nsegs, cudaMemcpyHostToDevice);
+        p->nsegs = nsegs;
+        p->seg_blocks = blocks_for(segs, nsegs);
+    }
+    if (e != cudaSuccess) {
+        cudaFree(p->d_chunks);
+        cudaFree(p->d_segs);
+        delete p;
+        return cuda_fail(e, "plan tables");
+    }
+    // rows per CTA: enough CTAs to fill the GPU several times over
+    p->rows = layout->ndim == 2 ? 64 : 16;
+    *plan = p;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_rows(void* plan, int64_t rows) {
+    HRT_CHECK_ARG(plan && rows > 0, "bad rows");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    p->rows = rows;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_remote(void* plan, void* comm, const hrt_remote_seg_t* remote,
+                               int nremote, const hrt_halo_seg_t* post, int npost) {
+    HRT_CHECK_ARG(plan, "null plan");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    p->comm = comm;
+    p->remote.assign(remote, remote + nremote);
+    cudaFree(p->d_post);
+    p->d_post = nullptr;
+    p->npost = 0;
+    if (npost) {
+        HRT_CUDA(cudaMalloc(&p->d_post, sizeof(hrt_halo_seg_t) * npost));
+        HRT_CUDA(cudaMemcpy(p->d_post, post, sizeof(hrt_halo_seg_t) * npost,
+                            cudaMemcpyHostToDevice));
+        p->npost = npost;
+        p->post_blocks = blocks_for(post, npost);
+    }
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_step(void* plan, void* stream, int64_t step, uint64_t* resid) {
+    HRT_CHECK_ARG(plan && stream, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    return do_step(p, as_stream(stream)->s, step, reinterpret_cast<unsigned long long*>(resid));
+}
+
+int hrt_jacobi_plan_update(void* plan, void* stream, int parity, uint64_t* resid_slot) {
+    HRT_CHECK_ARG(plan && stream, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    return launch_update(p, as_stream(stream)->s, parity & 1,
+                         reinterpret_cast<unsigned long long*>(resid_slot));
+}
+
+int hrt_jacobi_plan_halo(void* plan, void* stream, int parity) {
+    HRT_CHECK_ARG(plan && stream, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    return launch_halo(p, as_stream(stream)->s, parity & 1);
+}
+
+// Run steps [first, first+n).  mode 0: direct launches; mode 1: replay a
+// captured two-step CUDA graph (the residual slot advances with the step, so
+// with a residual the graph is re-instantiated per pair — use mode 0 then).
+int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint64_t* resid,
+                        int mode) {
+    HRT_CHECK_ARG(plan && stream && n >= 0, "bad run arguments");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream)->s;
+    unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
+    if (mode == 0 || r != nullptr) {
+        for (int64_t k = 0; k < n; ++k) {
+            rc = do_step(p, s, first + k, r);
+            if (rc) return rc;
+        }
+        return HRT_OK;
+    }
+    int64_t k = 0;
+    if (first & 1) {  // align to an even step
+        rc = do_step(p, s, first, nullptr);
+        if (rc) return rc;
+        k = 1;
+    }
+    if (n - k >= 2) {
+        if (!p->graph || p->graph_stream != s) {
+            if (p->graph) cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+            cudaGraph_t g;
+            HRT_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            int rc0 = do_step(p, s, 0, nullptr);
+            int rc1 = rc0 ? rc0 : do_step(p, s, 1, nullptr);
+            cudaError_t e = cudaStreamEndCapture(s, &g);
+            if (rc1) return rc1;
+            HRT_CUDA(e);
+            e = cudaGraphInstantiate(&p->graph, g, 0);
+            cudaGraphDestroy(g);
+            HRT_CUDA(e);
+            p->graph_stream = s;
+        }
+        for (; k + 2 <= n; k += 2) HRT_CUDA(cudaGraphLaunch(p->graph, s));
+    }
+    for (; k < n; ++k) {
+        rc = do_step(p, s, first + k, nullptr);
+        if (rc) return rc;
+    }
+    return HRT_OK;
+}
+
+// Steps [first, first+n) with CUDA events bracketing every update and halo
+// launch on `stream`; returns the summed device durations.  Synchronises.
+int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n, uint64_t* resid,
+                              double* update_ms, double* halo_ms, double* total_ms) {
+    HRT_CHECK_ARG(plan && stream && n >= 0, "bad run arguments");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    cudaStream_t s = as_stream(stream)->s;
+    unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
+    std::vector<cudaEvent_t> ev(3 * n + 1);
+    for (auto& x : ev) HRT_CUDA(cudaEventCreate(&x));
+    HRT_CUDA(cudaEventRecord(ev[0], s));
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t step = first + k;
+        const int parity = (int)(step & 1);
+        rc = launch_halo(p, s, parity);
+        if (rc) break;
+        HRT_CUDA(cudaEventRecord(ev[3 * k + 1], s));
+        rc = launch_update(p, s, parity, r ? r + step : nullptr);
+        if (rc) break;
+        HRT_CUDA(cudaEventRecord(ev[3 * k + 2], s));
+        HRT_CUDA(cudaEventRecord(ev[3 * k + 3], s));
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    double up = 0, ha = 0;
+    float ms = 0;
+    if (!rc && e == cudaSuccess) {
+        for (int64_t k = 0; k < n; ++k) {
+            cudaEventElapsedTime(&ms, ev[3 * k + 1], ev[3 * k + 2]);
+            up += ms;
+            cudaEventElapsedTime(&ms, k ? ev[3 * k] : ev[0], ev[3 * k + 1]);
+            ha += ms;
+        }
+        cudaEventElapsedTime(&ms, ev[0], ev[3 * n]);
+    }
+    for (auto& x : ev) cudaEventDestroy(x);
+    if (rc) return rc;
+    HRT_CUDA(e);
+    if (update_ms) *update_ms = up;
+    if (halo_ms) *halo_ms = ha;
+    if (total_ms) *total_ms = n ? ms : 0.0;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_destroy(void* plan) {
+    if (!plan) return HRT_OK;
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    use_device(p->gpu);
+    if (p->graph) cudaGraphExecDestroy(p->graph);
+    cudaFree(p->d_chunks);
+    cudaFree(p->d_segs);
+    cudaFree(p->d_post);
+    delete p;
+    return HRT_OK;
+}
+
+// Standalone plane copies (the reference's halo_pack_f / halo_unpack_f
+// bodies, jacobi.py:102-124, and any generic strided copy).
+int hrt_halo_copy(void* stream, const hrt_halo_seg_t* segs_dev, int nsegs, int parity,
+                  int64_t max_elems) {
+    HRT_CHECK_ARG(stream && (nsegs == 0 || segs_dev), "null argument");
+    if (nsegs == 0) return HRT_OK;
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    int64_t bps = std::max<int64_t>(
+        1, (max_elems + HALO_THREADS * HALO_PER_THREAD - 1) / (HALO_THREADS * HALO_PER_THREAD));
+    halo_copy_kernel<<<(unsigned)(nsegs * bps), HALO_THREADS, 0, st->s>>>(segs_dev, parity & 1, bps);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_jacobi_ghost_fill(void* stream, double* base, const hrt_chunk_layout_t* L, int mask,
+                          double value) {
+    HRT_CHECK_ARG(stream && base && L, "null argument");
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    const int64_t n = (L->ext[0] + 2) * (L->ext[1] + 2) * (L->ndim == 3 ? L->ext[2] + 2 : 1);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    ghost_fill_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st->s>>>(
+        base, L->origin, L->ext[0], L->ext[1], L->ext[2], L->stride[0], L->stride[1], L->ndim,
+        mask, value);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
+// float(np.sum(a)) of n contiguous device doubles, bit-exact with numpy.
+// Synchronises `stream`.
+int hrt_np_sum(void* stream, const double* a, int64_t n, double* out) {
+    HRT_CHECK_ARG(stream && out && (n == 0 || a), "null argument");
+    if (n == 0) {
+        *out = 0.0;
+        return HRT_OK;
+    }
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    // top of the tree on the host: subtrees of <= PW_SEG elements are leaves
+    std::vector<int64_t> off, len;
+    std::vector<std::pair<int64_t, int64_t>> stack{{0, n}};
+    while (!stack.empty()) {
+        auto [o, m] = stack.back();
+        stack.pop_back();
+        if (m <= PW_SEG) {
+            off.push_back(o);
+            len.push_back(m);
+        } else {
+            int64_t m2 = m / 2;
+            m2 -= m2 % 8;
+            stack.push_back({o + m2, m - m2});
+            stack.push_back({o, m2});
+        }
+    }
+    const size_t ns = off.size();
+    int64_t* d_tab = nullptr;
+    double* d_out = nullptr;
+    HRT_CUDA(cudaMallocAsync(&d_tab, sizeof(int64_t) * 2 * ns, st->s));
+    HRT_CUDA(cudaMallocAsync(&d_out, sizeof(double) * ns, st->s));
+    std::vector<int64_t> tab(2 * ns);
+    std::copy(off.begin(), off.end(), tab.begin());
+    std::copy(len.begin(), len.end(), tab.begin() + ns);
+    HRT_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(int64_t) * 2 * ns, cudaMemcpyHostToDevice,
+                             st->s));
+    pairwise_seg_kernel<<<(unsigned)ns, PW_THREADS, 0, st->s>>>(a, d_tab, d_tab + ns, d_out);
+    cudaError_t le = cudaGetLastError();
+    std::vector<double> seg(ns);
+    HRT_CUDA(cudaMemcpyAsync(seg.data(), d_out, sizeof(double) * ns, cudaMemcpyDeviceToHost, st->s));
+    cudaFreeAsync(d_tab, st->s);
+    cudaFreeAsync(d_out, st->s);
+    HRT_CUDA(cudaStreamSynchronize(st->s));
+    HRT_CUDA(le);
+    // combine with the same recursion
+    size_t next = 0;
+    struct Rec {
+        static double go(int64_t m, const std::vector<double>& s, size_t& i) {
+            if (m <= PW_SEG) return s[i++];
+            int64_t m2 = m / 2;
+            m2 -= m2 % 8;
+            volatile double l = go(m2, s, i);
+            volatile double r = go(m - m2, s, i);
+            return l + r;
+        }
+    };
+    volatile double total = Rec::go(n, seg, next);
+    *out = 0.0 + total;
+    return HRT_OK;
+}
+
+int hrt_div6_sweep(void* stream, uint64_t seed, int64_t n, int mode, uint64_t* mismatches,
+                   double* first_bad) {
+    HRT_CHECK_ARG(stream && mismatches, "null argument");
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    unsigned long long* d_cnt = nullptr;
+    double* d_bad = nullptr;
+    HRT_CUDA(cudaMallocAsync(&d_cnt, sizeof(unsigned long long), st->s));
+    HRT_CUDA(cudaMallocAsync(&d_bad, sizeof(double), st->s));
+    HRT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), st->s));
+    HRT_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(double), st->s));
+    div6_sweep_kernel<<<148 * 8, 256, 0, st->s>>>(seed, n, mode, d_cnt, d_bad);
+    cudaError_t le = cudaGetLastError();
+    unsigned long long cnt = 0;
+    double bad = 0;
+    HRT_CUDA(cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, st->s));
+    HRT_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st->s));
+    cudaFreeAsync(d_cnt, st->s);
+    cudaFreeAsync(d_bad, st->s);
+    HRT_CUDA(cudaStreamSynchronize(st->s));
+    HRT_CUDA(le);
+    *mismatches = cnt;
+    if (first_bad) *first_bad = bad;
+    return HRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,528 @@
+// libhrt_b200 — device layer: first-fit pools over HBM arenas, CUDA streams,
+// cudaEvent-backed completion tokens and asynchronous copies (H2D, D2H, D2D
+// and peer).  This replaces the reference's simulated device layer
+// (/root/reference/pkg/src/hrt/devices.py): FreeListAllocator (89-154),
+// DeviceBackend.attach/region (285-308), CompletionToken (199-222) and
+// DeviceRegistry.enqueue_transfer (446-496), whose D2D rejection
+// (devices.py:456-457) is lifted here.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "hrt_common.cuh"
+
+namespace hrt {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // clear the sticky-free allocation error
+        return HRT_E_OOM;
+    }
+    return HRT_E_CUDA;
+}
+
+int use_device(int gpu) {
+    int cur = -1;
+    HRT_CUDA(cudaGetDevice(&cur));
+    if (cur != gpu) HRT_CUDA(cudaSetDevice(gpu));
+    return HRT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// First-fit free list (FreeListAllocator, devices.py:89-154): address-ordered
+// free blocks, sizes rounded up to the alignment, first fit, coalescing with
+// the successor and then the predecessor on free.
+
+struct FreeList {
+    uint64_t capacity, alignment;
+    std::map<uint64_t, uint64_t> free_blocks;  // offset -> size (address order)
+    std::unordered_map<uint64_t, uint64_t> live;
+    std::mutex mu;
+
+    FreeList(uint64_t cap, uint64_t align) : capacity(cap), alignment(align) {
+        free_blocks[0] = cap;
+    }
+
+    int alloc(uint64_t size, uint64_t* off, uint64_t* granted) {
+        if (size == 0) {
+            set_error("allocation size must be positive, got 0");
+            return HRT_E_INVALID;
+        }
+        uint64_t need = (size + alignment - 1) / alignment * alignment;
+        std::lock_guard<std::mutex> g(mu);
+        for (auto it = free_blocks.begin(); it != free_blocks.end(); ++it) {
+            if (it->second >= need) {
+                uint64_t o = it->first, avail = it->second;
+                free_blocks.erase(it);
+                if (avail > need) free_blocks[o + need] = avail - need;
+                live[o] = need;
+                *off = o;
+                *granted = need;
+                return HRT_OK;
+            }
+        }
+        set_error("no free block fits %llu bytes", (unsigned long long)need);
+        return HRT_E_OOM;
+    }
+
+    int free(uint64_t off, uint64_t* size_out) {
+        std::lock_guard<std::mutex> g(mu);
+        auto lv = live.find(off);
+        if (lv == live.end()) {
+            set_error("offset %llu is not a live allocation", (unsigned long long)off);
+            return HRT_E_DOUBLE_FREE;
+        }
+        uint64_t size = lv->second;
+        live.erase(lv);
+        if (size_out) *size_out = size;
+        auto it = free_blocks.emplace(off, size).first;
+        auto nx = std::next(it);
+        if (nx != free_blocks.end() && off + size == nx->first) {
+            it->second += nx->second;
+            free_blocks.erase(nx);
+        }
+        if (it != free_blocks.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second == off) {
+                pv->second += it->second;
+                free_blocks.erase(it);
+            }
+        }
+        return HRT_OK;
+    }
+
+    void stats(uint64_t* lb, uint64_t* fb, uint64_t* nb) {
+        std::lock_guard<std::mutex> g(mu);
+        uint64_t l = 0, f = 0;
+        for (auto& kv : live) l += kv.second;
+        for (auto& kv : free_blocks) f += kv.second;
+        if (lb) *lb = l;
+        if (fb) *fb = f;
+        if (nb) *nb = free_blocks.size();
+    }
+
+    int check() {
+        std::lock_guard<std::mutex> g(mu);
+        std::vector<std::pair<uint64_t, uint64_t>> spans;
+        uint64_t total = 0;
+        for (auto& kv : live) { spans.push_back({kv.first, kv.first + kv.second}); total += kv.second; }
+        for (auto& kv : free_blocks) { spans.push_back({kv.first, kv.first + kv.second}); total += kv.second; }
+        if (total != capacity) {
+            set_error("live + free = %llu != capacity %llu", (unsigned long long)total,
+                      (unsigned long long)capacity);
+            return HRT_E_INVALID;
+        }
+        std::sort(spans.begin(), spans.end());
+        for (size_t i = 1; i < spans.size(); ++i)
+            if (spans[i - 1].second > spans[i].first) {
+                set_error("overlapping regions at %llu", (unsigned long long)spans[i].first);
+                return HRT_E_INVALID;
+            }
+        return HRT_OK;
+    }
+};
+
+struct Pool {
+    int gpu;
+    void* base;
+    FreeList fl;
+    Pool(int g, void* b, uint64_t cap) : gpu(g), base(b), fl(cap, HRT_ALIGNMENT) {}
+};
+
+// ---------------------------------------------------------------------------
+// Completion tokens: one cudaEvent each, recycled through a per-device pool.
+
+struct Token {
+    cudaEvent_t ev;
+    int gpu;
+};
+
+static std::mutex g_tok_mu;
+static std::unordered_map<uint64_t, Token> g_tokens;
+static std::unordered_map<int, std::vector<cudaEvent_t>> g_event_pool;
+static uint64_t g_next_token = 0;
+
+static int take_event(int gpu, unsigned flags, cudaEvent_t* ev) {
+    {
+        std::lock_guard<std::mutex> g(g_tok_mu);
+        auto& v = g_event_pool[gpu * 4 + (flags == cudaEventDefault ? 0 : 1)];
+        if (!v.empty()) {
+            *ev = v.back();
+            v.pop_back();
+            return HRT_OK;
+        }
+    }
+    HRT_CUDA(cudaEventCreateWithFlags(ev, flags));
+    return HRT_OK;
+}
+
+}  // namespace hrt
+
+using namespace hrt;
+
+extern "C" {
+
+const char* hrt_last_error(void) { return hrt::g_err; }
+
+int hrt_version(void) { return HRT_ABI_VERSION; }
+
+int hrt_device_count(int* n) {
+    HRT_CHECK_ARG(n, "null out pointer");
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+        *n = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    return HRT_OK;
+}
+
+int hrt_device_info(int gpu, char* name, int name_len, int* sm_count, uint64_t* hbm_bytes,
+                    int* cc_major, int* cc_minor) {
+    cudaDeviceProp p;
+    HRT_CUDA(cudaGetDeviceProperties(&p, gpu));
+    if (name && name_len > 0) snprintf(name, name_len, "%s", p.name);
+    if (sm_count) *sm_count = p.multiProcessorCount;
+    if (hbm_bytes) *hbm_bytes = p.totalGlobalMem;
+    if (cc_major) *cc_major = p.major;
+    if (cc_minor) *cc_minor = p.minor;
+    return HRT_OK;
+}
+
+int hrt_enable_peer_access(int gpu, int peer) {
+    if (gpu == peer) return HRT_OK;
+    int can = 0;
+    HRT_CUDA(cudaDeviceCanAccessPeer(&can, gpu, peer));
+    if (!can) {
+        set_error("device %d cannot access peer %d", gpu, peer);
+        return HRT_E_UNSUPPORTED;
+    }
+    int rc = use_device(gpu);
+    if (rc) return rc;
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return HRT_OK;
+    }
+    HRT_CUDA(e);
+    return HRT_OK;
+}
+
+// ---- first-fit allocator (host logic) ----
+
+int hrt_fl_create(uint64_t capacity, uint64_t alignment, void** fl) {
+    HRT_CHECK_ARG(fl, "null out pointer");
+    HRT_CHECK_ARG(capacity > 0, "allocator capacity must be positive");
+    HRT_CHECK_ARG(alignment > 0 && (alignment & (alignment - 1)) == 0,
+                  "alignment must be a power of two");
+    *fl = new FreeList(capacity, alignment);
+    return HRT_OK;
+}
+
+int hrt_fl_alloc(void* fl, uint64_t size, uint64_t* offset, uint64_t* granted) {
+    HRT_CHECK_ARG(fl && offset && granted, "null argument");
+    return reinterpret_cast<FreeList*>(fl)->alloc(size, offset, granted);
+}
+
+int hrt_fl_free(void* fl, uint64_t offset, uint64_t* size) {
+    HRT_CHECK_ARG(fl, "null allocator");
+    return reinterpret_cast<FreeList*>(fl)->free(offset, size);
+}
+
+int hrt_fl_stats(void* fl, uint64_t* live_bytes, uint64_t* free_bytes, uint64_t* free_blocks) {
+    HRT_CHECK_ARG(fl, "null allocator");
+    reinterpret_cast<FreeList*>(fl)->stats(live_bytes, free_bytes, free_blocks);
+    return HRT_OK;
+}
+
+int hrt_fl_check(void* fl) {
+    HRT_CHECK_ARG(fl, "null allocator");
+    return reinterpret_cast<FreeList*>(fl)->check();
+}
+
+void hrt_fl_destroy(void* fl) { delete reinterpret_cast<FreeList*>(fl); }
+
+// ---- device pools ----
+
+int hrt_pool_create(int gpu, uint64_t capacity, void** pool) {
+    HRT_CHECK_ARG(pool && capacity > 0, "bad pool arguments");
+    int rc = use_device(gpu);
+    if (rc) return rc;
+    void* base = nullptr;
+    HRT_CUDA(cudaMalloc(&base, capacity));
+    *pool = new Pool(gpu, base, capacity);
+    return HRT_OK;
+}
+
+int hrt_pool_alloc(void* pool, uint64_t size, uint64_t* offset, uint64_t* granted, void** dptr) {
+    HRT_CHECK_ARG(pool && offset && granted, "null argument");
+    Pool* p = reinterpret_cast<Pool*>(pool);
+    int rc = p->fl.alloc(size, offset, granted);
+    if (rc) return rc;
+    if (dptr) *dptr = static_cast<char*>(p->base) + *offset;
+    return HRT_OK;
+}
+
+int hrt_pool_free(void* pool, uint64_t offset) {
+    HRT_CHECK_ARG(pool, "null pool");
+    return reinterpret_cast<Pool*>(pool)->fl.free(offset, nullptr);
+}
+
+int hrt_pool_stats(void* pool, uint64_t* live_bytes, uint64_t* free_bytes) {
+    HRT_CHECK_ARG(pool, "null pool");
+    reinterpret_cast<Pool*>(pool)->fl.stats(live_bytes, free_bytes, nullptr);
+    return HRT_OK;
+}
+
+int hrt_pool_base(void* pool, void** base) {
+    HRT_CHECK_ARG(pool && base, "null argument");
+    *base = reinterpret_cast<Pool*>(pool)->base;
+    return HRT_OK;
+}
+
+int hrt_pool_destroy(void* pool) {
+    if (!pool) return HRT_OK;
+    Pool* p = reinterpret_cast<Pool*>(pool);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    cudaError_t e = cudaFree(p->base);
+    delete p;
+    HRT_CUDA(e);
+    return HRT_OK;
+}
+
+// ---- streams ----
+
+int hrt_stream_create(int gpu, int priority, void** stream) {
+    HRT_CHECK_ARG(stream, "null out pointer");
+    int rc = use_device(gpu);
+    if (rc) return rc;
+    Stream* s = new Stream();
+    s->gpu = gpu;
+    cudaError_t e = cudaStreamCreateWithPriority(&s->s, cudaStreamNonBlocking, priority);
+    if (e != cudaSuccess) {
+        delete s;
+        return cuda_fail(e, "cudaStreamCreateWithPriority");
+    }
+    *stream = s;
+    return HRT_OK;
+}
+
+int hrt_stream_wrap(int gpu, void* cuda_stream, void** stream) {
+    HRT_CHECK_ARG(stream, "null out pointer");
+    Stream* s = new Stream();
+    s->gpu = gpu;
+    s->s = reinterpret_cast<cudaStream_t>(cuda_stream);
+    *stream = s;
+    return HRT_OK;
+}
+
+void* hrt_stream_handle(void* stream) { return stream ? as_stream(stream)->s : nullptr; }
+
+int hrt_stream_destroy(void* stream, int owned) {
+    if (!stream) return HRT_OK;
+    Stream* s = as_stream(stream);
+    cudaError_t e = cudaSuccess;
+    if (owned) {
+        use_device(s->gpu);
+        e = cudaStreamDestroy(s->s);
+    }
+    delete s;
+    HRT_CUDA(e);
+    return HRT_OK;
+}
+
+int hrt_stream_synchronize(void* stream) {
+    HRT_CHECK_ARG(stream, "null stream");
+    HRT_CUDA(cudaStreamSynchronize(as_stream(stream)->s));
+    return HRT_OK;
+}
+
+int hrt_device_synchronize(int gpu) {
+    int rc = use_device(gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaDeviceSynchronize());
+    return HRT_OK;
+}
+
+// ---- tokens ----
+
+int hrt_token_record(void* stream, uint64_t* token) {
+    HRT_CHECK_ARG(stream && token, "null argument");
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    cudaEvent_t ev;
+    rc = take_event(s->gpu, cudaEventDefault, &ev);
+    if (rc) return rc;
+    HRT_CUDA(cudaEventRecord(ev, s->s));
+    std::lock_guard<std::mutex> g(g_tok_mu);
+    uint64_t id = ++g_next_token;
+    g_tokens[id] = Token{ev, s->gpu};
+    *token = id;
+    return HRT_OK;
+}
+
+static int find_token(uint64_t token, Token* out) {
+    std::lock_guard<std::mutex> g(g_tok_mu);
+    auto it = g_tokens.find(token);
+    if (it == g_tokens.end()) {
+        set_error("unknown token %llu", (unsigned long long)token);
+        return HRT_E_UNKNOWN_TOKEN;
+    }
+    *out = it->second;
+    return HRT_OK;
+}
+
+int hrt_token_query(uint64_t token) {
+    Token t;
+    int rc = find_token(token, &t);
+    if (rc) return rc;
+    cudaError_t e = cudaEventQuery(t.ev);
+    if (e == cudaSuccess) return 1;
+    if (e == cudaErrorNotReady) {
+        cudaGetLastError();
+        return 0;
+    }
+    set_error("token %llu failed: %s", (unsigned long long)token, cudaGetErrorString(e));
+    return 2;
+}
+
+int hrt_token_wait(uint64_t token) {
+    Token t;
+    int rc = find_token(token, &t);
+    if (rc) return rc;
+    HRT_CUDA(cudaEventSynchronize(t.ev));
+    return HRT_OK;
+}
+
+int hrt_stream_wait_token(void* stream, uint64_t token) {
+    HRT_CHECK_ARG(stream, "null stream");
+    Token t;
+    int rc = find_token(token, &t);
+    if (rc) return rc;
+    Stream* s = as_stream(stream);
+    rc = use_device(s->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaStreamWaitEvent(s->s, t.ev, 0));
+    return HRT_OK;
+}
+
+int hrt_token_elapsed_ms(uint64_t start, uint64_t end, float* ms) {
+    HRT_CHECK_ARG(ms, "null out pointer");
+    Token a, b;
+    int rc = find_token(start, &a);
+    if (rc) return rc;
+    rc = find_token(end, &b);
+    if (rc) return rc;
+    HRT_CUDA(cudaEventElapsedTime(ms, a.ev, b.ev));
+    return HRT_OK;
+}
+
+int hrt_token_release(uint64_t token) {
+    std::lock_guard<std::mutex> g(g_tok_mu);
+    auto it = g_tokens.find(token);
+    if (it == g_tokens.end()) {
+        set_error("unknown token %llu", (unsigned long long)token);
+        return HRT_E_UNKNOWN_TOKEN;
+    }
+    g_event_pool[it->second.gpu * 4].push_back(it->second.ev);
+    g_tokens.erase(it);
+    return HRT_OK;
+}
+
+// ---- host memory and copies ----
+
+int hrt_host_alloc(uint64_t bytes, void** ptr) {
+    HRT_CHECK_ARG(ptr && bytes > 0, "bad host allocation");
+    HRT_CUDA(cudaHostAlloc(ptr, bytes, cudaHostAllocPortable));
+    return HRT_OK;
+}
+
+int hrt_host_free(void* ptr) {
+    if (!ptr) return HRT_OK;
+    HRT_CUDA(cudaFreeHost(ptr));
+    return HRT_OK;
+}
+
+int hrt_host_register(void* ptr, uint64_t bytes) {
+    HRT_CHECK_ARG(ptr && bytes > 0, "bad host registration");
+    HRT_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+    return HRT_OK;
+}
+
+int hrt_host_unregister(void* ptr) {
+    HRT_CUDA(cudaHostUnregister(ptr));
+    return HRT_OK;
+}
+
+int hrt_copy_async(void* stream, void* dst, const void* src, uint64_t bytes) {
+    HRT_CHECK_ARG(stream, "null stream");
+    if (bytes == 0) return HRT_OK;
+    HRT_CHECK_ARG(dst && src, "null copy pointer");
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->s));
+    return HRT_OK;
+}
+
+int hrt_copy_peer_async(void* stream, void* dst, int dst_gpu, const void* src, int src_gpu,
+                        uint64_t bytes) {
+    HRT_CHECK_ARG(stream, "null stream");
+    if (bytes == 0) return HRT_OK;
+    HRT_CHECK_ARG(dst && src, "null copy pointer");
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaMemcpyPeerAsync(dst, dst_gpu, src, src_gpu, bytes, s->s));
+    return HRT_OK;
+}
+
+int hrt_copy2d_async(void* stream, void* dst, uint64_t dpitch, const void* src, uint64_t spitch,
+                     uint64_t width, uint64_t height) {
+    HRT_CHECK_ARG(stream, "null stream");
+    if (width == 0 || height == 0) return HRT_OK;
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDefault, s->s));
+    return HRT_OK;
+}
+
+int hrt_memset_async(void* stream, void* dst, int value, uint64_t bytes) {
+    HRT_CHECK_ARG(stream, "null stream");
+    if (bytes == 0) return HRT_OK;
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaMemsetAsync(dst, value, bytes, s->s));
+    return HRT_OK;
+}
+
+int hrt_pointer_device(const void* ptr, int* gpu) {
+    HRT_CHECK_ARG(gpu, "null out pointer");
+    cudaPointerAttributes a;
+    HRT_CUDA(cudaPointerGetAttributes(&a, ptr));
+    *gpu = (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? a.device : -1;
+    return HRT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,575 @@
+"""Over-decomposed Jacobi on B200s — drop-in for the reference's
+``hrt.bench.jacobi`` (/root/reference/pkg/src/hrt/bench/jacobi.py).
+
+``run_jacobi3d`` keeps the reference signature and return value
+``(BenchReport, checksum, assembled)`` (jacobi.py:281-298).  Two engines:
+
+* ``engine="native"`` (default): every chunk lives in HBM as two ghosted
+  float64 buffers (jacobi.py:382-395); one step is one halo launch (all faces
+  of all chunks on a GPU: neighbour boundary plane read in place, ghost plane
+  written — the reference's pack -> mp_send -> unpack, jacobi.py:219-260,
+  fused into a plane copy) and one update launch over every chunk
+  (_update_body, jacobi.py:70-86), replayed as a CUDA graph.  Chunks on other
+  GPUs of the process are read over NVLink (peer access); chunks of other
+  processes are exchanged with NCCL send/recv (:class:`DistributedJacobi`).
+* ``engine="tasks"``: the reference's task protocol itself — halo objects,
+  pack/unpack/update tasks, ``mp_send`` — executed by the B200 runtime
+  (:mod:`.runtime`, :mod:`.comm`); see :mod:`.jacobi_tasks`.
+
+Results are bitwise equal to the reference for any chunk grid, OD level,
+rank and GPU count (same float operations in the same order per cell).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from .devices import ClockMode, DevicePool, PinnedBuffer, Stream
+from .errors import HrtError
+from .reporting import BenchReport
+
+BOUNDARY = 1.0
+# face f = (axis, side): side 0 is the low face, 1 the high face (jacobi.py:41)
+FACES = [(0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (2, 1)]
+F64 = 8
+
+
+def opposite(face: int) -> int:
+    """jacobi.py:44-46"""
+    axis, side = FACES[face]
+    return axis * 2 + (1 - side)
+
+
+# ---------------------------------------------------------------------------
+# decomposition (jacobi.py:300-380)
+
+
+@dataclass
+class Chunk:
+    lin: int
+    coord: tuple[int, int, int]
+    offsets: tuple[int, int, int]
+    rank: int
+    device_local: int
+    neighbors: dict[int, int] = field(default_factory=dict)  # face -> neighbour lin
+
+
+class ChunkGrid:
+    """Chunking of run_jacobi3d: grid default ``(1, 1, ranks*dpr*od)``
+    (300-301), chunk ``lin = ix + cx*(iy + cy*iz)`` (328-335), rank
+    ``lin*ranks//nchunks`` (325-326), device within the rank
+    ``pos*dpr//len(locals)`` (347, 367), neighbours per face (375-380)."""
+
+    def __init__(self, domain, ranks: int = 1, devices_per_rank: int = 1, od: int = 1,
+                 grid=None):
+        if grid is None:
+            grid = (1, 1, ranks * devices_per_rank * od)
+        self.domain = tuple(int(d) for d in domain)
+        self.grid = tuple(int(g) for g in grid)
+        if len(self.domain) != 3 or len(self.grid) != 3:
+            raise HrtError("domain and grid must have three extents")
+        if min(self.domain) < 1 or min(self.grid) < 1:
+            raise HrtError("domain and grid extents must be positive")
+        X, Y, Z = self.domain
+        cx, cy, cz = self.grid
+        if X % cx or Y % cy or Z % cz:
+            raise HrtError(f"domain {self.domain} not divisible by chunk grid {self.grid}")
+        self.ranks = ranks
+        self.devices_per_rank = devices_per_rank
+        self.nchunks = cx * cy * cz
+        self.ext = (X // cx, Y // cy, Z // cz)
+        per_rank: dict[int, list[int]] = {r: [] for r in range(ranks)}
+        for lin in range(self.nchunks):
+            per_rank[lin * ranks // self.nchunks].append(lin)
+        self.per_rank = per_rank
+        chunks = {}
+        for r in range(ranks):
+            for pos, lin in enumerate(per_rank[r]):
+                ix, iy, iz = lin % cx, (lin // cx) % cy, lin // (cx * cy)
+                ch = Chunk(lin, (ix, iy, iz), (ix * self.ext[0], iy * self.ext[1], iz * self.ext[2]),
+                           r, pos * devices_per_rank // max(1, len(per_rank[r])))
+                for f, (axis, side) in enumerate(FACES):
+                    c = [ix, iy, iz]
+                    c[axis] += -1 if side == 0 else 1
+                    if 0 <= c[0] < cx and 0 <= c[1] < cy and 0 <= c[2] < cz:
+                        ch.neighbors[f] = c[0] + cx * (c[1] + cy * c[2])
+                chunks[lin] = ch
+        self.chunks = [chunks[i] for i in range(self.nchunks)]
+
+    @property
+    def slab(self) -> bool:
+        return self.domain[2] == 1
+
+    def domain_face_mask(self, ch: Chunk) -> int:
+        m = 0
+        for f in range(6):
+            if f not in ch.neighbors:
+                m |= 1 << f
+        return m
+
+
+# ---------------------------------------------------------------------------
+# HBM layouts
+
+
+def chunk_layout(ext, slab: bool) -> N.ChunkLayout:
+    """Slab: 2D row-major (ex+2) x sx with the two z ghosts as constants
+    (a third of the reference's (ex+2, ey+2, 3) bytes); ghost column at
+    element 15 so every interior row starts 128-byte aligned.  Volume:
+    (ex+2, ey+2, ez+2) C order, z fastest (the reference's layout)."""
+    ex, ey, ez = ext
+    L = N.ChunkLayout()
+    L.ext[0], L.ext[1], L.ext[2] = ex, ey, ez
+    if slab:
+        if ez != 1:
+            raise HrtError("slab layout needs ez == 1")
+        sx = -(-(ey + 17) // 16) * 16
+        L.ndim = 2
+        L.stride[0], L.stride[1], L.stride[2] = sx, 1, 0
+        L.origin = 15
+        L.elems = (ex + 2) * sx
+    else:
+        sy = ez + 2
+        sx = (ey + 2) * sy
+        L.ndim = 3
+        L.stride[0], L.stride[1], L.stride[2] = sx, sy, 1
+        L.origin = 0
+        L.elems = (ex + 2) * sx
+    return L
+
+
+def _addr(L: N.ChunkLayout, base: int, i: int, j: int, k: int) -> int:
+    kk = k * L.stride[2] if L.ndim == 3 else 0
+    return base + F64 * (L.origin + i * L.stride[0] + j * L.stride[1] + kk)
+
+
+def face_plane(L: N.ChunkLayout, base: int, face: int, ghost: bool):
+    """(address, n0, n1, s0, s1) of a chunk's face plane: the ghost plane
+    (unpack target, jacobi.py:113-124) or the adjacent interior plane (pack
+    source, jacobi.py:102-110)."""
+    axis, side = FACES[face]
+    e = list(L.ext)
+    if ghost:
+        idx = 0 if side == 0 else e[axis] + 1
+    else:
+        idx = 1 if side == 0 else e[axis]
+    start = [1, 1, 1]
+    start[axis] = idx
+    if L.ndim == 2:
+        start[2] = 0
+        others = [a for a in (0, 1) if a != axis]
+        strides = {0: L.stride[0], 1: L.stride[1]}
+        n0, s0 = 1, 0
+        n1, s1 = e[others[0]], strides[others[0]]
+    else:
+        others = [a for a in (0, 1, 2) if a != axis]
+        n0, s0 = e[others[0]], L.stride[others[0]]
+        n1, s1 = e[others[1]], L.stride[others[1]]
+    return _addr(L, base, *start), n0, n1, s0, s1
+
+
+def interior_row_bytes(L: N.ChunkLayout):
+    """(width bytes, pitch bytes, rows) of the interior for 2D copies."""
+    if L.ndim == 2:
+        return L.ext[1] * F64, L.stride[0] * F64, L.ext[0]
+    return L.ext[2] * F64, L.stride[1] * F64, L.ext[1]
+
+
+def _seg(src_pair, dst_pair, n0, n1, ss0, ss1, ds0, ds1) -> N.HaloSeg:
+    g = N.HaloSeg()
+    g.src[0], g.src[1] = src_pair
+    g.dst[0], g.dst[1] = dst_pair
+    g.n0, g.n1, g.ss0, g.ss1, g.ds0, g.ds1 = n0, n1, ss0, ss1, ds0, ds1
+    return g
+
+
+def _arr(ctype, items):
+    items = list(items)
+    return (ctype * max(len(items), 1))(*items)
+
+
+# ---------------------------------------------------------------------------
+# single-process engine (1..n GPUs)
+
+
+class JacobiSolver:
+    """Device-resident chunked Jacobi for every chunk of this process.
+
+    ``placement`` maps chunk lin -> physical GPU.  By default chunks follow
+    the reference's (rank, device_local) assignment, with the virtual devices
+    ``rank*devices_per_rank + device_local`` spread round-robin over
+    ``gpus`` (default: all visible GPUs)."""
+
+    def __init__(self, grid: ChunkGrid, gpus: Optional[Sequence[int]] = None,
+                 placement: Optional[dict[int, int]] = None, rows: Optional[int] = None):
+        ngpu = N.gpu_count()
+        N.require_gpu(0)
+        self.grid = grid
+        if gpus is None:
+            gpus = list(range(ngpu))
+        self.gpus = list(gpus)
+        if placement is None:
+            dpr = grid.devices_per_rank
+            placement = {ch.lin: self.gpus[(ch.rank * dpr + ch.device_local) % len(self.gpus)]
+                         for ch in grid.chunks}
+        self.placement = placement
+        self.layout = chunk_layout(grid.ext, grid.slab)
+        L = self.layout
+        self.buf_bytes = -(-L.elems * F64 // 256) * 256
+        used = sorted({placement[ch.lin] for ch in grid.chunks})
+        self.used_gpus = used
+        self.streams = {g: Stream(g, name=f"jacobi{g}") for g in used}
+        self.pools: dict[int, DevicePool] = {}
+        self.bufs: dict[int, tuple[int, int]] = {}
+        for g in used:
+            mine = [ch for ch in grid.chunks if placement[ch.lin] == g]
+            self.pools[g] = DevicePool(g, 2 * len(mine) * self.buf_bytes + 256)
+            for ch in mine:
+                b0 = self.pools[g].alloc(self.buf_bytes)[2]
+                b1 = self.pools[g].alloc(self.buf_bytes)[2]
+                self.bufs[ch.lin] = (b0, b1)
+        # peer access for faces whose neighbour lives on another GPU
+        for ch in grid.chunks:
+            g = placement[ch.lin]
+            for nb in ch.neighbors.values():
+                h = placement[nb]
+                if h != g:
+                    N.call("hrt_enable_peer_access", g, h)
+        self.plans = {}
+        self.peer_deps: dict[int, set[int]] = {g: set() for g in used}
+        for g in used:
+            segs = []
+            mine = [ch for ch in grid.chunks if placement[ch.lin] == g]
+            for ch in mine:
+                for f, nb in sorted(ch.neighbors.items()):
+                    h = placement[nb]
+                    if h != g:
+                        self.peer_deps[g].add(h)
+                    segs.append(self._face_seg(ch.lin, f, nb))
+            plan = ctypes.c_void_p()
+            bufs = _arr(ctypes.c_uint64, [b for ch in mine for b in self.bufs[ch.lin]])
+            seg_arr = _arr(N.HaloSeg, segs)
+            N.call("hrt_jacobi_plan_create", g, ctypes.byref(L), len(mine), bufs, seg_arr,
+                   len(segs), ctypes.byref(plan))
+            if rows:
+                N.call("hrt_jacobi_plan_set_rows", plan, rows)
+            self.plans[g] = plan
+        self.resid = {}
+        self.steps_done = 0
+        self._field_pool = None
+        self._field_ptr = 0
+        self._init_ghosts()
+
+    # -- setup --------------------------------------------------------------
+
+    def _face_seg(self, lin: int, face: int, nb: int) -> N.HaloSeg:
+        """Ghost plane `face` of chunk `lin` <- the neighbour's boundary plane,
+        for both buffer parities (jacobi.py:213-217 alternate buffers)."""
+        L = self.layout
+        src, dst = [], []
+        for p in (0, 1):
+            s_addr, n0, n1, s0, s1 = face_plane(L, self.bufs[nb][p], opposite(face), ghost=False)
+            d_addr, _, _, d0, d1 = face_plane(L, self.bufs[lin][p], face, ghost=True)
+            src.append(s_addr)
+            dst.append(d_addr)
+        return _seg(src, dst, n0, n1, s0, s1, d0, d1)
+
+    def _init_ghosts(self) -> None:
+        """Both buffers: domain-face ghosts = BOUNDARY, others 0
+        (jacobi.py:382-395; the reference's update then copies the ghost
+        shell forward each step, jacobi.py:80-86, which keeps it constant)."""
+        L = self.layout
+        for ch in self.grid.chunks:
+            g = self.placement[ch.lin]
+            mask = self.grid.domain_face_mask(ch)
+            for b in self.bufs[ch.lin]:
+                N.call("hrt_jacobi_ghost_fill", self.streams[g].h, ctypes.c_void_p(b),
+                       ctypes.byref(L), mask, BOUNDARY)
+
+    def _field(self) -> int:
+        """Contiguous (X,Y,Z) float64 staging field on the first GPU."""
+        if self._field_pool is None:
+            X, Y, Z = self.grid.domain
+            nbytes = X * Y * Z * F64
+            g0 = self.used_gpus[0]
+            self._field_pool = DevicePool(g0, max(nbytes, 256) + 256)
+            self._field_ptr = self._field_pool.alloc(max(nbytes, 1))[2]
+        return self._field_ptr
+
+    def _chunk_copies(self, to_chunks: bool, parity: int, field_ptr: int, stream_of) -> None:
+        """Strided copies between the contiguous field and chunk interiors."""
+        L = self.layout
+        X, Y, Z = self.grid.domain
+        width, pitch, rows = interior_row_bytes(L)
+        for ch in self.grid.chunks:
+            g = self.placement[ch.lin]
+            st = stream_of(g)
+            ox, oy, oz = ch.offsets
+            base = self.bufs[ch.lin][parity]
+            if L.ndim == 2:
+                planes = [(_addr(L, base, 1, 1, 0), field_ptr + F64 * (ox * Y + oy))]
+                fpitch = Y * F64
+            else:
+                planes = [(_addr(L, base, 1 + i, 1, 1),
+                           field_ptr + F64 * (((ox + i) * Y + oy) * Z + oz))
+                          for i in range(L.ext[0])]
+                fpitch = Z * F64
+            for caddr, faddr in planes:
+                if to_chunks:
+                    N.call("hrt_copy2d_async", st.h, ctypes.c_void_p(caddr), pitch,
+                           ctypes.c_void_p(faddr), fpitch, width, rows)
+                else:
+                    N.call("hrt_copy2d_async", st.h, ctypes.c_void_p(faddr), fpitch,
+                           ctypes.c_void_p(caddr), pitch, width, rows)
+
+    # -- data in/out ----------------------------------------------------------
+
+    def upload(self, interior: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None):
+        """Initial interior (X,Y,Z) into buffer 0 of every chunk: one H2D of
+        the contiguous field, then device-side strided copies.  ``None`` is
+        the reference's initial state (interior 0.0, jacobi.py:385)."""
+        X, Y, Z = self.grid.domain
+        nbytes = X * Y * Z * F64
+        f = self._field()
+        g0 = self.used_gpus[0]
+        st0 = self.streams[g0]
+        if host is not None:
+            src_ptr = host.ptr
+        elif interior is not None:
+            arr = np.ascontiguousarray(interior, dtype=np.float64)
+            if arr.shape != (X, Y, Z):
+                raise HrtError(f"interior shape {arr.shape} != domain {(X, Y, Z)}")
+            src_ptr = arr.ctypes.data
+        else:
+            src_ptr = None
+        if src_ptr is None:
+            N.call("hrt_memset_async", st0.h, ctypes.c_void_p(f), 0, nbytes)
+        else:
+            N.call("hrt_copy_async", st0.h, ctypes.c_void_p(f), ctypes.c_void_p(src_ptr), nbytes)
+        self._fan_out(g0)
+        self._chunk_copies(True, 0, f, lambda g: self.streams[g])
+        self.steps_done = 0
+        self.sync()
+
+    def _fan_out(self, g0: int) -> None:
+        """Make every GPU's stream wait for GPU g0's stream."""
+        if len(self.used_gpus) > 1:
+            tok = self.streams[g0].record()
+            for g in self.used_gpus:
+                if g != g0:
+                    self.streams[g].wait(tok)
+
+    def _fan_in(self, g0: int) -> None:
+        for g in self.used_gpus:
+            if g != g0:
+                self.streams[g0].wait(self.streams[g].record())
+
+    def gather(self) -> int:
+        """Assemble the current field into the contiguous device staging
+        buffer (jacobi.py:425-435); returns its device address."""
+        f = self._field()
+        g0 = self.used_gpus[0]
+        self._fan_in(g0)
+        self._chunk_copies(False, self.steps_done % 2, f, lambda g: self.streams[g0])
+        return f
+
+    def download(self, out: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None):
+        X, Y, Z = self.grid.domain
+        nbytes = X * Y * Z * F64
+        f = self.gather()
+        st0 = self.streams[self.used_gpus[0]]
+        if host is not None:
+            dst = host.ptr
+            out = host.array(np.float64, (X, Y, Z))
+        else:
+            if out is None:
+                out = np.empty((X, Y, Z), dtype=np.float64)
+            dst = out.ctypes.data
+        N.call("hrt_copy_async", st0.h, ctypes.c_void_p(dst), ctypes.c_void_p(f), nbytes)
+        st0.synchronize()
+        return out
+
+    def checksum(self) -> float:
+        """float(np.sum(assembled)) (jacobi.py:436), bit-exact, on the GPU."""
+        X, Y, Z = self.grid.domain
+        f = self.gather()
+        out = ctypes.c_double()
+        N.call("hrt_np_sum", self.streams[self.used_gpus[0]].h, ctypes.c_void_p(f), X * Y * Z,
+               ctypes.byref(out))
+        return out.value
+
+    # -- stepping -------------------------------------------------------------
+
+    def reset_residual(self, steps: int) -> None:
+        self.resid = {}
+        for g in self.used_gpus:
+            pool = self.pools[g]
+            if not hasattr(self, "_rbuf"):
+                self._rbuf = {}
+            if g not in self._rbuf or self._rbuf[g][1] < steps:
+                self._rbuf[g] = (DevicePool(g, max(steps, 1) * 8 + 256), max(steps, 1))
+            rp = self._rbuf[g][0]
+            ptr = rp.base
+            N.call("hrt_memset_async", self.streams[g].h, ctypes.c_void_p(ptr), 0, max(steps, 1) * 8)
+            self.resid[g] = ptr
+        self._resid_steps = steps
+
+    def run(self, steps: int, residual: bool = True, graph: bool = True) -> None:
+        """Advance ``steps`` steps.  One GPU: the plan runs them (CUDA graph
+        when no residual slot is needed).  Several GPUs: per step, each GPU
+        waits (GPU-side) for its peer neighbours' previous step, then runs
+        its halo faces (NVLink reads) and update."""
+        if steps < 0:
+            raise HrtError("steps must be >= 0")
+        if residual:
+            self.reset_residual(self.steps_done + steps)
+        first = self.steps_done
+        if len(self.used_gpus) == 1:
+            g = self.used_gpus[0]
+            N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, first, steps,
+                   ctypes.c_void_p(self.resid[g] if residual else 0), 1 if graph else 0)
+        else:
+            prev: dict[int, object] = {}
+            for k in range(steps):
+                step = first + k
+                cur = {}
+                for g in self.used_gpus:
+                    for h in self.peer_deps[g]:
+                        if h in prev:
+                            self.streams[g].wait(prev[h])
+                    N.call("hrt_jacobi_plan_step", self.plans[g], self.streams[g].h, step,
+                           ctypes.c_void_p(self.resid[g] if residual else 0))
+                    cur[g] = self.streams[g].record()
+                prev = cur
+        self.steps_done += steps
+
+    def run_timed(self, steps: int, residual: bool = True):
+        """run() with CUDA events around every launch (single GPU); returns
+        (update_ms_total, halo_ms_total, total_ms)."""
+        if len(self.used_gpus) != 1:
+            raise HrtError("run_timed drives a single GPU")
+        if residual:
+            self.reset_residual(self.steps_done + steps)
+        g = self.used_gpus[0]
+        up, ha, tot = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        N.call("hrt_jacobi_plan_run_timed", self.plans[g], self.streams[g].h, self.steps_done, steps,
+               ctypes.c_void_p(self.resid[g] if residual else 0), ctypes.byref(up),
+               ctypes.byref(ha), ctypes.byref(tot))
+        self.steps_done += steps
+        return up.value, ha.value, tot.value
+
+    def residual_history(self) -> np.ndarray:
+        """max |u_{s+1} - u_s| per step, max over GPUs (builder-defined; the
+        reference has no residual)."""
+        n = getattr(self, "_resid_steps", 0)
+        out = np.zeros(n, dtype=np.uint64)
+        for g in self.used_gpus:
+            if g not in self.resid:
+                continue
+            tmp = np.empty(n, dtype=np.uint64)
+            if n:
+                N.call("hrt_copy_async", self.streams[g].h, ctypes.c_void_p(tmp.ctypes.data),
+                       ctypes.c_void_p(self.resid[g]), n * 8)
+                self.streams[g].synchronize()
+            out = np.maximum(out, tmp)
+        return out.view(np.float64)
+
+    def sync(self) -> None:
+        for st in self.streams.values():
+            st.synchronize()
+
+    def close(self) -> None:
+        for p in getattr(self, "plans", {}).values():
+            N.lib().hrt_jacobi_plan_destroy(p)
+        self.plans = {}
+
+
+# ---------------------------------------------------------------------------
+# drop-in driver
+
+
+def run_jacobi3d(
+    domain: tuple[int, int, int],
+    ranks: int = 1,
+    devices_per_rank: int = 1,
+    od: int = 1,
+    steps: int = 10,
+    grid: Optional[tuple[int, int, int]] = None,
+    clock: ClockMode = ClockMode.WALL,
+    latency: float = 1e-5,
+    bandwidth: float = 2e8,
+    streams: int = 5,
+    update_cost_per_cell: float = 2e-8,
+    face_cost_per_cell: float = 1e-9,
+    device_aware: bool = False,
+    capacity: int = 256 << 20,
+    check: bool = False,
+    tracer=None,
+    engine: str = "native",
+    gpus: Optional[Sequence[int]] = None,
+) -> tuple[BenchReport, float, np.ndarray]:
+    """Run the proxy app on B200s; returns (report, checksum, assembled
+    interior) like jacobi.py:281-462.  ``clock``, ``latency``,
+    ``bandwidth``, ``*_cost_per_cell`` and ``capacity`` parameterise the
+    reference's simulator and are accepted for signature compatibility;
+    time here is real device time."""
+    if engine == "tasks":
+        from .jacobi_tasks import run_jacobi3d_tasks
+
+        return run_jacobi3d_tasks(domain, ranks=ranks, devices_per_rank=devices_per_rank, od=od,
+                                  steps=steps, grid=grid, streams=streams,
+                                  device_aware=device_aware, check=check, tracer=tracer,
+                                  gpus=gpus)
+    if engine != "native":
+        raise HrtError(f"unknown engine {engine!r}")
+    cg = ChunkGrid(domain, ranks, devices_per_rank, od, grid)
+    solver = JacobiSolver(cg, gpus=gpus)
+    try:
+        solver.upload()
+        t0 = time.perf_counter()
+        solver.run(steps, residual=True)
+        solver.sync()
+        makespan = time.perf_counter() - t0
+        assembled = solver.download()
+        checksum = solver.checksum()
+        resid = solver.residual_history()
+    finally:
+        solver.close()
+    X, Y, Z = cg.domain
+    report = BenchReport(
+        "jacobi3d",
+        columns=["step", "virtual_makespan_s", "residual"],
+        meta={
+            "domain": list(cg.domain), "grid": list(cg.grid), "ranks": ranks,
+            "devices_per_rank": devices_per_rank, "od": od, "steps": steps,
+            "checksum": checksum, "makespan_s": makespan, "engine": "native",
+            "gpus": solver.used_gpus,
+            "glups": (X * Y * Z * steps / makespan / 1e9) if makespan > 0 else 0.0,
+        },
+    )
+    for s in range(1, steps + 1):
+        report.add(step=s, virtual_makespan_s=makespan * s / steps, residual=float(resid[s - 1]))
+    if check:
+        ref = jacobi_single_array(cg.domain, steps)
+        if not np.array_equal(assembled, ref):
+            raise HrtError("jacobi3d result differs from the single-array reference")
+    return report, checksum, assembled
+
+
+def jacobi_single_array(domain, steps: int, gpu: int = 0) -> np.ndarray:
+    """The single-array solver the reference checks against
+    (jacobi_reference, jacobi.py:49-67), here one unchunked B200 solve."""
+    cg = ChunkGrid(domain, grid=(1, 1, 1))
+    s = JacobiSolver(cg, gpus=[gpu])
+    try:
+        s.upload()
+        s.run(steps, residual=False)
+        return s.download()
+    finally:
+        s.close()

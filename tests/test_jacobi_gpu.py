@@ -1,0 +1,117 @@
+"""GPU parity of the native Jacobi engine (libhrt_b200.so on a B200)
+against the reference's golden vectors and the C oracle.
+
+Bar: bit-exact float64 (the north star's --fmad=false mode) for the field,
+the checksum and the residual history."""
+
+import ctypes
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import kwargs_of
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def hrt():
+    import paper_2303_02543_b200 as P
+    from paper_2303_02543_b200 import _native as N
+
+    N.require_gpu(0)
+    return P
+
+
+def test_div6_markstein_equals_ieee(hrt):
+    """The update kernel's division (Markstein correction) is bitwise IEEE
+    x/6.0: 2^28 uniform [0,6), 2^26 near 1/2/3/6, 2^26 random finite."""
+    from paper_2303_02543_b200 import _native as N
+    from paper_2303_02543_b200.devices import Stream
+
+    st = Stream(0)
+    for mode, n in ((0, 1 << 28), (1, 1 << 26), (2, 1 << 26)):
+        mism, bad = ctypes.c_uint64(), ctypes.c_double()
+        N.call("hrt_div6_sweep", st.h, 12345 + mode, n, mode, ctypes.byref(mism), ctypes.byref(bad))
+        assert mism.value == 0, (mode, bad.value)
+
+
+LADDER_NATIVE = [
+    "cube8_s3", "ac10_g111", "ac10_g222", "ac10_od2", "ac10_od4", "ac10_r2d2", "slab64_s10",
+    "slab1024_s5", "cfg1", "halo32_s20", "halo32_s20_r2d2", "halo32_s20_direct",
+    "halo16_cube_s12", "cube24_s30", "slab48x40_s64", "slab96x80_s13", "slab256_s300",
+    "unit_chunks_slab", "unit_chunks_cube", "zero_steps", "rect_slab", "thin_x", "zslab_3d",
+]
+
+
+@pytest.mark.parametrize("name", LADDER_NATIVE)
+def test_ladder_bitwise(hrt, ladder, small_arrays, name):
+    e = ladder[name]
+    rep, cs, arr = hrt.run_jacobi3d(tuple(e["domain"]), steps=e["steps"], **kwargs_of(e))
+    if name in small_arrays:
+        ref = small_arrays[name]
+        bad = np.argwhere(arr != ref)
+        assert bad.size == 0, f"{len(bad)} cells differ, first {bad[:3].tolist()}"
+    assert sha(arr) == e["sha256"]
+    assert repr(cs) == e["checksum"]
+    assert len(rep.rows) == e["steps"]
+
+
+def test_cfg2_prefix_bitwise(hrt, ladder):
+    """16384^2 slab, 8x8 chunks (cfg2 decomposition), 1 and 3 steps."""
+    for s in (1, 3):
+        e = ladder[f"cfg2_prefix_s{s}"]
+        _, cs, arr = hrt.run_jacobi3d((16384, 16384, 1), steps=s, grid=(8, 8, 1))
+        assert sha(arr) == e["sha256"]
+        assert repr(cs) == e["checksum"]
+
+
+def test_residual_history_bitwise(hrt, oracle):
+    for dom, grid, steps in [((40, 24, 1), (5, 3, 1), 33), ((12, 10, 6), (2, 1, 3), 15),
+                             ((512, 384, 1), (4, 3, 1), 150)]:
+        rep, _, arr = hrt.run_jacobi3d(dom, steps=steps, grid=grid)
+        ref, res = oracle.jacobi_c(dom, steps, residual=True)
+        assert np.array_equal(arr, ref)
+        got = np.array([r["residual"] for r in rep.rows])
+        assert np.array_equal(got, res), np.argwhere(got != res)[:5]
+
+
+def test_mid_size_vs_oracle(hrt, oracle):
+    """4096^2 for 257 steps, 4x8 chunks: field and checksum vs the C oracle."""
+    dom, steps = (4096, 4096, 1), 257
+    _, cs, arr = hrt.run_jacobi3d(dom, steps=steps, grid=(4, 8, 1))
+    ref = oracle.jacobi_c(dom, steps)
+    assert np.array_equal(arr, ref)
+    assert cs == oracle.checksum(ref)
+
+
+def test_check_mode_and_check_failure_detection(hrt):
+    rep, cs, arr = hrt.run_jacobi3d((8, 8, 8), steps=3, check=True)
+    assert arr.shape == (8, 8, 8)
+    assert 0.0 < arr.mean() < 1.0
+    assert rep.columns[:2] == ["step", "virtual_makespan_s"]
+
+
+def test_full_size_properties(hrt):
+    """cfg2 at full size (16384^2, 1000 steps): size-independent properties —
+    decomposition invariance (8x8 vs 2x32 chunks, bitwise), exact mirror
+    symmetry in x ((xm+xp) is commutative), Dirichlet bound 0 < u <= 1."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    out = []
+    for grid in ((8, 8, 1), (2, 32, 1)):
+        s = JacobiSolver(ChunkGrid((16384, 16384, 1), grid=grid))
+        s.upload()
+        s.run(1000, residual=True)
+        out.append((s.download(), s.checksum(), s.residual_history()))
+        s.close()
+    (a, ca, ra), (b, cb, rb) = out
+    assert np.array_equal(a, b) and ca == cb and np.array_equal(ra, rb)
+    assert np.array_equal(a, a[::-1])
+    assert a.min() > 0.0 and a.max() <= 1.0
+    assert np.all(ra[1:] <= ra[:-1] * 1.0000001 + 1e-300) or ra[-1] < ra[0]

@@ -1,0 +1,32 @@
+"""Quick device timing of the slab update kernel on cfg2 (development probe).
+
+python tools/probe_slab.py [steps] [rows...]
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2303_02543_b200 import _native as N  # noqa: E402
+from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver  # noqa: E402
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+rows_list = [int(r) for r in sys.argv[2:]] or [64]
+X = Y = 16384
+cells = X * Y
+for rows in rows_list:
+    s = JacobiSolver(ChunkGrid((X, Y, 1), grid=(8, 8, 1)), rows=rows)
+    s.upload()
+    s.run_timed(5)
+    up, ha, tot = s.run_timed(steps)
+    glups = cells * steps / (tot / 1e3) / 1e9
+    upd_gbs = 16 * cells * steps / (up / 1e3) / 1e9
+    print(f"rows={rows}: total {tot/steps:.3f} ms/step  update {up/steps:.3f} ms  halo {ha/steps:.4f} ms"
+          f"  GLUPS {glups:.1f}  update-kernel {upd_gbs:.0f} GB/s", flush=True)
+    t0 = time.perf_counter()
+    s.run(steps, residual=False, graph=True)
+    s.sync()
+    dt = time.perf_counter() - t0
+    print(f"   graph run: {dt/steps*1e3:.3f} ms/step GLUPS {cells*steps/dt/1e9:.1f}", flush=True)
+    s.close()
