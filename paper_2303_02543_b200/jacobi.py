@@ -195,76 +195,157 @@ def _arr(ctype, items):
 
 
 # ---------------------------------------------------------------------------
-# single-process engine (1..n GPUs)
+# the per-process engine
+
+
+def _contiguous(n0, n1, s0, s1) -> bool:
+    return n0 * n1 == 0 or (s1 == 1 and (n0 == 1 or s0 == n1))
 
 
 class JacobiSolver:
-    """Device-resident chunked Jacobi for every chunk of this process.
+    """Device-resident chunked Jacobi for the chunks this process owns.
 
-    ``placement`` maps chunk lin -> physical GPU.  By default chunks follow
-    the reference's (rank, device_local) assignment, with the virtual devices
-    ``rank*devices_per_rank + device_local`` spread round-robin over
-    ``gpus`` (default: all visible GPUs)."""
+    * Single process (``rank=None``): every chunk; ``placement`` maps chunk
+      lin -> GPU.  By default chunks follow the reference's (rank,
+      device_local) assignment with virtual devices
+      ``rank*devices_per_rank + device_local`` spread round-robin over
+      ``gpus``.  Faces between GPUs are read over NVLink (peer access).
+    * One process per GPU (``rank`` given): the chunks of
+      ``grid.per_rank[rank]`` (jacobi.py:325-339) on ``gpus[0]``; faces whose
+      neighbour belongs to another rank travel by NCCL send/recv (``comm``
+      from :func:`paper_2303_02543_b200.distributed.nccl_comm`), packed
+      into staging buffers only when the plane is strided.
+    """
 
     def __init__(self, grid: ChunkGrid, gpus: Optional[Sequence[int]] = None,
-                 placement: Optional[dict[int, int]] = None, rows: Optional[int] = None):
-        ngpu = N.gpu_count()
+                 placement: Optional[dict[int, int]] = None, rows: Optional[int] = None,
+                 rank: Optional[int] = None, comm=None):
         N.require_gpu(0)
+        ngpu = N.gpu_count()
         self.grid = grid
-        if gpus is None:
-            gpus = list(range(ngpu))
-        self.gpus = list(gpus)
-        if placement is None:
-            dpr = grid.devices_per_rank
-            placement = {ch.lin: self.gpus[(ch.rank * dpr + ch.device_local) % len(self.gpus)]
-                         for ch in grid.chunks}
+        self.rank = rank
+        self.comm = comm
+        gpus = list(range(ngpu)) if gpus is None else list(gpus)
+        self.gpus = gpus
+        if rank is not None:
+            owned = list(grid.per_rank[rank])
+            placement = {lin: gpus[0] for lin in owned}
+        else:
+            owned = [ch.lin for ch in grid.chunks]
+            if placement is None:
+                dpr = grid.devices_per_rank
+                placement = {ch.lin: gpus[(ch.rank * dpr + ch.device_local) % len(gpus)]
+                             for ch in grid.chunks}
+        self.owned = owned
         self.placement = placement
         self.layout = chunk_layout(grid.ext, grid.slab)
         L = self.layout
         self.buf_bytes = -(-L.elems * F64 // 256) * 256
-        used = sorted({placement[ch.lin] for ch in grid.chunks})
-        self.used_gpus = used
-        self.streams = {g: Stream(g, name=f"jacobi{g}") for g in used}
+        self.used_gpus = sorted({placement[lin] for lin in owned})
+        self.streams = {g: Stream(g, name=f"jacobi{g}") for g in self.used_gpus}
+        self.rank_of = {ch.lin: ch.rank for ch in grid.chunks}
+        # remote messages (dst chunk, face) in canonical global order
+        remote_msgs = []
+        if rank is not None:
+            for ch in grid.chunks:
+                for f, nb in sorted(ch.neighbors.items()):
+                    if self.rank_of[nb] != self.rank_of[ch.lin] and rank in (
+                            self.rank_of[nb], self.rank_of[ch.lin]):
+                        remote_msgs.append((ch.lin, f, nb))
+        # storage: two buffers per owned chunk (+ staging for strided remote planes)
+        staging = 0
+        for (c, f, nb) in remote_msgs:
+            _, n0, n1, s0, s1 = face_plane(L, 0, f, ghost=True)
+            if not _contiguous(n0, n1, s0, s1):
+                staging += -(-n0 * n1 * F64 // 256) * 256
         self.pools: dict[int, DevicePool] = {}
         self.bufs: dict[int, tuple[int, int]] = {}
-        for g in used:
-            mine = [ch for ch in grid.chunks if placement[ch.lin] == g]
-            self.pools[g] = DevicePool(g, 2 * len(mine) * self.buf_bytes + 256)
-            for ch in mine:
+        for g in self.used_gpus:
+            mine = [lin for lin in owned if placement[lin] == g]
+            extra = staging if g == self.used_gpus[0] else 0
+            self.pools[g] = DevicePool(g, 2 * len(mine) * self.buf_bytes + extra + 4096)
+            for lin in mine:
                 b0 = self.pools[g].alloc(self.buf_bytes)[2]
                 b1 = self.pools[g].alloc(self.buf_bytes)[2]
-                self.bufs[ch.lin] = (b0, b1)
-        # peer access for faces whose neighbour lives on another GPU
-        for ch in grid.chunks:
-            g = placement[ch.lin]
-            for nb in ch.neighbors.values():
-                h = placement[nb]
-                if h != g:
+                self.bufs[lin] = (b0, b1)
+        for lin in owned:
+            g = placement[lin]
+            for nb in grid.chunks[lin].neighbors.values():
+                h = placement.get(nb)
+                if h is not None and h != g:
                     N.call("hrt_enable_peer_access", g, h)
+        # per-GPU plans: local/peer faces (+ packs), remote ops, unpacks
         self.plans = {}
-        self.peer_deps: dict[int, set[int]] = {g: set() for g in used}
-        for g in used:
-            segs = []
-            mine = [ch for ch in grid.chunks if placement[ch.lin] == g]
-            for ch in mine:
-                for f, nb in sorted(ch.neighbors.items()):
-                    h = placement[nb]
-                    if h != g:
-                        self.peer_deps[g].add(h)
-                    segs.append(self._face_seg(ch.lin, f, nb))
+        self.peer_deps: dict[int, set[int]] = {g: set() for g in self.used_gpus}
+        pre: dict[int, list] = {g: [] for g in self.used_gpus}
+        for lin in owned:
+            g = placement[lin]
+            for f, nb in sorted(grid.chunks[lin].neighbors.items()):
+                if nb in placement:
+                    if placement[nb] != g:
+                        self.peer_deps[g].add(placement[nb])
+                    pre[g].append(self._face_seg(lin, f, nb))
+        remote_ops, post = [], []
+        g0 = self.used_gpus[0]
+        for (c, f, nb) in remote_msgs:
+            if self.rank_of[nb] == rank:  # I send nb's boundary plane
+                pairs = [face_plane(L, self.bufs[nb][p], opposite(f), ghost=False) for p in (0, 1)]
+                _, n0, n1, s0, s1 = pairs[0]
+                if _contiguous(n0, n1, s0, s1):
+                    addrs = [pairs[0][0], pairs[1][0]]
+                else:
+                    st = self.pools[g0].alloc(n0 * n1 * F64)[2]
+                    pre[g0].append(_seg([pairs[0][0], pairs[1][0]], [st, st], n0, n1, s0, s1,
+                                        n1, 1))
+                    addrs = [st, st]
+                remote_ops.append(self._remote(addrs, n0 * n1, self.rank_of[c], 0))
+            else:  # I receive into c's ghost plane
+                pairs = [face_plane(L, self.bufs[c][p], f, ghost=True) for p in (0, 1)]
+                _, n0, n1, s0, s1 = pairs[0]
+                if _contiguous(n0, n1, s0, s1):
+                    addrs = [pairs[0][0], pairs[1][0]]
+                else:
+                    st = self.pools[g0].alloc(n0 * n1 * F64)[2]
+                    post.append(_seg([st, st], [pairs[0][0], pairs[1][0]], n0, n1, n1, 1, s0, s1))
+                    addrs = [st, st]
+                remote_ops.append(self._remote(addrs, n0 * n1, self.rank_of[nb], 1))
+        if remote_ops and comm is None:
+            raise HrtError("faces cross ranks: an NCCL communicator is required")
+        for g in self.used_gpus:
+            mine = [lin for lin in owned if placement[lin] == g]
             plan = ctypes.c_void_p()
-            bufs = _arr(ctypes.c_uint64, [b for ch in mine for b in self.bufs[ch.lin]])
-            seg_arr = _arr(N.HaloSeg, segs)
+            bufs = _arr(ctypes.c_uint64, [b for lin in mine for b in self.bufs[lin]])
+            seg_arr = _arr(N.HaloSeg, pre[g])
             N.call("hrt_jacobi_plan_create", g, ctypes.byref(L), len(mine), bufs, seg_arr,
-                   len(segs), ctypes.byref(plan))
+                   len(pre[g]), ctypes.byref(plan))
             if rows:
                 N.call("hrt_jacobi_plan_set_rows", plan, rows)
+            if g == g0 and remote_ops:
+                N.call("hrt_jacobi_plan_set_remote", plan, ctypes.c_void_p(comm),
+                       _arr(N.RemoteSeg, remote_ops), len(remote_ops), _arr(N.HaloSeg, post),
+                       len(post))
             self.plans[g] = plan
-        self.resid = {}
+        self.n_remote = len(remote_ops)
+        self.n_faces = sum(len(v) for v in pre.values())
+        self.resid: dict[int, int] = {}
+        self._rbuf: dict[int, tuple[DevicePool, int]] = {}
+        self._resid_steps = 0
         self.steps_done = 0
         self._field_pool = None
         self._field_ptr = 0
+        # bounding box of the owned chunks (the whole domain in one process)
+        lo = [min(grid.chunks[lin].offsets[a] for lin in owned) for a in range(3)]
+        hi = [max(grid.chunks[lin].offsets[a] + grid.ext[a] for lin in owned) for a in range(3)]
+        self.box_lo = tuple(lo)
+        self.box = tuple(h - l for l, h in zip(lo, hi))
         self._init_ghosts()
+
+    @staticmethod
+    def _remote(addrs, count, peer, kind) -> N.RemoteSeg:
+        r = N.RemoteSeg()
+        r.buf[0], r.buf[1] = addrs
+        r.count, r.peer, r.kind = count, peer, kind
+        return r
 
     # -- setup --------------------------------------------------------------
 
@@ -285,33 +366,36 @@ class JacobiSolver:
         (jacobi.py:382-395; the reference's update then copies the ghost
         shell forward each step, jacobi.py:80-86, which keeps it constant)."""
         L = self.layout
-        for ch in self.grid.chunks:
-            g = self.placement[ch.lin]
-            mask = self.grid.domain_face_mask(ch)
-            for b in self.bufs[ch.lin]:
+        for lin in self.owned:
+            g = self.placement[lin]
+            mask = self.grid.domain_face_mask(self.grid.chunks[lin])
+            for b in self.bufs[lin]:
                 N.call("hrt_jacobi_ghost_fill", self.streams[g].h, ctypes.c_void_p(b),
                        ctypes.byref(L), mask, BOUNDARY)
 
+    @property
+    def field_elems(self) -> int:
+        return self.box[0] * self.box[1] * self.box[2]
+
     def _field(self) -> int:
-        """Contiguous (X,Y,Z) float64 staging field on the first GPU."""
+        """Contiguous staging field (the owned bounding box) on the first GPU."""
         if self._field_pool is None:
-            X, Y, Z = self.grid.domain
-            nbytes = X * Y * Z * F64
+            nbytes = max(self.field_elems * F64, 256)
             g0 = self.used_gpus[0]
-            self._field_pool = DevicePool(g0, max(nbytes, 256) + 256)
-            self._field_ptr = self._field_pool.alloc(max(nbytes, 1))[2]
+            self._field_pool = DevicePool(g0, nbytes + 256)
+            self._field_ptr = self._field_pool.alloc(nbytes)[2]
         return self._field_ptr
 
     def _chunk_copies(self, to_chunks: bool, parity: int, field_ptr: int, stream_of) -> None:
         """Strided copies between the contiguous field and chunk interiors."""
         L = self.layout
-        X, Y, Z = self.grid.domain
+        X, Y, Z = self.box
         width, pitch, rows = interior_row_bytes(L)
-        for ch in self.grid.chunks:
-            g = self.placement[ch.lin]
-            st = stream_of(g)
-            ox, oy, oz = ch.offsets
-            base = self.bufs[ch.lin][parity]
+        for lin in self.owned:
+            ch = self.grid.chunks[lin]
+            st = stream_of(self.placement[lin])
+            ox, oy, oz = (o - l for o, l in zip(ch.offsets, self.box_lo))
+            base = self.bufs[lin][parity]
             if L.ndim == 2:
                 planes = [(_addr(L, base, 1, 1, 0), field_ptr + F64 * (ox * Y + oy))]
                 fpitch = Y * F64
@@ -330,12 +414,12 @@ class JacobiSolver:
 
     # -- data in/out ----------------------------------------------------------
 
-    def upload(self, interior: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None):
-        """Initial interior (X,Y,Z) into buffer 0 of every chunk: one H2D of
-        the contiguous field, then device-side strided copies.  ``None`` is
-        the reference's initial state (interior 0.0, jacobi.py:385)."""
-        X, Y, Z = self.grid.domain
-        nbytes = X * Y * Z * F64
+    def upload(self, interior: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None,
+               sync: bool = True):
+        """Initial interior of the owned box into buffer 0 of every chunk: one
+        H2D of the contiguous field, then device-side strided copies.  ``None``
+        is the reference's initial state (interior 0.0, jacobi.py:385)."""
+        nbytes = self.field_elems * F64
         f = self._field()
         g0 = self.used_gpus[0]
         st0 = self.streams[g0]
@@ -343,8 +427,8 @@ class JacobiSolver:
             src_ptr = host.ptr
         elif interior is not None:
             arr = np.ascontiguousarray(interior, dtype=np.float64)
-            if arr.shape != (X, Y, Z):
-                raise HrtError(f"interior shape {arr.shape} != domain {(X, Y, Z)}")
+            if arr.shape != self.box:
+                raise HrtError(f"interior shape {arr.shape} != owned box {self.box}")
             src_ptr = arr.ctypes.data
         else:
             src_ptr = None
@@ -355,10 +439,10 @@ class JacobiSolver:
         self._fan_out(g0)
         self._chunk_copies(True, 0, f, lambda g: self.streams[g])
         self.steps_done = 0
-        self.sync()
+        if sync:
+            self.sync()
 
     def _fan_out(self, g0: int) -> None:
-        """Make every GPU's stream wait for GPU g0's stream."""
         if len(self.used_gpus) > 1:
             tok = self.streams[g0].record()
             for g in self.used_gpus:
@@ -371,8 +455,8 @@ class JacobiSolver:
                 self.streams[g0].wait(self.streams[g].record())
 
     def gather(self) -> int:
-        """Assemble the current field into the contiguous device staging
-        buffer (jacobi.py:425-435); returns its device address."""
+        """Assemble the owned box into the contiguous device staging buffer
+        (jacobi.py:425-435); returns its device address."""
         f = self._field()
         g0 = self.used_gpus[0]
         self._fan_in(g0)
@@ -380,16 +464,15 @@ class JacobiSolver:
         return f
 
     def download(self, out: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None):
-        X, Y, Z = self.grid.domain
-        nbytes = X * Y * Z * F64
+        nbytes = self.field_elems * F64
         f = self.gather()
         st0 = self.streams[self.used_gpus[0]]
         if host is not None:
             dst = host.ptr
-            out = host.array(np.float64, (X, Y, Z))
+            out = host.array(np.float64, self.box)
         else:
             if out is None:
-                out = np.empty((X, Y, Z), dtype=np.float64)
+                out = np.empty(self.box, dtype=np.float64)
             dst = out.ctypes.data
         N.call("hrt_copy_async", st0.h, ctypes.c_void_p(dst), ctypes.c_void_p(f), nbytes)
         st0.synchronize()
@@ -397,26 +480,24 @@ class JacobiSolver:
 
     def checksum(self) -> float:
         """float(np.sum(assembled)) (jacobi.py:436), bit-exact, on the GPU."""
-        X, Y, Z = self.grid.domain
+        if self.box != self.grid.domain:
+            raise HrtError("checksum needs the whole domain in this process")
         f = self.gather()
         out = ctypes.c_double()
-        N.call("hrt_np_sum", self.streams[self.used_gpus[0]].h, ctypes.c_void_p(f), X * Y * Z,
-               ctypes.byref(out))
+        N.call("hrt_np_sum", self.streams[self.used_gpus[0]].h, ctypes.c_void_p(f),
+               self.field_elems, ctypes.byref(out))
         return out.value
 
     # -- stepping -------------------------------------------------------------
 
     def reset_residual(self, steps: int) -> None:
         self.resid = {}
+        n = max(steps, 1)
         for g in self.used_gpus:
-            pool = self.pools[g]
-            if not hasattr(self, "_rbuf"):
-                self._rbuf = {}
-            if g not in self._rbuf or self._rbuf[g][1] < steps:
-                self._rbuf[g] = (DevicePool(g, max(steps, 1) * 8 + 256), max(steps, 1))
-            rp = self._rbuf[g][0]
-            ptr = rp.base
-            N.call("hrt_memset_async", self.streams[g].h, ctypes.c_void_p(ptr), 0, max(steps, 1) * 8)
+            if g not in self._rbuf or self._rbuf[g][1] < n:
+                self._rbuf[g] = (DevicePool(g, n * 8 + 256), n)
+            ptr = self._rbuf[g][0].base
+            N.call("hrt_memset_async", self.streams[g].h, ctypes.c_void_p(ptr), 0, n * 8)
             self.resid[g] = ptr
         self._resid_steps = steps
 
@@ -451,32 +532,35 @@ class JacobiSolver:
 
     def run_timed(self, steps: int, residual: bool = True):
         """run() with CUDA events around every launch (single GPU); returns
-        (update_ms_total, halo_ms_total, total_ms)."""
+        (update_ms_total, halo_ms_total, total_ms).  Synchronises."""
         if len(self.used_gpus) != 1:
             raise HrtError("run_timed drives a single GPU")
         if residual:
             self.reset_residual(self.steps_done + steps)
         g = self.used_gpus[0]
         up, ha, tot = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
-        N.call("hrt_jacobi_plan_run_timed", self.plans[g], self.streams[g].h, self.steps_done, steps,
-               ctypes.c_void_p(self.resid[g] if residual else 0), ctypes.byref(up),
+        N.call("hrt_jacobi_plan_run_timed", self.plans[g], self.streams[g].h, self.steps_done,
+               steps, ctypes.c_void_p(self.resid[g] if residual else 0), ctypes.byref(up),
                ctypes.byref(ha), ctypes.byref(tot))
         self.steps_done += steps
         return up.value, ha.value, tot.value
 
+    def residual_bits(self) -> dict[int, int]:
+        """device address of each GPU's residual history (uint64 bit patterns)."""
+        return dict(self.resid)
+
     def residual_history(self) -> np.ndarray:
-        """max |u_{s+1} - u_s| per step, max over GPUs (builder-defined; the
-        reference has no residual)."""
-        n = getattr(self, "_resid_steps", 0)
+        """max |u_{s+1} - u_s| per step, max over this process's GPUs
+        (builder-defined; the reference has no residual)."""
+        n = self._resid_steps
         out = np.zeros(n, dtype=np.uint64)
         for g in self.used_gpus:
-            if g not in self.resid:
+            if g not in self.resid or n == 0:
                 continue
             tmp = np.empty(n, dtype=np.uint64)
-            if n:
-                N.call("hrt_copy_async", self.streams[g].h, ctypes.c_void_p(tmp.ctypes.data),
-                       ctypes.c_void_p(self.resid[g]), n * 8)
-                self.streams[g].synchronize()
+            N.call("hrt_copy_async", self.streams[g].h, ctypes.c_void_p(tmp.ctypes.data),
+                   ctypes.c_void_p(self.resid[g]), n * 8)
+            self.streams[g].synchronize()
             out = np.maximum(out, tmp)
         return out.view(np.float64)
 
