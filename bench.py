@@ -1,0 +1,381 @@
+"""Headline benchmark: Jacobi GLUPS on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+One bench *step* is one complete job of the workload: the chunked field is
+reset to the reference's initial state (interior 0.0, Dirichlet 1.0,
+jacobi.py:382-395) and advanced ``iters`` Jacobi iterations (halo faces +
+7-point update + L-inf residual per iteration), exactly as
+run_jacobi3d(domain, grid=..., steps=iters) does (jacobi.py:281-462).
+
+* N=1: cfg2 — 16384^2 float64, 8x8 chunks, 1000 iterations (BASELINE
+  configs[1]).  N>1: cfg3 — 32768^2 float64, 8 chunks per GPU, 1000
+  iterations, one process per GPU, faces between processes by NCCL
+  send/recv inside libhrt_b200 (strong scaling).
+* ``value``: GLUPS with the field resident in HBM, CUDA events on the solver
+  stream, max over ranks.  ``e2e``: the same job through the public API
+  (JacobiSolver.upload from pinned host memory -> run -> download to pinned
+  host memory + residual history), H2D/D2H inside the timed region.
+* ``roofline``: the slab update kernel, 16 algorithmic bytes per lattice
+  update (read u, write u'), CUDA events around every update launch.
+* ``cpu_baseline``: the C/OpenMP oracle (oracle/, a port of the reference's
+  jacobi_reference) on this host's cores, bounded sample, rank 0 at N=1.
+* ``--impl reference``: the reference CPU path (the oracle port, all host
+  threads) on the same workload, bounded samples per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Jacobi GLUPS at 1/2/4/8 B200 (% HBM roofline); halo msg GB/s vs size"
+UNIT = "GLUPS"
+BYTES_PER_UPDATE = 16  # read u once, write u' once (float64)
+CFG3_GRIDS = {1: (2, 4, 1), 2: (4, 4, 1), 4: (8, 4, 1), 8: (8, 8, 1)}
+
+
+def workload(name: str, n: int):
+    if name == "auto":
+        name = "cfg2" if n == 1 else "cfg3"
+    if name == "cfg1":
+        return dict(name="cfg1", desc="Jacobi 2D 1024x1024 float64, 4x4 blocks, 100 iterations",
+                    domain=(1024, 1024, 1), grid=(4, 4, 1), iters=100)
+    if name == "cfg2":
+        return dict(name="cfg2",
+                    desc="Jacobi 2D 16384x16384 float64, 8x8 blocks, 1000 iterations on 1 B200",
+                    domain=(16384, 16384, 1), grid=(8, 8, 1), iters=1000)
+    if name == "cfg3":
+        grid = CFG3_GRIDS.get(n, (8, n, 1))
+        return dict(name="cfg3",
+                    desc=f"Jacobi 2D 32768x32768 float64 strong scaling, 8 blocks per GPU "
+                         f"(grid {grid[0]}x{grid[1]}), 1000 iterations on {n} B200",
+                    domain=(32768, 32768, 1), grid=grid, iters=1000)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1].split()[0]))
+                mx = max(mx, float(f[2].split()[0]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(wl, budget_s: float = 15.0):
+    """The C/OpenMP oracle (oracle/jacobi_oracle.c, port of jacobi.py:49-67)
+    on a bounded sample of the workload: the full domain, k sweeps."""
+    from oracle import oracle as O
+
+    O.build()
+    X, Y, _ = wl["domain"]
+    slab = O.CpuSlab(X, Y)
+    t0 = time.perf_counter()
+    slab.sweep(1)
+    t1 = time.perf_counter() - t0
+    k = max(2, min(wl["iters"], int(budget_s / max(t1, 1e-4))))
+    t0 = time.perf_counter()
+    slab.sweep(k)
+    dt = time.perf_counter() - t0
+    slab.close()
+    return {"value": round(X * Y * k / dt / 1e9, 4), "unit": UNIT, "cores": O.cpu_threads(),
+            "kind": "port",
+            "sample": f"{X}x{Y} slab, {k} of the {wl['iters']} sweeps ({dt:.1f} s, setup "
+                      f"excluded), oracle/jacobi_oracle.c OpenMP, host of the GPU box"}
+
+
+def reduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def run_ours(args):
+    from paper_2303_02543_b200 import _native as N
+    from paper_2303_02543_b200.devices import PinnedBuffer
+    from paper_2303_02543_b200.distributed import DistributedJacobi, init_process
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    rank, world, local = init_process("nccl") if args.gpus > 1 else (0, 1, 0)
+    N.require_gpu(local)
+    wl = workload(args.workload, world)
+    iters = args.iters or wl["iters"]
+    X, Y, Z = wl["domain"]
+    cells = X * Y * Z
+    grid = ChunkGrid(wl["domain"], ranks=world, grid=wl["grid"])
+    if world == 1:
+        solver = JacobiSolver(grid, gpus=[local], variant=args.variant, rows=args.rows)
+    else:
+        solver = DistributedJacobi(grid, rank, world, local, variant=args.variant, rows=args.rows)
+    my_cells = solver.field_elems
+    nbytes = my_cells * 8
+    host_in = PinnedBuffer(nbytes)
+    host_in.array(dtype="float64")[:] = 0.0          # the reference's initial interior
+    host_out = PinnedBuffer(nbytes)
+    g = solver.used_gpus[0]
+    st = solver.streams[g]
+
+    solver.upload(host=host_in)
+    # the resident initial state for the device-timed job: keep a copy on HBM
+    init_field = solver._field()
+
+    def device_job():
+        """reset to the initial state (device-resident) + iters iterations;
+        returns (update_ms, halo_ms, total_ms) from CUDA events."""
+        solver._chunk_copies(True, 0, init_field, lambda gg: solver.streams[gg])
+        solver.steps_done = 0
+        return solver.run_timed(iters, residual=True)
+
+    # warm-up (also instantiates plans/graphs, faults in pages)
+    for _ in range(args.warmup):
+        device_job()
+    barrier(world)
+    st.synchronize()
+    upd = halo = tot = 0.0
+    with ClockSampler(local) as clk:
+        t_start = st.record()
+        for _ in range(args.steps):
+            u, h, t = device_job()
+            upd += u
+            halo += h
+            tot += t
+        t_end = st.record()
+        st.synchronize()
+    region_ms = t_start_elapsed = 0.0
+    import ctypes
+
+    ms = ctypes.c_float()
+    N.call("hrt_token_elapsed_ms", ctypes.c_uint64(t_start.token_id), ctypes.c_uint64(t_end.token_id),
+           ctypes.byref(ms))
+    region_ms = reduce_max(ms.value, world)
+    barrier(world)
+    value = cells * iters * args.steps / (region_ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (slab update): per-launch algorithmic
+    # bytes / average launch duration (events around every launch)
+    avg_upd_ms = upd / (args.steps * iters)
+    achieved = BYTES_PER_UPDATE * my_cells / (avg_upd_ms / 1e3) / 1e9
+    peak, peak_src = peaks()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": args.traffic,
+                "kernel": "slab_update_tma_kernel" if (args.variant in (None, 1)) else
+                "slab_update_kernel",
+                "bytes_per_launch": BYTES_PER_UPDATE * my_cells,
+                "avg_launch_ms": round(avg_upd_ms, 5), "peak_source": peak_src,
+                "update_share_of_step": round(upd / tot, 4) if tot else None,
+                "halo_share_of_step": round(halo / tot, 4) if tot else None}
+
+    # end to end through the public API with pinned host buffers
+    e2e_ms = 0.0
+    for k in range(args.e2e_steps + 1):
+        barrier(world)
+        st.synchronize()
+        t0 = st.record()
+        solver.upload(host=host_in, sync=False)
+        solver.run(iters, residual=True)
+        solver.download(host=host_out)
+        if world > 1:
+            res = solver.global_residual_history()
+        else:
+            res = solver.residual_history()
+        t1 = st.record()
+        st.synchronize()
+        N.call("hrt_token_elapsed_ms", ctypes.c_uint64(t0.token_id), ctypes.c_uint64(t1.token_id),
+               ctypes.byref(ms))
+        if k > 0:  # first one is the e2e warm-up
+            e2e_ms += ms.value
+    e2e_ms = reduce_max(e2e_ms, world)
+    e2e_value = cells * iters * args.e2e_steps / (e2e_ms / 1e3) / 1e9
+    h2d = nbytes * world
+    d2h = nbytes * world + 8 * iters * world
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(region_ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: the reference's initial state (interior 0.0, Dirichlet faces 1.0)",
+        "config": {"workload": wl["desc"], "domain": list(wl["domain"]), "grid": list(wl["grid"]),
+                   "iterations_per_step": iters, "chunks_per_gpu": len(solver.owned),
+                   "parallelism": f"domain decomposition over {world} GPU(s), one process each",
+                   "l2": f"no flush needed: field {cells * 8 / 2**30:.2f} GiB >> 126 MB L2",
+                   "bitexact": "float64 bitwise == reference (Markstein /6 == IEEE, sum order kept)",
+                   "residual": "L-inf per iteration, fused"},
+        "roofline": roofline,
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "what": "JacobiSolver.upload(pinned) + run(iters) + download(pinned) + residual"},
+        "gpu_launches": 2 * iters * args.steps,
+        "halo_faces_per_gpu": solver.n_faces, "remote_faces_per_gpu": solver.n_remote,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, args.cpu_budget)
+    else:
+        line["cpu_baseline"] = None
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference CPU path = the oracle port (the reference is pure Python and
+    cannot be compiled), all host threads, bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    O.build()
+    wl = workload(args.workload, world if args.gpus > 1 else 1)
+    X, Y, _ = wl["domain"]
+    slab = O.CpuSlab(X, Y)
+    t0 = time.perf_counter()
+    slab.sweep(1)
+    t1 = time.perf_counter() - t0
+    per_step = max(1, min(wl["iters"], int(args.ref_step_budget / max(t1, 1e-4))))
+    for _ in range(args.warmup):
+        slab.sweep(per_step)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        slab.sweep(per_step)
+    dt = time.perf_counter() - t0
+    slab.close()
+    value = X * Y * per_step * args.steps / dt / 1e9
+    cores = O.cpu_threads()
+    sample = (f"{X}x{Y} slab, {per_step} of the {wl["iters"]} sweeps per step (field setup "
+              f"excluded), oracle/jacobi_oracle.c OpenMP port of jacobi.py:49-67")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: the reference's initial state",
+        "config": {"workload": wl["desc"], "domain": list(wl["domain"]), "grid": list(wl["grid"]),
+                   "iterations_per_step": per_step},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--iters", type=int, default=0, help="override iterations per job")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--variant", type=int, default=None, help="slab kernel: 0 LDG, 1 TMA")
+    ap.add_argument("--rows", type=int, default=None)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per update launch (from profiles/)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-step-budget", type=float, default=3.0)
+    args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("need --steps >= 1")
+    if args.traffic is None:
+        args.traffic = _recorded_traffic()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+def _recorded_traffic():
+    """dram read+write bytes per update launch from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get("bytes_per_launch")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

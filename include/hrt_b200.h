@@ -143,6 +143,8 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t *layout, int nchunk
 int hrt_jacobi_plan_set_remote(void *plan, void *comm, const hrt_remote_seg_t *remote,
                                int nremote, const hrt_halo_seg_t *post, int npost);
 int hrt_jacobi_plan_set_rows(void *plan, int64_t rows);
+/* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring (default) */
+int hrt_jacobi_plan_set_variant(void *plan, int variant);
 /* one step: halo faces, then the 7-point update of every chunk (_update_body
  * jacobi.py:70-79); resid (nullable, device, uint64 bit patterns of float64)
  * receives max|u'-u| at index `step` via atomicMax (must start zeroed). */

@@ -173,8 +173,72 @@ static double pairwise(const double *a, int64_t n) {
 /* float(np.sum(a)) for a contiguous float64 array (jacobi.py:436). */
 double oracle_np_sum(const double *a, int64_t n) { return 0.0 + pairwise(a, n); }
 
-/* Largest single step of the cfg1/cfg2 sweep, timed by bench.py's CPU leg:
- * `steps` sweeps of the slab, interior written to nowhere.  Returns 0. */
+/* Persistent slab state for bench.py's timed CPU legs: setup (allocation,
+ * first touch) is excluded from the timed sweeps, like the survey's
+ * per-step differencing of the reference. */
+typedef struct {
+    int64_t X, Y;
+    double *u, *v;
+} oracle_slab_t;
+
+void *oracle_slab_new(int64_t X, int64_t Y) {
+    const int64_t X2 = X + 2, Y2 = Y + 2;
+    oracle_slab_t *h = (oracle_slab_t *)calloc(1, sizeof(oracle_slab_t));
+    if (!h) return NULL;
+    h->X = X;
+    h->Y = Y;
+    h->u = (double *)malloc((size_t)X2 * Y2 * sizeof(double));
+    h->v = (double *)malloc((size_t)X2 * Y2 * sizeof(double));
+    if (!h->u || !h->v) { free(h->u); free(h->v); free(h); return NULL; }
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < X2; ++i)
+        for (int64_t j = 0; j < Y2; ++j) {
+            int ghost = (i == 0 || i == X2 - 1 || j == 0 || j == Y2 - 1);
+            h->u[i * Y2 + j] = h->v[i * Y2 + j] = ghost ? BOUNDARY : 0.0;
+        }
+    return h;
+}
+
+/* `steps` sweeps (same arithmetic as oracle_jacobi2d); returns the last
+ * step's residual. */
+double oracle_slab_sweep(void *handle, int64_t steps) {
+    oracle_slab_t *h = (oracle_slab_t *)handle;
+    const int64_t X = h->X, Y = h->Y, Y2 = Y + 2;
+    double rmax = 0.0;
+    for (int64_t s = 0; s < steps; ++s) {
+        double *u = h->u, *v = h->v;
+        rmax = 0.0;
+        #pragma omp parallel for schedule(static) reduction(max : rmax)
+        for (int64_t i = 1; i <= X; ++i) {
+            const double *up = u + (i - 1) * Y2, *mid = u + i * Y2, *dn = u + (i + 1) * Y2;
+            double *out = v + i * Y2;
+            for (int64_t j = 1; j <= Y; ++j) {
+                double acc = up[j] + dn[j];
+                acc = acc + mid[j - 1];
+                acc = acc + mid[j + 1];
+                acc = acc + BOUNDARY;
+                acc = acc + BOUNDARY;
+                double nv = acc / 6.0;
+                double d = fabs(nv - mid[j]);
+                if (d > rmax) rmax = d;
+                out[j] = nv;
+            }
+        }
+        h->u = v;
+        h->v = u;
+    }
+    return rmax;
+}
+
+void oracle_slab_free(void *handle) {
+    oracle_slab_t *h = (oracle_slab_t *)handle;
+    if (!h) return;
+    free(h->u);
+    free(h->v);
+    free(h);
+}
+
+/* `steps` sweeps of a fresh slab (setup included).  Returns 0. */
 int oracle_jacobi2d_sweeps(int64_t X, int64_t Y, int64_t steps) {
     return oracle_jacobi2d(X, Y, steps, NULL, NULL);
 }

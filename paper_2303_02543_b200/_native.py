@@ -86,6 +86,7 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_remote": (c_int, [c_void_p, c_void_p, P(RemoteSeg), c_int, P(HaloSeg),
                                            c_int]),
     "hrt_jacobi_plan_set_rows": (c_int, [c_void_p, c_i64]),
+    "hrt_jacobi_plan_set_variant": (c_int, [c_void_p, c_int]),
     "hrt_jacobi_plan_step": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "hrt_jacobi_plan_update": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
     "hrt_jacobi_plan_halo": (c_int, [c_void_p, c_void_p, c_int]),

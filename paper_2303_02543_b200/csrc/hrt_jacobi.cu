@@ -202,6 +202,160 @@ slab_update_kernel(SlabArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// slab update, TMA variant: one producer thread streams the tile's rows
+// (each row segment incl. the two neighbour columns is one contiguous
+// 16-byte-aligned span) global -> shared with cp.async.bulk into a ring of
+// TMA_STAGES stages guarded by mbarriers (full: transaction bytes;
+// empty: one arrival per consumer warp).  Consumer warps read a row once
+// (double2 + left + right from shared memory: no shuffles, no edge loads),
+// release the stage, and keep the 3-row window in registers.
+
+constexpr int TMA_CONSUMER_WARPS = 4;
+constexpr int TMA_THREADS = 32 * (TMA_CONSUMER_WARPS + 1);
+constexpr int TMA_COLS = 64 * TMA_CONSUMER_WARPS;    // 2 columns per consumer thread
+constexpr int TMA_ROW = TMA_COLS + 4;                // + cols j0-2, j0-1 .. j0+W, j0+W+1
+constexpr int TMA_STAGES = 12;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_row_load(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(TMA_THREADS)
+slab_update_tma_kernel(SlabArgs a) {
+    __shared__ alignas(128) double ring[TMA_STAGES][TMA_ROW];
+    __shared__ alignas(8) uint64_t full[TMA_STAGES], empty[TMA_STAGES];
+    __shared__ double red[TMA_CONSUMER_WARPS];
+
+    const int64_t per_chunk = a.tiles_r * a.tiles_c;
+    const int64_t t = blockIdx.x;
+    const int64_t c = t / per_chunk;
+    const int64_t rem = t - c * per_chunk;
+    const int64_t rb = rem / a.tiles_c;
+    const int64_t cb = rem - rb * a.tiles_c;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    const double* __restrict__ u = a.chunks[c].b[a.parity] + a.origin;
+    double* __restrict__ w = a.chunks[c].b[a.parity ^ 1] + a.origin;
+    const int64_t j0 = 1 + cb * TMA_COLS;
+    const int64_t last = min(j0 + TMA_COLS - 1, a.ey);
+    const uint32_t nload = (uint32_t)(((last - j0 + 4) + 1) & ~int64_t(1));
+    const uint32_t bytes = nload * 8u;
+    const int64_t i0 = 1 + rb * a.rows;
+    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+    const int nrows = (int)(i1 - i0 + 3);  // rows i0-1 .. i1+1
+
+    if (tid == 0) {
+        for (int s = 0; s < TMA_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], TMA_CONSUMER_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == TMA_CONSUMER_WARPS) {
+        // producer
+        if (lane == 0) {
+            const double* src = u + (i0 - 1) * a.sx + (j0 - 2);
+            for (int q = 0; q < nrows; ++q) {
+                const int s = q % TMA_STAGES;
+                if (q >= TMA_STAGES) mbar_wait(&empty[s], ((q / TMA_STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], bytes);
+                tma_row_load(&ring[s][0], src + (int64_t)q * a.sx, bytes, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // consumers: thread owns columns j, j+1 -> ring positions p = 2*tid+2, +3
+    const int64_t j = j0 + 2 * tid;
+    const bool act = j <= a.ey;
+    const bool both = j + 1 <= a.ey;
+    const int p = 2 * tid + 2;
+    const double zg = a.zghost;
+    double rmax = 0.0;
+
+    auto take = [&](int q, double2& v, double& l, double& r) {
+        const int s = q % TMA_STAGES;
+        mbar_wait(&full[s], (q / TMA_STAGES) & 1);
+        v = *reinterpret_cast<const double2*>(&ring[s][p]);
+        l = ring[s][p - 1];
+        r = ring[s][p + 2];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    };
+
+    double2 up, mid, dn;
+    double lx, ry, dl, dr, tl, tr;
+    take(0, up, tl, tr);
+    take(1, mid, lx, ry);
+    for (int q = 2; q < nrows; ++q) {
+        take(q, dn, dl, dr);
+        if (act) {
+            const int64_t r = i0 - 2 + q;
+            double2 o;
+            o.x = div6(sum6(up.x, dn.x, lx, mid.y, zg, zg));
+            o.y = div6(sum6(up.y, dn.y, mid.x, ry, zg, zg));
+            double* dst = w + r * a.sx + j;
+            if (both) {
+                *reinterpret_cast<double2*>(dst) = o;
+                rmax = fmax(rmax, fmax(fabs(__dsub_rn(o.x, mid.x)), fabs(__dsub_rn(o.y, mid.y))));
+            } else {
+                dst[0] = o.x;
+                rmax = fmax(rmax, fabs(__dsub_rn(o.x, mid.x)));
+            }
+        }
+        up = mid;
+        mid = dn;
+        lx = dl;
+        ry = dr;
+    }
+
+    if (a.resid) {
+        rmax = warp_max(rmax);
+        if (lane == 0) red[warp] = rmax;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * TMA_CONSUMER_WARPS));
+        if (tid == 0) {
+            double m = red[0];
+#pragma unroll
+            for (int k = 1; k < TMA_CONSUMER_WARPS; ++k) m = fmax(m, red[k]);
+            resid_max(a.resid, m);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // volume update: general (X,Y,Z) domains; element (i,j,k) at
 // base + origin + i*sx + j*sy + k.  Threads tile (j,k), march i.
 
@@ -461,6 +615,7 @@ struct Plan {
     std::vector<hrt_remote_seg_t> remote;
     void* comm = nullptr;
     int64_t rows = 64;
+    int variant = 1;  // slab kernel: 0 LDG register march, 1 TMA ring
     // graph of two steps (parity 0 then 1) per residual base pointer
     cudaGraphExec_t graph = nullptr;
     unsigned long long* graph_resid = nullptr;
@@ -499,7 +654,10 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.zghost = HRT_BOUNDARY;
         const int64_t grid = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
         if (grid == 0) return HRT_OK;
-        slab_update_kernel<<<(unsigned)grid, SLAB_THREADS, 0, s>>>(a);
+        if (p->variant == 1)
+            slab_update_tma_kernel<<<(unsigned)grid, TMA_THREADS, 0, s>>>(a);
+        else
+            slab_update_kernel<<<(unsigned)grid, SLAB_THREADS, 0, s>>>(a);
     } else {
         VolArgs a;
         a.chunks = p->d_chunks;
@@ -610,6 +768,17 @@ int hrt_jacobi_plan_set_rows(void* plan, int64_t rows) {
     HRT_CHECK_ARG(plan && rows > 0, "bad rows");
     Plan* p = reinterpret_cast<Plan*>(plan);
     p->rows = rows;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_variant(void* plan, int variant) {
+    HRT_CHECK_ARG(plan && (variant == 0 || variant == 1), "variant must be 0 or 1");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    p->variant = variant;
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;

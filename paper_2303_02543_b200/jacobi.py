@@ -23,6 +23,7 @@ rank and GPU count (same float operations in the same order per cell).
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -129,7 +130,9 @@ def chunk_layout(ext, slab: bool) -> N.ChunkLayout:
     if slab:
         if ez != 1:
             raise HrtError("slab layout needs ez == 1")
-        sx = -(-(ey + 17) // 16) * 16
+        # >= 19 spare elements per row: 15 before the ghost column (alignment)
+        # and the TMA variant's row span reaching column ey+2
+        sx = -(-(ey + 20) // 16) * 16
         L.ndim = 2
         L.stride[0], L.stride[1], L.stride[2] = sx, 1, 0
         L.origin = 15
@@ -219,8 +222,10 @@ class JacobiSolver:
 
     def __init__(self, grid: ChunkGrid, gpus: Optional[Sequence[int]] = None,
                  placement: Optional[dict[int, int]] = None, rows: Optional[int] = None,
-                 rank: Optional[int] = None, comm=None):
+                 rank: Optional[int] = None, comm=None, variant: Optional[int] = None):
         N.require_gpu(0)
+        if variant is None and os.environ.get("HRT_SLAB_VARIANT"):
+            variant = int(os.environ["HRT_SLAB_VARIANT"])
         ngpu = N.gpu_count()
         self.grid = grid
         self.rank = rank
@@ -320,6 +325,8 @@ class JacobiSolver:
                    len(pre[g]), ctypes.byref(plan))
             if rows:
                 N.call("hrt_jacobi_plan_set_rows", plan, rows)
+            if variant is not None:
+                N.call("hrt_jacobi_plan_set_variant", plan, variant)
             if g == g0 and remote_ops:
                 N.call("hrt_jacobi_plan_set_remote", plan, ctypes.c_void_p(comm),
                        _arr(N.RemoteSeg, remote_ops), len(remote_ops), _arr(N.HaloSeg, post),

@@ -15,8 +15,10 @@ steps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 rows_list = [int(r) for r in sys.argv[2:]] or [64]
 X = Y = 16384
 cells = X * Y
-for rows in rows_list:
-    s = JacobiSolver(ChunkGrid((X, Y, 1), grid=(8, 8, 1)), rows=rows)
+variants = [int(v) for v in os.environ.get("PROBE_VARIANTS", "0,1").split(",")]
+for variant, rows in [(v, r) for v in variants for r in rows_list]:
+    print(f"variant {variant}", end=" ")
+    s = JacobiSolver(ChunkGrid((X, Y, 1), grid=(8, 8, 1)), rows=rows, variant=variant)
     s.upload()
     s.run_timed(5)
     up, ha, tot = s.run_timed(steps)
