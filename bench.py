@@ -190,7 +190,7 @@ def run_ours(args):
     g = solver.used_gpus[0]
     st = solver.streams[g]
 
-    solver.upload(host=host_in)
+    solver.upload(host=host_in, nonneg=True)
     # the resident initial state for the device-timed job: keep a copy on HBM
     init_field = solver._field()
 
@@ -233,8 +233,9 @@ def run_ours(args):
     peak, peak_src = peaks()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": args.traffic,
-                "kernel": "slab_update_tma_kernel" if (args.variant in (None, 1)) else
-                "slab_update_kernel",
+                "kernel": {None: "slab_update_tma4_kernel<false,true>",
+                           2: "slab_update_tma4_kernel<false,true>",
+                           1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant],
                 "bytes_per_launch": BYTES_PER_UPDATE * my_cells,
                 "avg_launch_ms": round(avg_upd_ms, 5), "peak_source": peak_src,
                 "update_share_of_step": round(upd / tot, 4) if tot else None,
@@ -246,7 +247,7 @@ def run_ours(args):
         barrier(world)
         st.synchronize()
         t0 = st.record()
-        solver.upload(host=host_in, sync=False)
+        solver.upload(host=host_in, sync=False, nonneg=True)
         solver.run(iters, residual=True)
         solver.download(host=host_out)
         if world > 1:

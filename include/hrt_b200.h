@@ -143,8 +143,13 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t *layout, int nchunk
 int hrt_jacobi_plan_set_remote(void *plan, void *comm, const hrt_remote_seg_t *remote,
                                int nremote, const hrt_halo_seg_t *post, int npost);
 int hrt_jacobi_plan_set_rows(void *plan, int64_t rows);
-/* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring (default) */
+/* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,
+ * 2 = TMA ring with four columns per thread (default) */
 int hrt_jacobi_plan_set_variant(void *plan, int variant);
+/* caller guarantees a finite, non-negative field (the reference's problem):
+ * the slab kernel's six-term sum is then >= 2 and the division needs no
+ * subnormal/special-value guard */
+int hrt_jacobi_plan_set_nonneg(void *plan, int nonneg);
 /* one step: halo faces, then the 7-point update of every chunk (_update_body
  * jacobi.py:70-79); resid (nullable, device, uint64 bit patterns of float64)
  * receives max|u'-u| at index `step` via atomicMax (must start zeroed). */

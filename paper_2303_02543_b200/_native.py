@@ -87,6 +87,7 @@ SIGNATURES = {
                                            c_int]),
     "hrt_jacobi_plan_set_rows": (c_int, [c_void_p, c_i64]),
     "hrt_jacobi_plan_set_variant": (c_int, [c_void_p, c_int]),
+    "hrt_jacobi_plan_set_nonneg": (c_int, [c_void_p, c_int]),
     "hrt_jacobi_plan_step": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "hrt_jacobi_plan_update": (c_int, [c_void_p, c_void_p, c_int, c_void_p]),
     "hrt_jacobi_plan_halo": (c_int, [c_void_p, c_void_p, c_int]),

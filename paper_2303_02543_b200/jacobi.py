@@ -201,6 +201,45 @@ def _arr(ctype, items):
 # the per-process engine
 
 
+def remote_faces(grid: ChunkGrid, rank: int) -> list[tuple[int, int, int]]:
+    """Faces crossing a process boundary that involve ``rank``, as
+    (destination chunk, face, source chunk) in one canonical global order
+    (destination lin, then face).  The source chunk's rank sends its boundary
+    plane opposite(face); the destination's rank receives it into the ghost
+    plane ``face`` — the reference's per-face mp_send (jacobi.py:227-237).
+    Every rank derives the same order, so the k-th send from A to B pairs
+    with the k-th receive on B from A (NCCL's in-order matching)."""
+    out = []
+    for ch in grid.chunks:
+        for f, nb in sorted(ch.neighbors.items()):
+            src_rank, dst_rank = grid.chunks[nb].rank, ch.rank
+            if src_rank != dst_rank and rank in (src_rank, dst_rank):
+                out.append((ch.lin, f, nb))
+    return out
+
+
+def remote_ops(grid: ChunkGrid, rank: int) -> list[tuple[str, int, int, int, int]]:
+    """The NCCL op list of ``rank``: (kind 'send'|'recv', peer, dst chunk,
+    face, element count), in issue order."""
+    ext = grid.ext
+    ops = []
+    for c, f, nb in remote_faces(grid, rank):
+        axis = FACES[f][0]
+        count = 1
+        for a in range(3):
+            if a != axis:
+                count *= ext[a]
+        if grid.chunks[nb].rank == rank:
+            ops.append(("send", grid.chunks[c].rank, c, f, count))
+        else:
+            ops.append(("recv", grid.chunks[nb].rank, c, f, count))
+    return ops
+
+
+def _nonneg(a: np.ndarray) -> bool:
+    return bool(np.isfinite(a).all() and (a >= 0).all())
+
+
 def _contiguous(n0, n1, s0, s1) -> bool:
     return n0 * n1 == 0 or (s1 == 1 and (n0 == 1 or s0 == n1))
 
@@ -249,14 +288,7 @@ class JacobiSolver:
         self.used_gpus = sorted({placement[lin] for lin in owned})
         self.streams = {g: Stream(g, name=f"jacobi{g}") for g in self.used_gpus}
         self.rank_of = {ch.lin: ch.rank for ch in grid.chunks}
-        # remote messages (dst chunk, face) in canonical global order
-        remote_msgs = []
-        if rank is not None:
-            for ch in grid.chunks:
-                for f, nb in sorted(ch.neighbors.items()):
-                    if self.rank_of[nb] != self.rank_of[ch.lin] and rank in (
-                            self.rank_of[nb], self.rank_of[ch.lin]):
-                        remote_msgs.append((ch.lin, f, nb))
+        remote_msgs = remote_faces(grid, rank) if rank is not None else []
         # storage: two buffers per owned chunk (+ staging for strided remote planes)
         staging = 0
         for (c, f, nb) in remote_msgs:
@@ -332,6 +364,8 @@ class JacobiSolver:
                        _arr(N.RemoteSeg, remote_ops), len(remote_ops), _arr(N.HaloSeg, post),
                        len(post))
             self.plans[g] = plan
+        self.nonneg = None
+        self._set_nonneg(True)  # the reference's initial state: interior 0.0, faces 1.0
         self.n_remote = len(remote_ops)
         self.n_faces = sum(len(v) for v in pre.values())
         self.resid: dict[int, int] = {}
@@ -346,6 +380,15 @@ class JacobiSolver:
         self.box_lo = tuple(lo)
         self.box = tuple(h - l for l, h in zip(lo, hi))
         self._init_ghosts()
+
+    def _set_nonneg(self, flag: bool) -> None:
+        """A finite field >= 0 stays so under the update (sums of non-negative
+        values over 6 with the 1.0 boundary); the slab kernel then skips the
+        division's range check (its six-term sum is >= 2)."""
+        if flag != self.nonneg:
+            for plan in self.plans.values():
+                N.call("hrt_jacobi_plan_set_nonneg", plan, 1 if flag else 0)
+            self.nonneg = flag
 
     @staticmethod
     def _remote(addrs, count, peer, kind) -> N.RemoteSeg:
@@ -422,23 +465,29 @@ class JacobiSolver:
     # -- data in/out ----------------------------------------------------------
 
     def upload(self, interior: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None,
-               sync: bool = True):
+               sync: bool = True, nonneg: Optional[bool] = None):
         """Initial interior of the owned box into buffer 0 of every chunk: one
         H2D of the contiguous field, then device-side strided copies.  ``None``
-        is the reference's initial state (interior 0.0, jacobi.py:385)."""
+        is the reference's initial state (interior 0.0, jacobi.py:385).
+        ``nonneg`` asserts (or, if None, checks on the host) that the data are
+        finite and >= 0, which selects the unguarded division."""
         nbytes = self.field_elems * F64
         f = self._field()
         g0 = self.used_gpus[0]
         st0 = self.streams[g0]
         if host is not None:
             src_ptr = host.ptr
+            self._set_nonneg(bool(nonneg) if nonneg is not None else _nonneg(
+                host.array(np.float64, self.box)))
         elif interior is not None:
             arr = np.ascontiguousarray(interior, dtype=np.float64)
             if arr.shape != self.box:
                 raise HrtError(f"interior shape {arr.shape} != owned box {self.box}")
             src_ptr = arr.ctypes.data
+            self._set_nonneg(bool(nonneg) if nonneg is not None else _nonneg(arr))
         else:
             src_ptr = None
+            self._set_nonneg(True)
         if src_ptr is None:
             N.call("hrt_memset_async", st0.h, ctypes.c_void_p(f), 0, nbytes)
         else:

@@ -115,3 +115,39 @@ def test_full_size_properties(hrt):
     assert np.array_equal(a, a[::-1])
     assert a.min() > 0.0 and a.max() <= 1.0
     assert np.all(ra[1:] <= ra[:-1] * 1.0000001 + 1e-300) or ra[-1] < ra[0]
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_kernel_variants_bitwise(hrt, oracle, variant):
+    """Every slab kernel variant (LDG march, TMA ring, TMA ring x4) on a
+    ragged decomposition whose chunk width is not a multiple of the tile."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    dom, steps = (300, 1030, 1), 41
+    s = JacobiSolver(ChunkGrid(dom, grid=(3, 2, 1)), variant=variant, rows=37)
+    s.upload()
+    s.run(steps)
+    got, res = s.download(), s.residual_history()
+    s.close()
+    ref, rref = oracle.jacobi_c(dom, steps, residual=True)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(res, rref)
+
+
+@pytest.mark.parametrize("dom,grid", [((40, 70, 1), (4, 5, 1)), ((10, 12, 14), (2, 3, 2))])
+def test_arbitrary_initial_data_guarded_division(hrt, oracle, dom, grid):
+    """Signed, tiny (subnormal-quotient) and large initial data: the solver
+    detects the field is not non-negative and keeps the division guard."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    rng = np.random.default_rng(7)
+    init = rng.standard_normal(dom) * rng.choice([1e-310, 1e-300, 1.0, 1e300], size=dom)
+    for steps in (1, 6):
+        s = JacobiSolver(ChunkGrid(dom, grid=grid))
+        s.upload(init)
+        assert s.nonneg is False
+        s.run(steps, residual=False)
+        got = s.download()
+        s.close()
+        ref = oracle.jacobi_reference(dom, steps, initial=init)
+        assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
