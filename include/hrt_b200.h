@@ -167,6 +167,14 @@ int hrt_jacobi_plan_destroy(void *plan);
 /* standalone plane copies (halo_pack_f / halo_unpack_f bodies); segs on device */
 int hrt_halo_copy(void *stream, const hrt_halo_seg_t *segs_dev, int nsegs, int parity,
                   int64_t max_elems);
+/* one plane copy described by value (uses src[0]/dst[0]) — a pack or unpack
+ * task body (jacobi.py:102-124) */
+int hrt_plane_copy(void *stream, const hrt_halo_seg_t *seg);
+/* one chunk in the reference's dense ghosted (ex+2,ey+2,ez+2) layout,
+ * u -> nxt exactly as _update_body (jacobi.py:70-86): interior update + ghost
+ * shell carry; resid_slot (nullable) gets max|nxt-u| via atomicMax */
+int hrt_jacobi_chunk_update(void *stream, const double *u, double *nxt, int64_t ex, int64_t ey,
+                            int64_t ez, uint64_t *resid_slot);
 /* ghost shell of one chunk buffer: faces in `mask` (bit f = FACES[f],
  * jacobi.py:41) get `value` (Dirichlet, jacobi.py:386-393), others 0 */
 int hrt_jacobi_ghost_fill(void *stream, double *base, const hrt_chunk_layout_t *layout,

@@ -96,6 +96,9 @@ SIGNATURES = {
                                           P(c_d), P(c_d)]),
     "hrt_jacobi_plan_destroy": (c_int, [c_void_p]),
     "hrt_halo_copy": (c_int, [c_void_p, c_void_p, c_int, c_int, c_i64]),
+    "hrt_plane_copy": (c_int, [c_void_p, P(HaloSeg)]),
+    "hrt_jacobi_chunk_update": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_i64,
+                                        c_void_p]),
     "hrt_jacobi_ghost_fill": (c_int, [c_void_p, c_void_p, P(ChunkLayout), c_int, c_d]),
     "hrt_np_sum": (c_int, [c_void_p, c_void_p, c_i64, P(c_d)]),
     "hrt_div6_sweep": (c_int, [c_void_p, c_u64, c_i64, c_int, P(c_u64), P(c_d)]),

@@ -606,6 +606,38 @@ halo_copy_kernel(const hrt_halo_seg_t* __restrict__ segs, int parity, int64_t bl
     }
 }
 
+// one plane copy passed by value (standalone pack/unpack tasks)
+__global__ void __launch_bounds__(HALO_THREADS) plane_copy_kernel(hrt_halo_seg_t g) {
+    const double* __restrict__ src = reinterpret_cast<const double*>(g.src[0]);
+    double* __restrict__ dst = reinterpret_cast<double*>(g.dst[0]);
+    const int64_t n = g.n0 * g.n1;
+    for (int64_t e = blockIdx.x * (int64_t)HALO_THREADS + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * HALO_THREADS) {
+        const int64_t o = e / g.n1, i = e - o * g.n1;
+        dst[o * g.ds0 + i * g.ds1] = src[o * g.ss0 + i * g.ss1];
+    }
+}
+
+// ghost shell carry of _update_body (jacobi.py:80-86): nxt's six ghost
+// planes = u's, for a volume-layout chunk (z ghosts stored)
+__global__ void ghost_shell_copy_kernel(const double* __restrict__ u, double* __restrict__ w,
+                                        int64_t ex, int64_t ey, int64_t ez, int64_t sx,
+                                        int64_t sy) {
+    const int64_t gx = ex + 2, gy = ey + 2, gz = ez + 2;
+    const int64_t n = gx * gy * gz;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / (gy * gz);
+        const int64_t r = e - i * gy * gz;
+        const int64_t j = r / gz;
+        const int64_t k = r - j * gz;
+        if (i == 0 || i == gx - 1 || j == 0 || j == gy - 1 || k == 0 || k == gz - 1) {
+            const int64_t off = i * sx + j * sy + k;
+            w[off] = u[off];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // ghost initialisation: set the ghost shell of a chunk buffer to `value`
 // for faces in `mask` (bit f = face f of jacobi.py:41 FACES) and 0 elsewhere.
@@ -850,6 +882,9 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.tiles_i = (a.ex + a.rows - 1) / a.rows;
         a.tiles_j = (a.ey + VOL_TY - 1) / VOL_TY;
         a.tiles_k = (a.ez + VOL_TX - 1) / VOL_TX;
+        a.du = nullptr;
+        a.dw = nullptr;
+        a.flat = 0;
         a.resid = resid;
         const int64_t grid = (int64_t)p->nchunks * a.tiles_i * a.tiles_j * a.tiles_k;
         if (grid == 0) return HRT_OK;
@@ -1152,6 +1187,56 @@ int hrt_halo_copy(void* stream, const hrt_halo_seg_t* segs_dev, int nsegs, int p
     int64_t bps = std::max<int64_t>(
         1, (max_elems + HALO_THREADS * HALO_PER_THREAD - 1) / (HALO_THREADS * HALO_PER_THREAD));
     halo_copy_kernel<<<(unsigned)(nsegs * bps), HALO_THREADS, 0, st->s>>>(segs_dev, parity & 1, bps);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
+int hrt_plane_copy(void* stream, const hrt_halo_seg_t* seg) {
+    HRT_CHECK_ARG(stream && seg, "null argument");
+    const int64_t n = seg->n0 * seg->n1;
+    if (n == 0) return HRT_OK;
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    const int64_t blocks = std::min<int64_t>((n + HALO_THREADS - 1) / HALO_THREADS, 148 * 8);
+    plane_copy_kernel<<<(unsigned)blocks, HALO_THREADS, 0, st->s>>>(*seg);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
+// One chunk in the reference's own layout — a dense ghosted (ex+2, ey+2,
+// ez+2) float64 C-order object (jacobi.py:383) — updated u -> nxt exactly as
+// _update_body (jacobi.py:70-86): 7-point interior update, then the ghost
+// shell carried forward.  resid_slot (nullable) receives max|nxt-u|.
+int hrt_jacobi_chunk_update(void* stream, const double* u, double* nxt, int64_t ex, int64_t ey,
+                            int64_t ez, uint64_t* resid_slot) {
+    HRT_CHECK_ARG(stream && u && nxt && ex > 0 && ey > 0 && ez > 0, "bad chunk update arguments");
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    VolArgs a;
+    a.chunks = nullptr;
+    a.du = u;
+    a.dw = nxt;
+    a.parity = 0;
+    a.ex = ex;
+    a.ey = ey;
+    a.ez = ez;
+    a.sy = ez + 2;
+    a.sx = (ey + 2) * a.sy;
+    a.origin = 0;
+    a.rows = 16;
+    a.flat = ez == 1;
+    a.tiles_i = (ex + a.rows - 1) / a.rows;
+    a.tiles_j = a.flat ? (ey + VOL_TX * VOL_TY - 1) / (VOL_TX * VOL_TY) : (ey + VOL_TY - 1) / VOL_TY;
+    a.tiles_k = a.flat ? 1 : (ez + VOL_TX - 1) / VOL_TX;
+    a.resid = reinterpret_cast<unsigned long long*>(resid_slot);
+    const int64_t grid = a.tiles_i * a.tiles_j * a.tiles_k;
+    volume_update_kernel<<<(unsigned)grid, dim3(VOL_TX, VOL_TY), 0, st->s>>>(a);
+    HRT_CUDA(cudaGetLastError());
+    const int64_t n = (ex + 2) * (ey + 2) * (ez + 2);
+    ghost_shell_copy_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0,
+                              st->s>>>(u, nxt, ex, ey, ez, a.sx, a.sy);
     HRT_CUDA(cudaGetLastError());
     return HRT_OK;
 }
