@@ -385,11 +385,11 @@ __device__ __forceinline__ double div6_t(double s) {
     else return div6_fast(s);
 }
 
-template <bool GUARD, bool RESID>
+template <bool GUARD, bool RESID, int STAGES = T4_STAGES, bool FENCE = false>
 __global__ void __launch_bounds__(T4_THREADS)
 slab_update_tma4_kernel(SlabArgs a) {
-    __shared__ alignas(128) double ring[T4_STAGES][T4_ROW];
-    __shared__ alignas(8) uint64_t full[T4_STAGES], empty[T4_STAGES];
+    __shared__ alignas(128) double ring[STAGES][T4_ROW];
+    __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES];
     __shared__ double red[T4_CONSUMER_WARPS];
 
     const int64_t per_chunk = a.tiles_r * a.tiles_c;
@@ -411,7 +411,7 @@ slab_update_tma4_kernel(SlabArgs a) {
     const int64_t sx = a.sx;
 
     if (tid == 0) {
-        for (int s = 0; s < T4_STAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], T4_CONSUMER_WARPS);
         }
@@ -426,11 +426,11 @@ slab_update_tma4_kernel(SlabArgs a) {
             int s = 0;
             uint32_t ph = 0;
             for (int q = 0; q < nrows; ++q) {
-                if (q >= T4_STAGES) mbar_wait(&empty[s], ph ^ 1);
+                if (q >= STAGES) mbar_wait(&empty[s], ph ^ 1);
                 mbar_expect_tx(&full[s], bytes);
                 tma_row_load(&ring[s][0], src, bytes, &full[s]);
                 src += sx;
-                if (++s == T4_STAGES) {
+                if (++s == STAGES) {
                     s = 0;
                     ph ^= 1;
                 }
@@ -454,9 +454,10 @@ slab_update_tma4_kernel(SlabArgs a) {
         const double2 v23 = *reinterpret_cast<const double2*>(&ring[s][p + 2]);
         l = ring[s][p - 1];
         r = ring[s][p + 4];
+        if (FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == T4_STAGES) {
+        if (++s == STAGES) {
             s = 0;
             ph ^= 1;
         }
@@ -853,16 +854,23 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.zghost = HRT_BOUNDARY;
         const int64_t grid = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
         if (grid == 0) return HRT_OK;
-        if (p->variant == 2) {
+        if (p->variant >= 2) {
             const bool guard = !p->nonneg;
-            if (guard && resid)
-                slab_update_tma4_kernel<true, true><<<(unsigned)grid, T4_THREADS, 0, s>>>(a);
-            else if (guard)
-                slab_update_tma4_kernel<true, false><<<(unsigned)grid, T4_THREADS, 0, s>>>(a);
-            else if (resid)
-                slab_update_tma4_kernel<false, true><<<(unsigned)grid, T4_THREADS, 0, s>>>(a);
-            else
-                slab_update_tma4_kernel<false, false><<<(unsigned)grid, T4_THREADS, 0, s>>>(a);
+            const unsigned g = (unsigned)grid;
+#define T4_LAUNCH(ST, FE)                                                              \
+    do {                                                                               \
+        if (guard && resid) slab_update_tma4_kernel<true, true, ST, FE><<<g, T4_THREADS, 0, s>>>(a);  \
+        else if (guard) slab_update_tma4_kernel<true, false, ST, FE><<<g, T4_THREADS, 0, s>>>(a);     \
+        else if (resid) slab_update_tma4_kernel<false, true, ST, FE><<<g, T4_THREADS, 0, s>>>(a);     \
+        else slab_update_tma4_kernel<false, false, ST, FE><<<g, T4_THREADS, 0, s>>>(a);               \
+    } while (0)
+            switch (p->variant) {
+                case 2: T4_LAUNCH(8, false); break;
+                case 3: T4_LAUNCH(11, false); break;
+                case 4: T4_LAUNCH(8, true); break;
+                default: T4_LAUNCH(11, true); break;
+            }
+#undef T4_LAUNCH
         } else if (p->variant == 1) {
             slab_update_tma_kernel<<<(unsigned)grid, TMA_THREADS, 0, s>>>(a);
         } else {
@@ -989,7 +997,7 @@ int hrt_jacobi_plan_set_rows(void* plan, int64_t rows) {
 }
 
 int hrt_jacobi_plan_set_variant(void* plan, int variant) {
-    HRT_CHECK_ARG(plan && variant >= 0 && variant <= 2, "variant must be 0, 1 or 2");
+    HRT_CHECK_ARG(plan && variant >= 0 && variant <= 5, "variant must be 0..5");
     Plan* p = reinterpret_cast<Plan*>(plan);
     p->variant = variant;
     if (p->graph) {
