@@ -312,6 +312,7 @@ slab_update_tma_kernel(SlabArgs a) {
         v = *reinterpret_cast<const double2*>(&ring[s][p]);
         l = ring[s][p - 1];
         r = ring[s][p + 2];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs next TMA
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     };
@@ -370,7 +371,7 @@ constexpr int T4_CONSUMER_WARPS = 4;
 constexpr int T4_THREADS = 32 * (T4_CONSUMER_WARPS + 1);
 constexpr int T4_COLS = 128 * T4_CONSUMER_WARPS;  // 4 columns per consumer thread
 constexpr int T4_ROW = T4_COLS + 4;
-constexpr int T4_STAGES = 8;
+constexpr int T4_STAGES = 11;  // 11 x 4128 B ring: within the 48 KB static limit
 
 __device__ __forceinline__ double div6_fast(double s) {
     const double r = 0x1.5555555555555p-3;
@@ -385,7 +386,7 @@ __device__ __forceinline__ double div6_t(double s) {
     else return div6_fast(s);
 }
 
-template <bool GUARD, bool RESID, int STAGES = T4_STAGES, bool FENCE = false>
+template <bool GUARD, bool RESID, int STAGES = T4_STAGES>
 __global__ void __launch_bounds__(T4_THREADS)
 slab_update_tma4_kernel(SlabArgs a) {
     __shared__ alignas(128) double ring[STAGES][T4_ROW];
@@ -403,6 +404,7 @@ slab_update_tma4_kernel(SlabArgs a) {
     const int lane = tid & 31;
 
     const int64_t j0 = 1 + cb * T4_COLS;
+    if (j0 > a.ey) return;  // (uniform) no interior columns in this tile
     const int64_t last = min(j0 + T4_COLS - 1, a.ey);
     const uint32_t bytes = (uint32_t)((((last - j0 + 4) + 1) & ~int64_t(1)) * 8);
     const int64_t i0 = 1 + rb * a.rows;
@@ -454,7 +456,10 @@ slab_update_tma4_kernel(SlabArgs a) {
         const double2 v23 = *reinterpret_cast<const double2*>(&ring[s][p + 2]);
         l = ring[s][p - 1];
         r = ring[s][p + 4];
-        if (FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        // the next TMA write into this stage is an async-proxy access: order
+        // this warp's generic-proxy reads before it (without this fence the
+        // ring races; measured on B200)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         if (++s == STAGES) {
@@ -854,22 +859,14 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.zghost = HRT_BOUNDARY;
         const int64_t grid = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
         if (grid == 0) return HRT_OK;
-        if (p->variant >= 2) {
+        if (p->variant == 2) {
             const bool guard = !p->nonneg;
             const unsigned g = (unsigned)grid;
-#define T4_LAUNCH(ST, FE)                                                              \
-    do {                                                                               \
-        if (guard && resid) slab_update_tma4_kernel<true, true, ST, FE><<<g, T4_THREADS, 0, s>>>(a);  \
-        else if (guard) slab_update_tma4_kernel<true, false, ST, FE><<<g, T4_THREADS, 0, s>>>(a);     \
-        else if (resid) slab_update_tma4_kernel<false, true, ST, FE><<<g, T4_THREADS, 0, s>>>(a);     \
-        else slab_update_tma4_kernel<false, false, ST, FE><<<g, T4_THREADS, 0, s>>>(a);               \
-    } while (0)
-            switch (p->variant) {
-                case 2: T4_LAUNCH(8, false); break;
-                case 3: T4_LAUNCH(11, false); break;
-                case 4: T4_LAUNCH(8, true); break;
-                default: T4_LAUNCH(11, true); break;
-            }
+#define T4_LAUNCH(G, R) slab_update_tma4_kernel<G, R><<<g, T4_THREADS, 0, s>>>(a)
+            if (guard && resid) T4_LAUNCH(true, true);
+            else if (guard) T4_LAUNCH(true, false);
+            else if (resid) T4_LAUNCH(false, true);
+            else T4_LAUNCH(false, false);
 #undef T4_LAUNCH
         } else if (p->variant == 1) {
             slab_update_tma_kernel<<<(unsigned)grid, TMA_THREADS, 0, s>>>(a);
@@ -997,7 +994,7 @@ int hrt_jacobi_plan_set_rows(void* plan, int64_t rows) {
 }
 
 int hrt_jacobi_plan_set_variant(void* plan, int variant) {
-    HRT_CHECK_ARG(plan && variant >= 0 && variant <= 5, "variant must be 0..5");
+    HRT_CHECK_ARG(plan && variant >= 0 && variant <= 2, "variant must be 0, 1 or 2");
     Plan* p = reinterpret_cast<Plan*>(plan);
     p->variant = variant;
     if (p->graph) {

@@ -151,3 +151,29 @@ def test_arbitrary_initial_data_guarded_division(hrt, oracle, dom, grid):
         s.close()
         ref = oracle.jacobi_reference(dom, steps, initial=init)
         assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
+
+
+def test_tma_ring_race_regression(hrt):
+    """16384^2, 8x8 chunks, 10 steps, repeated: without the async-proxy fence
+    between the consumers' shared-memory reads and the producer's next TMA
+    write into the same ring stage, 4 of 5 runs corrupted a cell (found on
+    B200 via the residual history).  Field and residual must be identical to
+    the LDG kernel on one chunk every time."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    dom = (16384, 16384, 1)
+
+    def run(grid, variant):
+        s = JacobiSolver(ChunkGrid(dom, grid=grid), variant=variant)
+        s.upload()
+        s.run(10, residual=True, graph=False)
+        out = s.download(), s.residual_history()
+        s.close()
+        return out
+
+    ref_f, ref_r = run((1, 1, 1), 0)
+    for variant in (2, 1):
+        for _ in range(4 if variant == 2 else 2):
+            f, r = run((8, 8, 1), variant)
+            assert np.array_equal(r, ref_r), (variant, np.nonzero(r != ref_r)[0][:5])
+            assert np.array_equal(f, ref_f), variant
