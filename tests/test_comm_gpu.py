@@ -1,0 +1,125 @@
+"""Message path and task-protocol Jacobi on B200s: mp_send (direct device
+copies vs host staging), ping-pong byte identity (AC-08 analogue), put/get,
+and run_jacobi3d(engine="tasks") — the reference's own per-chunk protocol
+(pack -> mp_send -> unpack -> update tasks) — bitwise against the goldens."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import kwargs_of, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    from paper_2303_02543_b200 import _native as N
+
+    N.require_gpu(0)
+
+
+@pytest.mark.parametrize("path", ["direct", "staging"])
+def test_pingpong_byte_identity(path):
+    from paper_2303_02543_b200.pingpong import run_pingpong
+
+    sizes = [8, 448, 449, 4096, 1 << 20, 3 << 20]
+    rep = run_pingpong(sizes, iterations=3, path=path, verify=True)
+    assert [r["size_bytes"] for r in rep.rows] == sizes
+    for r in rep.rows:
+        assert r["mean_latency_s"] > 0
+        assert r["bandwidth_Bps"] == pytest.approx(r["size_bytes"] / r["mean_latency_s"])
+    if path == "direct":
+        assert rep.meta["staging_copies"] == 0  # AC-08: no host staging on the device path
+        assert rep.meta["device_copies"] == 2 * 3 * len(sizes)
+    else:
+        assert rep.meta["staging_copies"] > 0
+
+
+def test_pingpong_payload_sequence_is_the_references():
+    """The payload bytes are the reference's (default_rng(99), pingpong.py:107,115)."""
+    g = load_golden("pingpong.json")
+    rng = np.random.default_rng(g["seed"])
+    for p in g["payloads"][:12]:
+        b = rng.integers(0, 256, size=p["size"], dtype=np.uint8)
+        assert hashlib.sha256(b.tobytes()).hexdigest() == p["sha256"]
+
+
+def test_mp_send_bytes_ordering_and_objects():
+    from paper_2303_02543_b200.comm import MobileRef, drive, exchange_all, shutdown_all
+    from paper_2303_02543_b200.devices import DeviceType
+    from paper_2303_02543_b200.native_kernels import Fill
+    from paper_2303_02543_b200.worlds import WorldConfig, make_loopback_world
+
+    for aware in (True, False):
+        comms = make_loopback_world(WorldConfig(ranks=2, device_aware=aware))
+        got = []
+        hid = [c.register_handler(lambda m, a, ctx: got.append(a)) for c in comms][0]
+        for c in comms:
+            c.create_mobile_object(b"m")
+        exchange_all(comms)
+        for k in range(20):
+            comms[0].mp_send(MobileRef(1, 0), hid, bytes([k]) * (k * 40))
+        drive(comms, until=lambda: len(got) == 20)
+        assert [len(g) for g in got] == [k * 40 for k in range(20)]
+        assert all(g == bytes([k]) * (k * 40) for k, g in enumerate(got))
+        # object sends are ordered after the writer task (GPU-side edge)
+        rt0 = comms[0].runtime
+        rt0.register_kernel("fill9", gpu_sim=Fill(9))
+        obj = rt0.create_object((5000,), dtype=np.uint8)
+        t = rt0.task().device(DeviceType.GPU_SIM)
+        t.arg(obj).write()
+        t.submit("fill9")
+        got.clear()
+        comms[0].mp_send(MobileRef(1, 0), hid, obj)
+        drive(comms, until=lambda: len(got) == 1)
+        w = got[0]
+        drive(comms, until=lambda: w.written or w.host_state.value == "valid")
+        assert np.array_equal(comms[1].runtime.peek(w).reshape(-1), np.full(5000, 9, np.uint8))
+        shutdown_all(comms)
+
+
+def test_put_get_roundtrip():
+    from paper_2303_02543_b200.comm import GlobalObjectId, drive, exchange_all, shutdown_all
+    from paper_2303_02543_b200.worlds import WorldConfig, make_loopback_world
+
+    comms = make_loopback_world(WorldConfig(ranks=2, device_aware=True))
+    for c in comms:
+        c.create_mobile_object(b"m")
+    exchange_all(comms)
+    done = []
+    hid = [c.register_handler(lambda m, a, ctx: done.append(a)) for c in comms][0]
+    rt1 = comms[1].runtime
+    target = rt1.create_object((256,), dtype=np.uint8)
+    v = rt1.request_data(target, write=True).get()
+    v[:] = 3
+    rt1.release(target)
+    comms[0].hetero_put(GlobalObjectId(1, target.object_id), bytes(range(256)), hid)
+    drive(comms, until=lambda: len(done) == 1)
+    rt1.synchronize()
+    assert np.array_equal(rt1.peek(target), np.arange(256, dtype=np.uint8))
+    dest = comms[0].runtime.create_object((256,), dtype=np.uint8)
+    comms[0].hetero_get(GlobalObjectId(1, target.object_id), dest, hid)
+    drive(comms, until=lambda: len(done) == 2)
+    comms[0].runtime.synchronize()
+    assert np.array_equal(comms[0].runtime.peek(dest), np.arange(256, dtype=np.uint8))
+    shutdown_all(comms)
+
+
+TASK_LADDER = ["cube8_s3", "ac10_g222", "ac10_r2d2", "slab64_s10", "halo32_s20",
+               "halo32_s20_r2d2", "halo32_s20_direct", "halo16_cube_s12", "zero_steps",
+               "rect_slab", "thin_x", "zslab_3d"]
+
+
+@pytest.mark.parametrize("name", TASK_LADDER)
+def test_task_engine_ladder_bitwise(ladder, name):
+    from paper_2303_02543_b200.jacobi import run_jacobi3d
+
+    e = ladder[name]
+    rep, cs, arr = run_jacobi3d(tuple(e["domain"]), steps=e["steps"], engine="tasks",
+                                **kwargs_of(e))
+    assert hashlib.sha256(arr.tobytes()).hexdigest() == e["sha256"]
+    assert repr(cs) == e["checksum"]
+    if e["kwargs"].get("device_aware"):
+        assert sum(s["staging_copies"] for s in rep.meta["stats"]) == 0
