@@ -38,7 +38,7 @@ from typing import Callable, Optional, Union
 import numpy as np
 
 from .config import default_recv_cache_bytes
-from .devices import DeviceAllocation, DeviceType, HostRegion, TokenStatus
+from .devices import DeviceAllocation, DeviceType, ForeignAllocation, HostRegion, TokenStatus
 from .errors import DeadlockError, HrtError, NotOwner, ProtocolError, TransportClosed
 from .objects import AccessMode, CopyInfo, CopyState, HeteroObject
 from .runtime import AccessOp, Runtime
@@ -484,7 +484,10 @@ class Comm:
         waits = list(wait) + ([loc.token] if loc.token is not None else [])
         if loc.alloc is not None:
             self.stats.device_copies += 1
-            return reg.enqueue_transfer(loc.alloc, dst, size, wait=waits)
+            src = loc.alloc
+            if loc.registry is not reg:  # another rank's device memory (same process)
+                src = ForeignAllocation(loc.alloc, loc.registry.gpu_of(loc.alloc.device_id))
+            return reg.enqueue_transfer(src, dst, size, wait=waits)
         if loc.host is not None:
             self.stats.staging_copies += 1
             return reg.enqueue_transfer(np.ascontiguousarray(loc.host), dst, size, wait=waits)
@@ -709,9 +712,13 @@ def drive(comms: list[Comm], until: Callable[[], bool], timeout: float = 120.0) 
                 break
         if work:
             continue
+        state = "; ".join(
+            f"rank {c.rank}: {c.runtime.debug_state()} outgoing="
+            f"{[(d, [e.label + ('+' if e.ready else '-') for e in q][:4]) for d, q in c._outgoing.items() if q]}"
+            f" handlers={sum(len(q) for q in c._hq.values())}" for c in comms)
         if time.monotonic() > deadline:
-            raise DeadlockError("drive timed out")
-        raise DeadlockError("no progress possible across ranks")
+            raise DeadlockError(f"drive timed out ({state})")
+        raise DeadlockError(f"no progress possible across ranks ({state})")
 
 
 def exchange_all(comms: list[Comm]) -> list[list[MobileRef]]:

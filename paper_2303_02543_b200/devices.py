@@ -456,7 +456,16 @@ class _Device:
         return self.descriptor.device_id
 
 
-Location = Union[DeviceAllocation, HostRegion, np.ndarray]
+@dataclass(frozen=True)
+class ForeignAllocation:
+    """A device allocation owned by another rank's registry in this process
+    (the direct message path reads it as a peer-copy source)."""
+
+    alloc: DeviceAllocation
+    gpu: int
+
+
+Location = Union[DeviceAllocation, HostRegion, np.ndarray, ForeignAllocation]
 
 
 class DeviceRegion:
@@ -624,7 +633,11 @@ class DeviceRegistry:
     # -- async operations ---------------------------------------------------
 
     def _resolve(self, loc: Location, nbytes: int) -> tuple[int, Optional[int]]:
-        """(byte address, device_id or None for host) of a location."""
+        """(byte address, device_id or None for host) of a location.  A
+        :class:`ForeignAllocation` (another rank's registry, same process)
+        resolves to its physical GPU."""
+        if isinstance(loc, ForeignAllocation):
+            return loc.alloc.ptr, ("gpu", loc.gpu)
         if isinstance(loc, DeviceAllocation):
             self.device(loc.device_id)
             if nbytes > loc.size:
@@ -660,6 +673,8 @@ class DeviceRegistry:
             if size:
                 ctypes.memmove(dp, sp, size)
             return CompletionToken.completed(TokenKind.TRANSFER)
+        if isinstance(dd, tuple):
+            raise InvalidLocation("a foreign allocation can only be a transfer source")
         if dd is not None:
             dev = self.device(dd)
             stream = dev.h2d
@@ -670,8 +685,9 @@ class DeviceRegistry:
             stream.wait(t)
         t0 = self.clock.now
         if size:
-            if sd is not None and dd is not None and self.gpu_of(sd) != self.gpu_of(dd):
-                g_s, g_d = self.gpu_of(sd), self.gpu_of(dd)
+            g_s = sd[1] if isinstance(sd, tuple) else (self.gpu_of(sd) if sd is not None else None)
+            g_d = self.gpu_of(dd) if dd is not None else None
+            if g_s is not None and g_d is not None and g_s != g_d:
                 self.enable_peer(g_d, g_s)
                 N.call("hrt_copy_peer_async", stream.h, ctypes.c_void_p(dp), g_d,
                        ctypes.c_void_p(sp), g_s, ctypes.c_uint64(size))
