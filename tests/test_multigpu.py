@@ -1,0 +1,57 @@
+"""Multi-GPU paths (skipped on single-GPU boxes): one process driving several
+B200s with chunk faces read over NVLink (peer access), and one process per
+GPU under torchrun with faces exchanged by NCCL send/recv inside
+libhrt_b200 — both bitwise against the oracle."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def ngpu():
+    from paper_2303_02543_b200 import _native as N
+
+    return N.gpu_count()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_two():
+    if ngpu() < 2:
+        pytest.skip("needs >= 2 GPUs")
+
+
+@pytest.mark.parametrize("dom,grid,steps", [((1024, 1024, 1), (4, 4, 1), 50),
+                                            ((300, 700, 1), (3, 7, 1), 64),
+                                            ((40, 36, 30), (2, 3, 2), 17)])
+def test_single_process_peer_faces(oracle, dom, grid, steps):
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    n = min(ngpu(), 4)
+    s = JacobiSolver(ChunkGrid(dom, ranks=1, devices_per_rank=n, grid=grid),
+                     gpus=list(range(n)))
+    assert len(s.used_gpus) == n
+    s.upload()
+    s.run(steps)
+    got, res = s.download(), s.residual_history()
+    cs = s.checksum()
+    s.close()
+    ref, rres = oracle.jacobi_c(dom, steps, residual=True)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(res, rres)
+    assert cs == oracle.checksum(ref)
+
+
+def test_torchrun_nccl_faces():
+    n = min(ngpu(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29533",
+           os.path.join(ROOT, "tools", "dist_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert "DIST_CHECK PASS" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]

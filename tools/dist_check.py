@@ -1,0 +1,49 @@
+"""Multi-process parity check (run under torchrun, one process per GPU):
+DistributedJacobi with NCCL faces vs the C oracle, field and residual.
+
+torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2303_02543_b200.distributed import DistributedJacobi, init_process  # noqa: E402
+from paper_2303_02543_b200.jacobi import ChunkGrid  # noqa: E402
+
+rank, world, local = init_process("nccl")
+# y faces (strided: packed), x faces (contiguous rows: direct), 3D z faces
+cases = [((1024, 1024, 1), (4, 4, 1), 60), ((600, 520, 1), (3, 2 * world, 1), 77),
+         ((512, 300, 1), (2 * world, 1, 1), 45), ((48, 40, 32), (2, 2, world), 21),
+         ((4096, 4096, 1), (8, 8, 1), 130)]
+ok_all = True
+for dom, grid, steps in cases:
+    cg = ChunkGrid(dom, ranks=world, grid=grid)
+    s = DistributedJacobi(cg, rank, world, local)
+    s.upload()
+    s.run(steps, residual=True)
+    box = s.download()
+    res = s.global_residual_history()
+    lo = s.box_lo
+    s.close()
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, box))
+    if rank == 0:
+        from oracle import oracle as O
+
+        full = np.empty(dom)
+        for (l0, b) in parts:
+            full[l0[0]:l0[0] + b.shape[0], l0[1]:l0[1] + b.shape[1], l0[2]:l0[2] + b.shape[2]] = b
+        ref, rres = O.jacobi_c(dom, steps, residual=True)
+        ok = np.array_equal(full, ref) and np.array_equal(res, rres)
+        ok_all &= ok
+        print(f"dist_check world={world} dom={dom} grid={grid} steps={steps}: "
+              f"field {'OK' if np.array_equal(full, ref) else 'DIFF'} "
+              f"resid {'OK' if np.array_equal(res, rres) else 'DIFF'}", flush=True)
+dist.barrier()
+if rank == 0:
+    print("DIST_CHECK", "PASS" if ok_all else "FAIL", flush=True)
+dist.destroy_process_group()
