@@ -143,6 +143,12 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t *layout, int nchunk
 int hrt_jacobi_plan_set_remote(void *plan, void *comm, const hrt_remote_seg_t *remote,
                                int nremote, const hrt_halo_seg_t *post, int npost);
 int hrt_jacobi_plan_set_rows(void *plan, int64_t rows);
+/* chunk origins (3 int64 per chunk, plan order) inside the process's
+ * contiguous field, then one-launch scatter (upload, jacobi.py:382-395) /
+ * gather (jacobi.py:425-435) between the field and buffer `parity` */
+int hrt_jacobi_plan_set_offsets(void *plan, const int64_t *offs3);
+int hrt_jacobi_plan_field_copy(void *plan, void *stream, double *field, int64_t FY, int64_t FZ,
+                               int parity, int to_chunks);
 /* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,
  * 2 = TMA ring with four columns per thread (default) */
 int hrt_jacobi_plan_set_variant(void *plan, int variant);

@@ -86,6 +86,9 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_remote": (c_int, [c_void_p, c_void_p, P(RemoteSeg), c_int, P(HaloSeg),
                                            c_int]),
     "hrt_jacobi_plan_set_rows": (c_int, [c_void_p, c_i64]),
+    "hrt_jacobi_plan_set_offsets": (c_int, [c_void_p, P(c_i64)]),
+    "hrt_jacobi_plan_field_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_int,
+                                           c_int]),
     "hrt_jacobi_plan_set_variant": (c_int, [c_void_p, c_int]),
     "hrt_jacobi_plan_set_nonneg": (c_int, [c_void_p, c_int]),
     "hrt_jacobi_plan_step": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),

@@ -386,12 +386,12 @@ __device__ __forceinline__ double div6_t(double s) {
     else return div6_fast(s);
 }
 
-template <bool GUARD, bool RESID, int STAGES = T4_STAGES>
-__global__ void __launch_bounds__(T4_THREADS)
+template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, int STAGES = T4_STAGES>
+__global__ void __launch_bounds__(32 * (CW + 1))
 slab_update_tma4_kernel(SlabArgs a) {
-    __shared__ alignas(128) double ring[STAGES][T4_ROW];
+    __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES];
-    __shared__ double red[T4_CONSUMER_WARPS];
+    __shared__ double red[CW];
 
     const int64_t per_chunk = a.tiles_r * a.tiles_c;
     const int64_t t = blockIdx.x;
@@ -403,9 +403,9 @@ slab_update_tma4_kernel(SlabArgs a) {
     const int warp = tid >> 5;
     const int lane = tid & 31;
 
-    const int64_t j0 = 1 + cb * T4_COLS;
+    const int64_t j0 = 1 + cb * (128 * CW);
     if (j0 > a.ey) return;  // (uniform) no interior columns in this tile
-    const int64_t last = min(j0 + T4_COLS - 1, a.ey);
+    const int64_t last = min(j0 + (128 * CW) - 1, a.ey);
     const uint32_t bytes = (uint32_t)((((last - j0 + 4) + 1) & ~int64_t(1)) * 8);
     const int64_t i0 = 1 + rb * a.rows;
     const int64_t i1 = min(a.ex, i0 + a.rows - 1);
@@ -415,14 +415,14 @@ slab_update_tma4_kernel(SlabArgs a) {
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], T4_CONSUMER_WARPS);
+            mbar_init(&empty[s], CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp == T4_CONSUMER_WARPS) {
+    if (warp == CW) {
         if (lane == 0) {
             const double* src = a.chunks[c].b[a.parity] + a.origin + (i0 - 1) * sx + (j0 - 2);
             int s = 0;
@@ -511,11 +511,11 @@ slab_update_tma4_kernel(SlabArgs a) {
     if (RESID) {
         rmax = warp_max(rmax);
         if (lane == 0) red[warp] = rmax;
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * T4_CONSUMER_WARPS));
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
         if (tid == 0) {
             double m = red[0];
 #pragma unroll
-            for (int k = 1; k < T4_CONSUMER_WARPS; ++k) m = fmax(m, red[k]);
+            for (int k = 1; k < CW; ++k) m = fmax(m, red[k]);
             resid_max(a.resid, m);
         }
     }
@@ -610,6 +610,37 @@ halo_copy_kernel(const hrt_halo_seg_t* __restrict__ segs, int parity, int64_t bl
         const int64_t o = e / g.n1, i = e - o * g.n1;
         dst[o * g.ds0 + i * g.ds1] = src[o * g.ss0 + i * g.ss1];
     }
+}
+
+// contiguous (FX, FY, FZ) field <-> every chunk interior of a plan, one CTA
+// per interior row: upload scatter / gather (jacobi.py:425-435) in one launch
+__global__ void __launch_bounds__(256)
+field_copy_kernel(const ChunkBufs* __restrict__ chunks, const int64_t* __restrict__ offs, int parity,
+                  int ndim, int64_t ex, int64_t ey, int64_t ez, int64_t sx, int64_t sy,
+                  int64_t origin, double* __restrict__ field, int64_t FY, int64_t FZ,
+                  int to_chunks) {
+    const int64_t rows = ndim == 2 ? ex : ex * ey;
+    const int64_t c = blockIdx.x / rows;
+    const int64_t r = blockIdx.x - c * rows;
+    const int64_t ox = offs[3 * c], oy = offs[3 * c + 1], oz = offs[3 * c + 2];
+    double* base = chunks[c].b[parity] + origin;
+    double* crow;
+    double* frow;
+    int64_t n;
+    if (ndim == 2) {
+        crow = base + (r + 1) * sx + 1;
+        frow = field + (ox + r) * FY + oy;
+        n = ey;
+    } else {
+        const int64_t i = r / ey, j = r - i * ey;
+        crow = base + (i + 1) * sx + (j + 1) * sy + 1;
+        frow = field + ((ox + i) * FY + (oy + j)) * FZ + oz;
+        n = ez;
+    }
+    if (to_chunks)
+        for (int64_t k = threadIdx.x; k < n; k += 256) crow[k] = frow[k];
+    else
+        for (int64_t k = threadIdx.x; k < n; k += 256) frow[k] = crow[k];
 }
 
 // one plane copy passed by value (standalone pack/unpack tasks)
@@ -812,6 +843,7 @@ struct Plan {
     int nsegs = 0;
     int64_t seg_blocks = 1;
     hrt_halo_seg_t* d_post = nullptr;
+    int64_t* d_offs = nullptr;  // chunk origins in the field (field_copy)
     int npost = 0;
     int64_t post_blocks = 1;
     std::vector<hrt_remote_seg_t> remote;
@@ -853,7 +885,10 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.origin = L.origin;
         a.rows = p->rows;
         a.tiles_r = (a.ex + a.rows - 1) / a.rows;
-        const int cols = p->variant == 2 ? T4_COLS : SLAB_COLS;
+        // chunks at most 256 wide (e.g. cfg5's 256^2 blocks) use 2 consumer
+        // warps per CTA so no thread is idle
+        const bool narrow = p->variant == 2 && a.ey <= 256;
+        const int cols = p->variant == 2 ? (narrow ? 256 : T4_COLS) : SLAB_COLS;
         a.tiles_c = (a.ey + cols - 1) / cols;
         a.resid = resid;
         a.zghost = HRT_BOUNDARY;
@@ -862,11 +897,18 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         if (p->variant == 2) {
             const bool guard = !p->nonneg;
             const unsigned g = (unsigned)grid;
-#define T4_LAUNCH(G, R) slab_update_tma4_kernel<G, R><<<g, T4_THREADS, 0, s>>>(a)
-            if (guard && resid) T4_LAUNCH(true, true);
-            else if (guard) T4_LAUNCH(true, false);
-            else if (resid) T4_LAUNCH(false, true);
-            else T4_LAUNCH(false, false);
+#define T4_LAUNCH(G, R, CW) slab_update_tma4_kernel<G, R, CW><<<g, 32 * (CW + 1), 0, s>>>(a)
+            if (narrow) {
+                if (guard && resid) T4_LAUNCH(true, true, 2);
+                else if (guard) T4_LAUNCH(true, false, 2);
+                else if (resid) T4_LAUNCH(false, true, 2);
+                else T4_LAUNCH(false, false, 2);
+            } else {
+                if (guard && resid) T4_LAUNCH(true, true, 4);
+                else if (guard) T4_LAUNCH(true, false, 4);
+                else if (resid) T4_LAUNCH(false, true, 4);
+                else T4_LAUNCH(false, false, 4);
+            }
 #undef T4_LAUNCH
         } else if (p->variant == 1) {
             slab_update_tma_kernel<<<(unsigned)grid, TMA_THREADS, 0, s>>>(a);
@@ -979,6 +1021,40 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     // rows per CTA: enough CTAs to fill the GPU several times over
     p->rows = layout->ndim == 2 ? 64 : 16;
     *plan = p;
+    return HRT_OK;
+}
+
+// chunk origins (3 int64 per chunk, plan order) inside the process's field
+int hrt_jacobi_plan_set_offsets(void* plan, const int64_t* offs3) {
+    HRT_CHECK_ARG(plan && offs3, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    cudaFree(p->d_offs);
+    p->d_offs = nullptr;
+    if (p->nchunks == 0) return HRT_OK;
+    HRT_CUDA(cudaMalloc(&p->d_offs, sizeof(int64_t) * 3 * p->nchunks));
+    HRT_CUDA(cudaMemcpy(p->d_offs, offs3, sizeof(int64_t) * 3 * p->nchunks, cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
+// field (FX x FY x FZ, contiguous float64, any GPU reachable from this one)
+// -> buffer `parity` of every chunk (to_chunks=1), or back (0)
+int hrt_jacobi_plan_field_copy(void* plan, void* stream, double* field, int64_t FY, int64_t FZ,
+                               int parity, int to_chunks) {
+    HRT_CHECK_ARG(plan && stream && field, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG(p->d_offs || p->nchunks == 0, "set the chunk offsets first");
+    if (p->nchunks == 0) return HRT_OK;
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    const hrt_chunk_layout_t& L = p->L;
+    const int64_t rows = L.ndim == 2 ? L.ext[0] : L.ext[0] * L.ext[1];
+    const int64_t grid = rows * p->nchunks;
+    field_copy_kernel<<<(unsigned)grid, 256, 0, as_stream(stream)->s>>>(
+        p->d_chunks, p->d_offs, parity & 1, L.ndim, L.ext[0], L.ext[1], L.ext[2], L.stride[0],
+        L.stride[1], L.origin, field, FY, FZ, to_chunks);
+    HRT_CUDA(cudaGetLastError());
     return HRT_OK;
 }
 
@@ -1176,6 +1252,7 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_chunks);
     cudaFree(p->d_segs);
     cudaFree(p->d_post);
+    cudaFree(p->d_offs);
     delete p;
     return HRT_OK;
 }

@@ -293,8 +293,8 @@ class JacobiSolver:
         staging = 0
         for (c, f, nb) in remote_msgs:
             _, n0, n1, s0, s1 = face_plane(L, 0, f, ghost=True)
-            if not _contiguous(n0, n1, s0, s1):
-                staging += -(-n0 * n1 * F64 // 256) * 256
+            staging += n0 * n1 * F64
+        staging = -(-staging // 256) * 256 + 256 * 4 * max(1, grid.ranks)
         self.pools: dict[int, DevicePool] = {}
         self.bufs: dict[int, tuple[int, int]] = {}
         for g in self.used_gpus:
@@ -322,30 +322,41 @@ class JacobiSolver:
                     if placement[nb] != g:
                         self.peer_deps[g].add(placement[nb])
                     pre[g].append(self._face_seg(lin, f, nb))
+        # Cross-process faces, aggregated per (peer, direction): the halo
+        # launch packs every face bound for a peer into one staging buffer
+        # (canonical order), one ncclSend/ncclRecv pair per peer moves it,
+        # and unpack copies scatter the received buffer into ghost planes.
+        # One message per neighbour rank instead of one per face keeps the
+        # exchange latency-bound at one NCCL round per step.
         remote_ops, post = [], []
         g0 = self.used_gpus[0]
+        groups: dict[tuple[int, int], list] = {}
         for (c, f, nb) in remote_msgs:
-            if self.rank_of[nb] == rank:  # I send nb's boundary plane
-                pairs = [face_plane(L, self.bufs[nb][p], opposite(f), ghost=False) for p in (0, 1)]
-                _, n0, n1, s0, s1 = pairs[0]
-                if _contiguous(n0, n1, s0, s1):
-                    addrs = [pairs[0][0], pairs[1][0]]
-                else:
-                    st = self.pools[g0].alloc(n0 * n1 * F64)[2]
-                    pre[g0].append(_seg([pairs[0][0], pairs[1][0]], [st, st], n0, n1, s0, s1,
-                                        n1, 1))
-                    addrs = [st, st]
-                remote_ops.append(self._remote(addrs, n0 * n1, self.rank_of[c], 0))
-            else:  # I receive into c's ghost plane
-                pairs = [face_plane(L, self.bufs[c][p], f, ghost=True) for p in (0, 1)]
-                _, n0, n1, s0, s1 = pairs[0]
-                if _contiguous(n0, n1, s0, s1):
-                    addrs = [pairs[0][0], pairs[1][0]]
-                else:
-                    st = self.pools[g0].alloc(n0 * n1 * F64)[2]
-                    post.append(_seg([st, st], [pairs[0][0], pairs[1][0]], n0, n1, n1, 1, s0, s1))
-                    addrs = [st, st]
-                remote_ops.append(self._remote(addrs, n0 * n1, self.rank_of[nb], 1))
+            if self.rank_of[nb] == rank:
+                groups.setdefault((self.rank_of[c], 0), []).append((c, f, nb))
+            else:
+                groups.setdefault((self.rank_of[nb], 1), []).append((c, f, nb))
+        for (peer, kind) in sorted(groups):
+            faces = groups[(peer, kind)]
+            total = 0
+            for (c, f, nb) in faces:
+                _, n0, n1, _, _ = face_plane(L, 0, f, ghost=True)
+                total += n0 * n1
+            st = self.pools[g0].alloc(total * F64)[2]
+            off = 0
+            for (c, f, nb) in faces:
+                if kind == 0:  # pack nb's boundary plane opposite(f)
+                    pl = [face_plane(L, self.bufs[nb][p], opposite(f), ghost=False) for p in (0, 1)]
+                    _, n0, n1, s0, s1 = pl[0]
+                    dst = st + off * F64
+                    pre[g0].append(_seg([pl[0][0], pl[1][0]], [dst, dst], n0, n1, s0, s1, n1, 1))
+                else:  # unpack into c's ghost plane f
+                    pl = [face_plane(L, self.bufs[c][p], f, ghost=True) for p in (0, 1)]
+                    _, n0, n1, s0, s1 = pl[0]
+                    src = st + off * F64
+                    post.append(_seg([src, src], [pl[0][0], pl[1][0]], n0, n1, n1, 1, s0, s1))
+                off += n0 * n1
+            remote_ops.append(self._remote([st, st], total, peer, kind))
         if remote_ops and comm is None:
             raise HrtError("faces cross ranks: an NCCL communicator is required")
         for g in self.used_gpus:
@@ -379,6 +390,7 @@ class JacobiSolver:
         hi = [max(grid.chunks[lin].offsets[a] + grid.ext[a] for lin in owned) for a in range(3)]
         self.box_lo = tuple(lo)
         self.box = tuple(h - l for l, h in zip(lo, hi))
+        self._set_offsets()
         self._init_ghosts()
 
     def _set_nonneg(self, flag: bool) -> None:
@@ -436,31 +448,23 @@ class JacobiSolver:
             self._field_ptr = self._field_pool.alloc(nbytes)[2]
         return self._field_ptr
 
-    def _chunk_copies(self, to_chunks: bool, parity: int, field_ptr: int, stream_of) -> None:
-        """Strided copies between the contiguous field and chunk interiors."""
-        L = self.layout
-        X, Y, Z = self.box
-        width, pitch, rows = interior_row_bytes(L)
-        for lin in self.owned:
-            ch = self.grid.chunks[lin]
-            st = stream_of(self.placement[lin])
-            ox, oy, oz = (o - l for o, l in zip(ch.offsets, self.box_lo))
-            base = self.bufs[lin][parity]
-            if L.ndim == 2:
-                planes = [(_addr(L, base, 1, 1, 0), field_ptr + F64 * (ox * Y + oy))]
-                fpitch = Y * F64
-            else:
-                planes = [(_addr(L, base, 1 + i, 1, 1),
-                           field_ptr + F64 * (((ox + i) * Y + oy) * Z + oz))
-                          for i in range(L.ext[0])]
-                fpitch = Z * F64
-            for caddr, faddr in planes:
-                if to_chunks:
-                    N.call("hrt_copy2d_async", st.h, ctypes.c_void_p(caddr), pitch,
-                           ctypes.c_void_p(faddr), fpitch, width, rows)
-                else:
-                    N.call("hrt_copy2d_async", st.h, ctypes.c_void_p(faddr), fpitch,
-                           ctypes.c_void_p(caddr), pitch, width, rows)
+    def _chunk_copies(self, to_chunks: bool, parity: int, field_ptr: int, stream_of=None) -> None:
+        """Field <-> chunk interiors: one field_copy launch per GPU, on that
+        GPU's solver stream (the field lives on the first GPU; the others
+        reach it over NVLink).  Callers order the GPUs (_fan_out/_fan_in)."""
+        _, Y, Z = self.box
+        for g in self.used_gpus:
+            N.call("hrt_jacobi_plan_field_copy", self.plans[g], self.streams[g].h,
+                   ctypes.c_void_p(field_ptr), Y, Z, parity, 1 if to_chunks else 0)
+
+    def _set_offsets(self) -> None:
+        for g in self.used_gpus:
+            mine = [lin for lin in self.owned if self.placement[lin] == g]
+            offs = [o - lo for lin in mine
+                    for o, lo in zip(self.grid.chunks[lin].offsets, self.box_lo)]
+            N.call("hrt_jacobi_plan_set_offsets", self.plans[g], _arr(ctypes.c_int64, offs))
+            if g != self.used_gpus[0]:
+                N.call("hrt_enable_peer_access", g, self.used_gpus[0])
 
     # -- data in/out ----------------------------------------------------------
 
@@ -515,8 +519,8 @@ class JacobiSolver:
         (jacobi.py:425-435); returns its device address."""
         f = self._field()
         g0 = self.used_gpus[0]
+        self._chunk_copies(False, self.steps_done % 2, f)
         self._fan_in(g0)
-        self._chunk_copies(False, self.steps_done % 2, f, lambda g: self.streams[g0])
         return f
 
     def download(self, out: Optional[np.ndarray] = None, host: Optional[PinnedBuffer] = None):
