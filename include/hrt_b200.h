@@ -132,6 +132,16 @@ typedef struct hrt_remote_seg {
     int32_t kind;
 } hrt_remote_seg_t;
 
+/* Fused halo push, per chunk: where the update kernel stores the chunk's
+ * new boundary plane of face f (FACES order north, south, west, east) when
+ * it writes buffer parity p — the neighbour's ghost plane (same GPU, or a
+ * peer GPU over NVLink), or a packed NCCL staging slot; null for a domain
+ * face.  stride[f] = element step along that plane. */
+typedef struct hrt_push {
+    uint64_t ptr[4][2];
+    int64_t stride[4];
+} hrt_push_t;
+
 /* Step engine for all chunks of one GPU (replaces the per-chunk task chain
  * of _RankDriver.start_step/_try_finish_step jacobi.py:219-273).
  * bufs: 2*nchunks device addresses (buffer 0, buffer 1 per chunk).
@@ -147,6 +157,11 @@ int hrt_jacobi_plan_set_rows(void *plan, int64_t rows);
  * contiguous field, then one-launch scatter (upload, jacobi.py:382-395) /
  * gather (jacobi.py:425-435) between the field and buffer `parity` */
 int hrt_jacobi_plan_set_offsets(void *plan, const int64_t *offs3);
+/* enable (table != NULL) / disable the fused halo push for slab variant 2:
+ * a step is then one update launch (+ the NCCL exchange of pushed staging);
+ * the full halo pass runs only when ghosts are stale (after an upload) */
+int hrt_jacobi_plan_set_push(void *plan, const hrt_push_t *table);
+int hrt_jacobi_plan_invalidate_ghosts(void *plan);
 int hrt_jacobi_plan_field_copy(void *plan, void *stream, double *field, int64_t FY, int64_t FZ,
                                int parity, int to_chunks);
 /* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,

@@ -34,6 +34,12 @@ class HaloSeg(ctypes.Structure):
                 ("ss0", c_i64), ("ss1", c_i64), ("ds0", c_i64), ("ds1", c_i64)]
 
 
+class Push(ctypes.Structure):
+    """hrt_push_t"""
+
+    _fields_ = [("ptr", (c_u64 * 2) * 4), ("stride", c_i64 * 4)]
+
+
 class RemoteSeg(ctypes.Structure):
     """hrt_remote_seg_t"""
 
@@ -87,6 +93,8 @@ SIGNATURES = {
                                            c_int]),
     "hrt_jacobi_plan_set_rows": (c_int, [c_void_p, c_i64]),
     "hrt_jacobi_plan_set_offsets": (c_int, [c_void_p, P(c_i64)]),
+    "hrt_jacobi_plan_set_push": (c_int, [c_void_p, c_void_p]),
+    "hrt_jacobi_plan_invalidate_ghosts": (c_int, [c_void_p]),
     "hrt_jacobi_plan_field_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_int,
                                            c_int]),
     "hrt_jacobi_plan_set_variant": (c_int, [c_void_p, c_int]),

@@ -86,8 +86,17 @@ constexpr int SLAB_THREADS = 128;
 constexpr int SLAB_COLS = 2 * SLAB_THREADS;
 constexpr int SLAB_U = 4;
 
+// per chunk: where its boundary planes go for each buffer parity (fused
+// halo push), face order FACES 0..3; stride = element step along the plane
+struct ChunkPush {
+    double* ptr[4][2];
+    int64_t stride[4];
+};
+static_assert(sizeof(ChunkPush) == sizeof(hrt_push_t), "ChunkPush layout");
+
 struct SlabArgs {
     const ChunkBufs* chunks;
+    const ChunkPush* push;  // null unless the plan pushes its halo
     int parity;
     int64_t ex, ey, sx, origin;
     int64_t rows;          // rows per CTA tile
@@ -386,7 +395,8 @@ __device__ __forceinline__ double div6_t(double s) {
     else return div6_fast(s);
 }
 
-template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, int STAGES = T4_STAGES>
+template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, bool PUSH = false,
+          int STAGES = T4_STAGES>
 __global__ void __launch_bounds__(32 * (CW + 1))
 slab_update_tma4_kernel(SlabArgs a) {
     __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
@@ -449,6 +459,22 @@ slab_update_tma4_kernel(SlabArgs a) {
     double rmax = 0.0;
     int s = 0;
     uint32_t ph = 0;
+    // push targets of this chunk for the buffer being written (face order
+    // north, south, west, east = FACES 0..3); null: domain face
+    double *pn = nullptr, *ps = nullptr, *pw = nullptr, *pe = nullptr;
+    int64_t sn = 0, ss = 0, sw = 0, se = 0;
+    if (PUSH) {
+        const ChunkPush& cp = a.push[c];
+        const int wp = a.parity ^ 1;
+        pn = cp.ptr[0][wp];
+        ps = cp.ptr[1][wp];
+        pw = cp.ptr[2][wp];
+        pe = cp.ptr[3][wp];
+        sn = cp.stride[0];
+        ss = cp.stride[1];
+        sw = cp.stride[2];
+        se = cp.stride[3];
+    }
 
     auto take = [&](double (&v)[4], double& l, double& r) {
         mbar_wait(&full[s], ph);
@@ -497,6 +523,26 @@ slab_update_tma4_kernel(SlabArgs a) {
                     wr[k] = o[k];
                     if (RESID) rmax = fmax(rmax, fabs(__dsub_rn(o[k], mid[k])));
                 }
+        }
+        if (PUSH) {
+            // fused halo: boundary rows/columns of the new field go straight
+            // into the neighbours' ghost planes of the same buffer parity
+            // (same GPU, a peer GPU over NVLink, or a packed NCCL staging
+            // slot) — the reference's pack -> mp_send -> unpack (jacobi.py:
+            // 102-124, 237) as extra stores of the producing kernel
+            const int64_t r = i0 - 2 + q;
+            if (r == 1 && pn) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nv) pn[(j - 1 + k) * sn] = o[k];
+            }
+            if (r == a.ex && ps) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nv) ps[(j - 1 + k) * ss] = o[k];
+            }
+            if (j == 1 && pw) pw[(r - 1) * sw] = o[0];
+            if (pe && nv > 0 && j + nv - 1 == a.ey) pe[(r - 1) * se] = o[nv - 1];
         }
         wr += sx;
 #pragma unroll
@@ -844,6 +890,9 @@ struct Plan {
     int64_t seg_blocks = 1;
     hrt_halo_seg_t* d_post = nullptr;
     int64_t* d_offs = nullptr;  // chunk origins in the field (field_copy)
+    ChunkPush* d_push = nullptr;  // fused halo push table (slab variant 2)
+    bool ghosts_ready = false;    // ghost planes of the next buffer are current
+    bool push_on() const { return d_push != nullptr && L.ndim == 2 && variant == 2; }
     int npost = 0;
     int64_t post_blocks = 1;
     std::vector<hrt_remote_seg_t> remote;
@@ -878,6 +927,7 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
     if (L.ndim == 2) {
         SlabArgs a;
         a.chunks = p->d_chunks;
+        a.push = p->push_on() ? p->d_push : nullptr;
         a.parity = parity;
         a.ex = L.ext[0];
         a.ey = L.ext[1];
@@ -897,7 +947,11 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         if (p->variant == 2) {
             const bool guard = !p->nonneg;
             const unsigned g = (unsigned)grid;
-#define T4_LAUNCH(G, R, CW) slab_update_tma4_kernel<G, R, CW><<<g, 32 * (CW + 1), 0, s>>>(a)
+#define T4_LAUNCH(G, R, CW)                                                              \
+    do {                                                                                 \
+        if (a.push) slab_update_tma4_kernel<G, R, CW, true><<<g, 32 * (CW + 1), 0, s>>>(a); \
+        else slab_update_tma4_kernel<G, R, CW, false><<<g, 32 * (CW + 1), 0, s>>>(a);      \
+    } while (0)
             if (narrow) {
                 if (guard && resid) T4_LAUNCH(true, true, 2);
                 else if (guard) T4_LAUNCH(true, false, 2);
@@ -962,11 +1016,47 @@ static int launch_halo(Plan* p, cudaStream_t s, int parity) {
     return HRT_OK;
 }
 
-static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
-    const int parity = (int)(step & 1);
+// cross-process faces only: NCCL exchange of the (pushed or packed) staging
+// buffers, then unpack into the ghost planes of `parity`
+static int launch_remote(Plan* p, cudaStream_t s, int parity) {
+    if (p->remote.empty()) return HRT_OK;
+    Stream tmp;
+    tmp.s = s;
+    tmp.gpu = p->gpu;
+    int rc = hrt_nccl_exchange(p->comm, &tmp, p->remote.data(), (int)p->remote.size(), parity);
+    if (rc) return rc;
+    if (p->npost > 0) {
+        halo_copy_kernel<<<(unsigned)(p->npost * p->post_blocks), HALO_THREADS, 0, s>>>(
+            p->d_post, parity, p->post_blocks);
+        HRT_CUDA(cudaGetLastError());
+    }
+    return HRT_OK;
+}
+
+// Push mode: the update kernel writes the next buffer's ghost planes (and
+// the remote send staging) itself, so a step is update + remote exchange;
+// the full halo pass runs only when the ghosts are stale (after an upload).
+static int prime_ghosts(Plan* p, cudaStream_t s, int parity) {
+    if (!p->push_on() || p->ghosts_ready) return HRT_OK;
     int rc = launch_halo(p, s, parity);
     if (rc) return rc;
-    return launch_update(p, s, parity, resid_base ? resid_base + step : nullptr);
+    p->ghosts_ready = true;
+    return HRT_OK;
+}
+
+static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
+    const int parity = (int)(step & 1);
+    unsigned long long* slot = resid_base ? resid_base + step : nullptr;
+    if (p->push_on()) {
+        int rc = prime_ghosts(p, s, parity);
+        if (rc) return rc;
+        rc = launch_update(p, s, parity, slot);
+        if (rc) return rc;
+        return launch_remote(p, s, parity ^ 1);
+    }
+    int rc = launch_halo(p, s, parity);
+    if (rc) return rc;
+    return launch_update(p, s, parity, slot);
 }
 
 extern "C" {
@@ -1055,6 +1145,34 @@ int hrt_jacobi_plan_field_copy(void* plan, void* stream, double* field, int64_t 
         p->d_chunks, p->d_offs, parity & 1, L.ndim, L.ext[0], L.ext[1], L.ext[2], L.stride[0],
         L.stride[1], L.origin, field, FY, FZ, to_chunks);
     HRT_CUDA(cudaGetLastError());
+    if (to_chunks) p->ghosts_ready = false;  // new interiors: ghost planes are stale
+    return HRT_OK;
+}
+
+// Enable the fused halo push (slab variant 2): per chunk (plan order) the
+// ghost-plane targets of its four faces for both parities; null = domain face.
+int hrt_jacobi_plan_set_push(void* plan, const hrt_push_t* table) {
+    HRT_CHECK_ARG(plan, "null plan");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    cudaFree(p->d_push);
+    p->d_push = nullptr;
+    p->ghosts_ready = false;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    if (!table || p->nchunks == 0) return HRT_OK;
+    HRT_CUDA(cudaMalloc(&p->d_push, sizeof(ChunkPush) * p->nchunks));
+    HRT_CUDA(cudaMemcpy(p->d_push, table, sizeof(ChunkPush) * p->nchunks, cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
+// Mark the ghost planes stale (the next step runs the full halo pass first).
+int hrt_jacobi_plan_invalidate_ghosts(void* plan) {
+    HRT_CHECK_ARG(plan, "null plan");
+    reinterpret_cast<Plan*>(plan)->ghosts_ready = false;
     return HRT_OK;
 }
 
@@ -1169,6 +1287,8 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
         k = 1;
     }
     if (n - k >= 2) {
+        rc = prime_ghosts(p, s, 0);  // outside the graph: replays assume current ghosts
+        if (rc) return rc;
         if (!p->graph || p->graph_stream != s) {
             if (p->graph) cudaGraphExecDestroy(p->graph);
             p->graph = nullptr;
@@ -1212,15 +1332,20 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
         ev.push_back(x);
     }
     HRT_CUDA(cudaEventRecord(ev[0], s));
+    const bool push = p->push_on();
     for (int64_t k = 0; k < n; ++k) {
         const int64_t step = first + k;
         const int parity = (int)(step & 1);
-        rc = launch_halo(p, s, parity);
+        rc = push ? prime_ghosts(p, s, parity) : launch_halo(p, s, parity);
         if (rc) break;
         HRT_CUDA(cudaEventRecord(ev[3 * k + 1], s));
         rc = launch_update(p, s, parity, r ? r + step : nullptr);
         if (rc) break;
         HRT_CUDA(cudaEventRecord(ev[3 * k + 2], s));
+        if (push) {
+            rc = launch_remote(p, s, parity ^ 1);
+            if (rc) break;
+        }
         HRT_CUDA(cudaEventRecord(ev[3 * k + 3], s));
     }
     cudaError_t e = cudaStreamSynchronize(s);
@@ -1230,7 +1355,9 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
         for (int64_t k = 0; k < n; ++k) {
             cudaEventElapsedTime(&ms, ev[3 * k + 1], ev[3 * k + 2]);
             up += ms;
-            cudaEventElapsedTime(&ms, k ? ev[3 * k] : ev[0], ev[3 * k + 1]);
+            cudaEventElapsedTime(&ms, ev[3 * k], ev[3 * k + 1]);  // halo before the update
+            ha += ms;
+            cudaEventElapsedTime(&ms, ev[3 * k + 2], ev[3 * k + 3]);  // exchange after it
             ha += ms;
         }
         cudaEventElapsedTime(&ms, ev[0], ev[3 * n]);
@@ -1253,6 +1380,7 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_segs);
     cudaFree(p->d_post);
     cudaFree(p->d_offs);
+    cudaFree(p->d_push);
     delete p;
     return HRT_OK;
 }

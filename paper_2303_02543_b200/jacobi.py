@@ -261,7 +261,8 @@ class JacobiSolver:
 
     def __init__(self, grid: ChunkGrid, gpus: Optional[Sequence[int]] = None,
                  placement: Optional[dict[int, int]] = None, rows: Optional[int] = None,
-                 rank: Optional[int] = None, comm=None, variant: Optional[int] = None):
+                 rank: Optional[int] = None, comm=None, variant: Optional[int] = None,
+                 push: Optional[bool] = None):
         N.require_gpu(0)
         if variant is None and os.environ.get("HRT_SLAB_VARIANT"):
             variant = int(os.environ["HRT_SLAB_VARIANT"])
@@ -330,6 +331,7 @@ class JacobiSolver:
         # exchange latency-bound at one NCCL round per step.
         remote_ops, post = [], []
         g0 = self.used_gpus[0]
+        self._push_remote: dict[tuple[int, int], int] = {}
         groups: dict[tuple[int, int], list] = {}
         for (c, f, nb) in remote_msgs:
             if self.rank_of[nb] == rank:
@@ -350,6 +352,7 @@ class JacobiSolver:
                     _, n0, n1, s0, s1 = pl[0]
                     dst = st + off * F64
                     pre[g0].append(_seg([pl[0][0], pl[1][0]], [dst, dst], n0, n1, s0, s1, n1, 1))
+                    self._push_remote[(nb, opposite(f))] = dst
                 else:  # unpack into c's ghost plane f
                     pl = [face_plane(L, self.bufs[c][p], f, ghost=True) for p in (0, 1)]
                     _, n0, n1, s0, s1 = pl[0]
@@ -391,6 +394,11 @@ class JacobiSolver:
         self.box_lo = tuple(lo)
         self.box = tuple(h - l for l, h in zip(lo, hi))
         self._set_offsets()
+        self.push = bool(push if push is not None else
+                         os.environ.get("HRT_PUSH", "1") != "0") and \
+            L.ndim == 2 and (variant is None or variant == 2)
+        if self.push:
+            self._setup_push()
         self._init_ghosts()
 
     def _set_nonneg(self, flag: bool) -> None:
@@ -456,6 +464,32 @@ class JacobiSolver:
         for g in self.used_gpus:
             N.call("hrt_jacobi_plan_field_copy", self.plans[g], self.streams[g].h,
                    ctypes.c_void_p(field_ptr), Y, Z, parity, 1 if to_chunks else 0)
+
+    def _setup_push(self) -> None:
+        """Fused halo: for every owned chunk and slab face, where the update
+        kernel stores the chunk's new boundary plane for each parity — the
+        neighbour's ghost plane (in place; over NVLink for a chunk on another
+        GPU of this process) or its packed NCCL staging slot."""
+        L = self.layout
+        for g in self.used_gpus:
+            mine = [lin for lin in self.owned if self.placement[lin] == g]
+            table = (N.Push * max(len(mine), 1))()
+            for i, lin in enumerate(mine):
+                for f in range(4):
+                    nb = self.grid.chunks[lin].neighbors.get(f)
+                    if nb is None:
+                        continue
+                    if nb in self.placement:
+                        for p in (0, 1):
+                            addr, _, _, _, s1 = face_plane(L, self.bufs[nb][p], opposite(f),
+                                                           ghost=True)
+                            table[i].ptr[f][p] = addr
+                        table[i].stride[f] = s1
+                    else:
+                        slot = self._push_remote[(lin, f)]
+                        table[i].ptr[f][0] = table[i].ptr[f][1] = slot
+                        table[i].stride[f] = 1
+            N.call("hrt_jacobi_plan_set_push", self.plans[g], ctypes.byref(table))
 
     def _set_offsets(self) -> None:
         for g in self.used_gpus:
