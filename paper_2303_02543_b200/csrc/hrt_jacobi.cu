@@ -461,19 +461,28 @@ slab_update_tma4_kernel(SlabArgs a) {
     uint32_t ph = 0;
     // push targets of this chunk for the buffer being written (face order
     // north, south, west, east = FACES 0..3); null: domain face
-    double *pn = nullptr, *ps = nullptr, *pw = nullptr, *pe = nullptr;
-    int64_t sn = 0, ss = 0, sw = 0, se = 0;
+    // (row planes are contiguous in both targets: in-buffer ghost rows and
+    // staging slots; column planes step by sx or 1)
+    double *pn = nullptr, *ps = nullptr, *pwp = nullptr, *pep = nullptr;
+    int64_t sw = 0, se = 0;
+    bool pw_on = false, pe_on = false;
+    int qrow_n = -1, qrow_s = -1, ke = 0;
     if (PUSH) {
-        const ChunkPush& cp = a.push[c];
+        const ChunkPush* cp = a.push + c;
         const int wp = a.parity ^ 1;
-        pn = cp.ptr[0][wp];
-        ps = cp.ptr[1][wp];
-        pw = cp.ptr[2][wp];
-        pe = cp.ptr[3][wp];
-        sn = cp.stride[0];
-        ss = cp.stride[1];
-        sw = cp.stride[2];
-        se = cp.stride[3];
+        pn = cp->ptr[0][wp];
+        ps = cp->ptr[1][wp];
+        double* pw = cp->ptr[2][wp];
+        double* pe = cp->ptr[3][wp];
+        sw = cp->stride[2];
+        se = cp->stride[3];
+        if (pn && i0 == 1) qrow_n = 2;                 // output row 1 is this tile's first
+        if (ps && i1 == a.ex) qrow_s = (int)(i1 - i0) + 2;  // output row ex is its last
+        pw_on = pw != nullptr && j == 1;
+        pe_on = pe != nullptr && nv > 0 && j + nv - 1 == a.ey;
+        ke = nv - 1;
+        if (pw_on) pwp = pw + (i0 - 1) * sw;
+        if (pe_on) pep = pe + (i0 - 1) * se;
     }
 
     auto take = [&](double (&v)[4], double& l, double& r) {
@@ -529,20 +538,26 @@ slab_update_tma4_kernel(SlabArgs a) {
             // into the neighbours' ghost planes of the same buffer parity
             // (same GPU, a peer GPU over NVLink, or a packed NCCL staging
             // slot) — the reference's pack -> mp_send -> unpack (jacobi.py:
-            // 102-124, 237) as extra stores of the producing kernel
-            const int64_t r = i0 - 2 + q;
-            if (r == 1 && pn) {
+            // 102-124, 237) as extra stores of the producing kernel.  All
+            // predicates are hoisted; per row this is two predicated stores.
+            if (pw_on) {
+                *pwp = o[0];
+                pwp += sw;
+            }
+            if (pe_on) {
+                *pep = ke == 3 ? o[3] : (ke == 2 ? o[2] : (ke == 1 ? o[1] : o[0]));
+                pep += se;
+            }
+            if (q == qrow_n) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (k < nv) pn[(j - 1 + k) * sn] = o[k];
+                    if (k < nv) pn[j - 1 + k] = o[k];
             }
-            if (r == a.ex && ps) {
+            if (q == qrow_s) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (k < nv) ps[(j - 1 + k) * ss] = o[k];
+                    if (k < nv) ps[j - 1 + k] = o[k];
             }
-            if (j == 1 && pw) pw[(r - 1) * sw] = o[0];
-            if (pe && nv > 0 && j + nv - 1 == a.ey) pe[(r - 1) * se] = o[nv - 1];
         }
         wr += sx;
 #pragma unroll
