@@ -235,7 +235,9 @@ def run_ours(args):
     achieved = BYTES_PER_UPDATE * my_cells / (avg_upd_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": args.traffic,
+                "frac": round(achieved / peak, 4),
+                "traffic": args.traffic if args.traffic is not None else
+                _recorded_traffic(wl["name"], world),
                 "kernel": {None: "slab_update_tma4_kernel<false,true>",
                            2: "slab_update_tma4_kernel<false,true>",
                            1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant],
@@ -370,19 +372,19 @@ def main():
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("need --steps >= 1")
-    if args.traffic is None:
-        args.traffic = _recorded_traffic()
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
 
 
-def _recorded_traffic():
-    """dram read+write bytes per update launch from the committed ncu capture."""
+def _recorded_traffic(workload: str, world: int):
+    """DRAM read+write bytes per update launch from the committed ncu capture
+    of the same workload on one GPU (profiles/traffic.json), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            return json.load(fh).get("bytes_per_launch")
+            entry = json.load(fh).get(workload)
+        return entry["bytes_per_launch"] if entry and world == 1 else None
     except Exception:
         return None
 
