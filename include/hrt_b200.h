@@ -162,6 +162,11 @@ int hrt_jacobi_plan_set_offsets(void *plan, const int64_t *offs3);
  * the full halo pass runs only when ghosts are stale (after an upload) */
 int hrt_jacobi_plan_set_push(void *plan, const hrt_push_t *table);
 int hrt_jacobi_plan_invalidate_ghosts(void *plan);
+/* overlap for cross-process faces (push mode): remote_mask[c] bit f = face f
+ * of chunk c crosses a process; tiles touching such faces run first, then
+ * the NCCL exchange runs on a side stream while the other tiles compute.
+ * NULL disables. */
+int hrt_jacobi_plan_set_split(void *plan, const int32_t *remote_mask);
 int hrt_jacobi_plan_field_copy(void *plan, void *stream, double *field, int64_t FY, int64_t FZ,
                                int parity, int to_chunks);
 /* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,

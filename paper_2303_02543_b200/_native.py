@@ -95,6 +95,7 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_offsets": (c_int, [c_void_p, P(c_i64)]),
     "hrt_jacobi_plan_set_push": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_invalidate_ghosts": (c_int, [c_void_p]),
+    "hrt_jacobi_plan_set_split": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_field_copy": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_i64, c_int,
                                            c_int]),
     "hrt_jacobi_plan_set_variant": (c_int, [c_void_p, c_int]),

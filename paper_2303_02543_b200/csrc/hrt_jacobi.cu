@@ -97,6 +97,7 @@ static_assert(sizeof(ChunkPush) == sizeof(hrt_push_t), "ChunkPush layout");
 struct SlabArgs {
     const ChunkBufs* chunks;
     const ChunkPush* push;  // null unless the plan pushes its halo
+    const int* tiles;       // null: all tiles (dense); else (chunk, rb, cb) triples
     int parity;
     int64_t ex, ey, sx, origin;
     int64_t rows;          // rows per CTA tile
@@ -403,12 +404,20 @@ slab_update_tma4_kernel(SlabArgs a) {
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES];
     __shared__ double red[CW];
 
-    const int64_t per_chunk = a.tiles_r * a.tiles_c;
-    const int64_t t = blockIdx.x;
-    const int64_t c = t / per_chunk;
-    const int64_t rem = t - c * per_chunk;
-    const int64_t rb = rem / a.tiles_c;
-    const int64_t cb = rem - rb * a.tiles_c;
+    int64_t c, rb, cb;
+    if (a.tiles) {  // explicit tile subset (split schedule)
+        const int* tt = a.tiles + 3 * (int64_t)blockIdx.x;
+        c = tt[0];
+        rb = tt[1];
+        cb = tt[2];
+    } else {
+        const int64_t per_chunk = a.tiles_r * a.tiles_c;
+        const int64_t t = blockIdx.x;
+        c = t / per_chunk;
+        const int64_t rem = t - c * per_chunk;
+        rb = rem / a.tiles_c;
+        cb = rem - rb * a.tiles_c;
+    }
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
@@ -908,6 +917,16 @@ struct Plan {
     ChunkPush* d_push = nullptr;  // fused halo push table (slab variant 2)
     bool ghosts_ready = false;    // ghost planes of the next buffer are current
     bool push_on() const { return d_push != nullptr && L.ndim == 2 && variant == 2; }
+    // split schedule (push mode with remote faces): edge tiles first, the
+    // NCCL exchange on `side` overlapped with the inner tiles
+    int* d_tiles_edge = nullptr;
+    int* d_tiles_inner = nullptr;
+    int64_t n_edge = 0, n_inner = 0;
+    int64_t split_rows = 0;  // rows value the tile lists were built for
+    std::vector<int> remote_mask;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool split_on() const { return push_on() && side != nullptr && !remote.empty(); }
     int npost = 0;
     int64_t post_blocks = 1;
     std::vector<hrt_remote_seg_t> remote;
@@ -937,12 +956,15 @@ using namespace hrt;
 extern "C" int hrt_nccl_exchange(void* comm, void* stream, const hrt_remote_seg_t* segs, int n,
                                  int parity);
 
-static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long* resid) {
+// subset: 0 every tile, 1 the edge tiles (they feed remote faces), 2 the rest
+static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long* resid,
+                         int subset = 0) {
     const hrt_chunk_layout_t& L = p->L;
     if (L.ndim == 2) {
         SlabArgs a;
         a.chunks = p->d_chunks;
         a.push = p->push_on() ? p->d_push : nullptr;
+        a.tiles = subset == 1 ? p->d_tiles_edge : (subset == 2 ? p->d_tiles_inner : nullptr);
         a.parity = parity;
         a.ex = L.ext[0];
         a.ey = L.ext[1];
@@ -957,7 +979,9 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.tiles_c = (a.ey + cols - 1) / cols;
         a.resid = resid;
         a.zghost = HRT_BOUNDARY;
-        const int64_t grid = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
+        const int64_t grid = subset == 1 ? p->n_edge
+                           : subset == 2 ? p->n_inner
+                                         : (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
         if (grid == 0) return HRT_OK;
         if (p->variant == 2) {
             const bool guard = !p->nonneg;
@@ -1059,9 +1083,69 @@ static int prime_ghosts(Plan* p, cudaStream_t s, int parity) {
     return HRT_OK;
 }
 
+// (Re)build the edge / inner tile lists for the current tiling.
+static int build_split(Plan* p) {
+    const hrt_chunk_layout_t& L = p->L;
+    const int64_t ex = L.ext[0], ey = L.ext[1];
+    const int64_t tr = (ex + p->rows - 1) / p->rows;
+    const int cols = ey <= 256 ? 256 : T4_COLS;
+    const int64_t tc = (ey + cols - 1) / cols;
+    std::vector<int> edge, inner;
+    for (int64_t c = 0; c < p->nchunks; ++c) {
+        const int m = p->remote_mask[c];
+        for (int64_t rb = 0; rb < tr; ++rb)
+            for (int64_t cb = 0; cb < tc; ++cb) {
+                const bool e = ((m & 1) && rb == 0) || ((m & 2) && rb == tr - 1) ||
+                               ((m & 4) && cb == 0) || ((m & 8) && cb == tc - 1);
+                auto& v = e ? edge : inner;
+                v.push_back((int)c);
+                v.push_back((int)rb);
+                v.push_back((int)cb);
+            }
+    }
+    cudaFree(p->d_tiles_edge);
+    cudaFree(p->d_tiles_inner);
+    p->d_tiles_edge = p->d_tiles_inner = nullptr;
+    p->n_edge = (int64_t)edge.size() / 3;
+    p->n_inner = (int64_t)inner.size() / 3;
+    if (!edge.empty()) {
+        HRT_CUDA(cudaMalloc(&p->d_tiles_edge, edge.size() * sizeof(int)));
+        HRT_CUDA(cudaMemcpy(p->d_tiles_edge, edge.data(), edge.size() * sizeof(int),
+                            cudaMemcpyHostToDevice));
+    }
+    if (!inner.empty()) {
+        HRT_CUDA(cudaMalloc(&p->d_tiles_inner, inner.size() * sizeof(int)));
+        HRT_CUDA(cudaMemcpy(p->d_tiles_inner, inner.data(), inner.size() * sizeof(int),
+                            cudaMemcpyHostToDevice));
+    }
+    p->split_rows = p->rows;
+    return HRT_OK;
+}
+
 static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
     const int parity = (int)(step & 1);
     unsigned long long* slot = resid_base ? resid_base + step : nullptr;
+    if (p->split_on()) {
+        // edge tiles (they push into the NCCL staging) -> fork: exchange +
+        // unpack on the side stream || inner tiles on the main stream -> join
+        int rc = prime_ghosts(p, s, parity);
+        if (rc) return rc;
+        if (p->split_rows != p->rows) {
+            rc = build_split(p);
+            if (rc) return rc;
+        }
+        rc = launch_update(p, s, parity, slot, 1);
+        if (rc) return rc;
+        HRT_CUDA(cudaEventRecord(p->ev_fork, s));
+        HRT_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+        rc = launch_remote(p, p->side, parity ^ 1);
+        if (rc) return rc;
+        HRT_CUDA(cudaEventRecord(p->ev_join, p->side));
+        rc = launch_update(p, s, parity, slot, 2);
+        if (rc) return rc;
+        HRT_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+        return HRT_OK;
+    }
     if (p->push_on()) {
         int rc = prime_ghosts(p, s, parity);
         if (rc) return rc;
@@ -1182,6 +1266,38 @@ int hrt_jacobi_plan_set_push(void* plan, const hrt_push_t* table) {
     HRT_CUDA(cudaMalloc(&p->d_push, sizeof(ChunkPush) * p->nchunks));
     HRT_CUDA(cudaMemcpy(p->d_push, table, sizeof(ChunkPush) * p->nchunks, cudaMemcpyHostToDevice));
     return HRT_OK;
+}
+
+// Split schedule for push mode with remote faces: remote_mask[c] has bit f
+// set when face f of chunk c (plan order) crosses a process boundary; tiles
+// touching such faces run first, the NCCL exchange overlaps the rest.
+// NULL disables.
+int hrt_jacobi_plan_set_split(void* plan, const int32_t* remote_mask) {
+    HRT_CHECK_ARG(plan, "null plan");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    if (!remote_mask) {
+        if (p->side) cudaStreamDestroy(p->side);
+        if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+        if (p->ev_join) cudaEventDestroy(p->ev_join);
+        p->side = nullptr;
+        p->ev_fork = p->ev_join = nullptr;
+        return HRT_OK;
+    }
+    p->remote_mask.assign(remote_mask, remote_mask + p->nchunks);
+    if (!p->side) {
+        int lo = 0, hi = 0;
+        HRT_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        HRT_CUDA(cudaStreamCreateWithPriority(&p->side, cudaStreamNonBlocking, hi));
+        HRT_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        HRT_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    }
+    return build_split(p);
 }
 
 // Mark the ghost planes stale (the next step runs the full halo pass first).
@@ -1348,12 +1464,21 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
     }
     HRT_CUDA(cudaEventRecord(ev[0], s));
     const bool push = p->push_on();
+    const bool split = p->split_on();
     for (int64_t k = 0; k < n; ++k) {
         const int64_t step = first + k;
         const int parity = (int)(step & 1);
         rc = push ? prime_ghosts(p, s, parity) : launch_halo(p, s, parity);
         if (rc) break;
         HRT_CUDA(cudaEventRecord(ev[3 * k + 1], s));
+        if (split) {
+            // "update" here spans edge tiles + overlapped exchange + inner tiles
+            rc = do_step(p, s, step, r);
+            if (rc) break;
+            HRT_CUDA(cudaEventRecord(ev[3 * k + 2], s));
+            HRT_CUDA(cudaEventRecord(ev[3 * k + 3], s));
+            continue;
+        }
         rc = launch_update(p, s, parity, r ? r + step : nullptr);
         if (rc) break;
         HRT_CUDA(cudaEventRecord(ev[3 * k + 2], s));
@@ -1396,6 +1521,11 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_post);
     cudaFree(p->d_offs);
     cudaFree(p->d_push);
+    cudaFree(p->d_tiles_edge);
+    cudaFree(p->d_tiles_inner);
+    if (p->side) cudaStreamDestroy(p->side);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
     delete p;
     return HRT_OK;
 }

@@ -490,6 +490,12 @@ class JacobiSolver:
                         table[i].ptr[f][0] = table[i].ptr[f][1] = slot
                         table[i].stride[f] = 1
             N.call("hrt_jacobi_plan_set_push", self.plans[g], ctypes.byref(table))
+            # overlap the NCCL exchange with the tiles that do not feed it
+            masks = [sum(1 << f for f, nb in self.grid.chunks[lin].neighbors.items()
+                         if f < 4 and nb not in self.placement) for lin in mine]
+            if any(masks) and os.environ.get("HRT_SPLIT", "1") != "0":
+                N.call("hrt_jacobi_plan_set_split", self.plans[g],
+                       _arr(ctypes.c_int32, masks))
 
     def _set_offsets(self) -> None:
         for g in self.used_gpus:
