@@ -49,6 +49,11 @@ int hrt_device_info(int gpu, char *name, int name_len, int *sm_count, uint64_t *
 int hrt_enable_peer_access(int gpu, int peer);
 int hrt_device_synchronize(int gpu);
 int hrt_pointer_device(const void *ptr, int *gpu);
+/* CUDA IPC (same node): export a cudaMalloc base (64-byte handle), map a
+ * handle from another process on `gpu` (peer access over NVLink), unmap */
+int hrt_ipc_get_handle(const void *base, uint8_t *out64);
+int hrt_ipc_open_handle(int gpu, const uint8_t *in64, void **ptr);
+int hrt_ipc_close_handle(void *ptr);
 
 /* ---- first-fit free list: FreeListAllocator devices.py:89-154 (host logic) ---- */
 int hrt_fl_create(uint64_t capacity, uint64_t alignment, void **fl);
@@ -167,6 +172,16 @@ int hrt_jacobi_plan_invalidate_ghosts(void *plan);
  * the NCCL exchange runs on a side stream while the other tiles compute.
  * NULL disables. */
 int hrt_jacobi_plan_set_split(void *plan, const int32_t *remote_mask);
+/* fused compute + communication across processes: the push table's remote
+ * entries point into the neighbours' IPC-mapped ghost planes; edge tiles
+ * (remote_mask as above) wait in-kernel for the neighbours' previous step
+ * (flags in `arrived`, written by them over NVLink), push, and the last one
+ * publishes the step into each neighbour's slot (remote_slots[k]).  No NCCL
+ * in the step; a neighbour silent for timeout_ns sets an error instead of
+ * hanging (hrt_jacobi_plan_ipc_error). */
+int hrt_jacobi_plan_set_ipc(void *plan, const int32_t *remote_mask, uint64_t *arrived, int n_nbr,
+                            const uint64_t *remote_slots, uint64_t timeout_ns);
+int hrt_jacobi_plan_ipc_error(void *plan, int *err);
 int hrt_jacobi_plan_field_copy(void *plan, void *stream, double *field, int64_t FY, int64_t FZ,
                                int parity, int to_chunks);
 /* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,

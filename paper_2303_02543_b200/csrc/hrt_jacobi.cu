@@ -98,6 +98,16 @@ struct SlabArgs {
     const ChunkBufs* chunks;
     const ChunkPush* push;  // null unless the plan pushes its halo
     const int* tiles;       // null: all tiles (dense); else (chunk, rb, cb) triples
+    // cross-process IPC push sync (null arrived: none).  Tiles [0, n_edge)
+    // of the tile list touch remote faces.
+    unsigned long long* arrived;                 // [n_nbr] steps published to us
+    unsigned long long* const* remote_slots;     // [n_nbr] our slot in each neighbour
+    int n_nbr;
+    unsigned int* edge_done;                     // per-parity edge-tile counter
+    int64_t n_edge;
+    unsigned long long tag;                      // this step + 1
+    unsigned long long timeout_ns;
+    int* err;
     int parity;
     int64_t ex, ey, sx, origin;
     int64_t rows;          // rows per CTA tile
@@ -396,6 +406,52 @@ __device__ __forceinline__ double div6_t(double s) {
     else return div6_fast(s);
 }
 
+// ---- cross-process step flags (IPC push mode) ----
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// step tag-1 published by every neighbour = its edge tiles of the previous
+// step are done.  A stuck neighbour raises *err after timeout_ns instead of
+// hanging the GPU.
+__device__ void sync_wait_neighbours(const SlabArgs& a) {
+    const unsigned long long need = a.tag - 1;
+    const unsigned long long t0 = globaltimer_ns();
+    for (int k = 0; k < a.n_nbr; ++k) {
+        while (ld_acquire_sys(a.arrived + k) < need) {
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+                atomicExch(a.err, 1);
+                return;
+            }
+            __nanosleep(100);
+        }
+    }
+    // peers wrote our ghost planes with generic stores; the producer reads
+    // them with TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// the last edge tile of this step publishes tag to every neighbour
+__device__ void sync_signal_neighbours(const SlabArgs& a) {
+    unsigned int* cnt = a.edge_done + a.parity;
+    const unsigned int old = atomicAdd(cnt, 1u);
+    if (old == (unsigned int)(a.n_edge - 1)) {
+        *cnt = 0;  // reused two steps later, after this kernel has ended
+        __threadfence_system();
+        for (int k = 0; k < a.n_nbr; ++k) st_release_sys(a.remote_slots[k], a.tag);
+    }
+}
+
 template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, bool PUSH = false,
           int STAGES = T4_STAGES>
 __global__ void __launch_bounds__(32 * (CW + 1))
@@ -430,8 +486,14 @@ slab_update_tma4_kernel(SlabArgs a) {
     const int64_t i1 = min(a.ex, i0 + a.rows - 1);
     const int nrows = (int)(i1 - i0 + 3);
     const int64_t sx = a.sx;
+    // cross-process edge tile (IPC push mode): wait until every remote
+    // neighbour finished its edge tiles of the previous step — their pushes
+    // into our ghost planes have landed (RAW) and they no longer read the
+    // ghost planes we are about to push into (WAR).  Inner tiles never wait.
+    const bool xedge = a.arrived != nullptr && (int64_t)blockIdx.x < a.n_edge;
 
     if (tid == 0) {
+        if (xedge) sync_wait_neighbours(a);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], CW);
@@ -588,6 +650,13 @@ slab_update_tma4_kernel(SlabArgs a) {
             for (int k = 1; k < CW; ++k) m = fmax(m, red[k]);
             resid_max(a.resid, m);
         }
+    }
+    if (xedge) {
+        // our pushes (peer stores over NVLink) are visible system-wide before
+        // the last edge tile of this step publishes the step to neighbours
+        __threadfence_system();
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * CW));
+        if (tid == 0) sync_signal_neighbours(a);
     }
 }
 
@@ -926,7 +995,20 @@ struct Plan {
     std::vector<int> remote_mask;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool split_on() const { return push_on() && side != nullptr && !remote.empty(); }
+    bool split_on() const { return push_on() && side != nullptr && !remote.empty() && !ipc; }
+    // IPC push mode: remote faces are pushed straight into the neighbour
+    // processes' ghost planes (CUDA IPC mappings); per-step flags replace
+    // the NCCL exchange (which only primes ghosts after an upload)
+    bool ipc = false;
+    unsigned long long* d_arrived = nullptr;          // owned by the caller
+    unsigned long long** d_remote_slots = nullptr;    // device array (plan-owned)
+    unsigned int* d_edge_done = nullptr;              // plan-owned, 2 slots
+    int* d_err = nullptr;                             // plan-owned
+    int n_nbr = 0;
+    unsigned long long gstep = 0;                     // global step counter (tags)
+    unsigned long long timeout_ns = 30000000000ULL;
+    int* d_tiles_all = nullptr;                       // edge tiles then inner tiles
+    bool ipc_on() const { return ipc && push_on(); }
     int npost = 0;
     int64_t post_blocks = 1;
     std::vector<hrt_remote_seg_t> remote;
@@ -961,10 +1043,23 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
                          int subset = 0) {
     const hrt_chunk_layout_t& L = p->L;
     if (L.ndim == 2) {
-        SlabArgs a;
+        SlabArgs a{};
         a.chunks = p->d_chunks;
         a.push = p->push_on() ? p->d_push : nullptr;
-        a.tiles = subset == 1 ? p->d_tiles_edge : (subset == 2 ? p->d_tiles_inner : nullptr);
+        a.tiles = subset == 1   ? p->d_tiles_edge
+                  : subset == 2 ? p->d_tiles_inner
+                  : subset == 3 ? p->d_tiles_all
+                                : nullptr;
+        if (subset == 3 && p->ipc_on()) {
+            a.arrived = p->d_arrived;
+            a.remote_slots = p->d_remote_slots;
+            a.n_nbr = p->n_nbr;
+            a.edge_done = p->d_edge_done;
+            a.n_edge = p->n_edge;
+            a.tag = p->gstep + 1;
+            a.timeout_ns = p->timeout_ns;
+            a.err = p->d_err;
+        }
         a.parity = parity;
         a.ex = L.ext[0];
         a.ey = L.ext[1];
@@ -979,9 +1074,10 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.tiles_c = (a.ey + cols - 1) / cols;
         a.resid = resid;
         a.zghost = HRT_BOUNDARY;
-        const int64_t grid = subset == 1 ? p->n_edge
-                           : subset == 2 ? p->n_inner
-                                         : (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
+        const int64_t grid = subset == 1   ? p->n_edge
+                             : subset == 2 ? p->n_inner
+                             : subset == 3 ? p->n_edge + p->n_inner
+                                           : (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
         if (grid == 0) return HRT_OK;
         if (p->variant == 2) {
             const bool guard = !p->nonneg;
@@ -1105,9 +1201,19 @@ static int build_split(Plan* p) {
     }
     cudaFree(p->d_tiles_edge);
     cudaFree(p->d_tiles_inner);
-    p->d_tiles_edge = p->d_tiles_inner = nullptr;
+    cudaFree(p->d_tiles_all);
+    p->d_tiles_edge = p->d_tiles_inner = p->d_tiles_all = nullptr;
     p->n_edge = (int64_t)edge.size() / 3;
     p->n_inner = (int64_t)inner.size() / 3;
+    {
+        std::vector<int> all(edge);
+        all.insert(all.end(), inner.begin(), inner.end());
+        if (!all.empty()) {
+            HRT_CUDA(cudaMalloc(&p->d_tiles_all, all.size() * sizeof(int)));
+            HRT_CUDA(cudaMemcpy(p->d_tiles_all, all.data(), all.size() * sizeof(int),
+                                cudaMemcpyHostToDevice));
+        }
+    }
     if (!edge.empty()) {
         HRT_CUDA(cudaMalloc(&p->d_tiles_edge, edge.size() * sizeof(int)));
         HRT_CUDA(cudaMemcpy(p->d_tiles_edge, edge.data(), edge.size() * sizeof(int),
@@ -1125,6 +1231,20 @@ static int build_split(Plan* p) {
 static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
     const int parity = (int)(step & 1);
     unsigned long long* slot = resid_base ? resid_base + step : nullptr;
+    if (p->ipc_on()) {
+        // one launch, edge tiles first: they wait for / signal the
+        // neighbour processes and push over NVLink; no NCCL in the step
+        int rc = prime_ghosts(p, s, parity);
+        if (rc) return rc;
+        if (p->split_rows != p->rows) {
+            rc = build_split(p);
+            if (rc) return rc;
+        }
+        rc = launch_update(p, s, parity, slot, 3);
+        if (rc) return rc;
+        ++p->gstep;
+        return HRT_OK;
+    }
     if (p->split_on()) {
         // edge tiles (they push into the NCCL staging) -> fork: exchange +
         // unpack on the side stream || inner tiles on the main stream -> join
@@ -1300,6 +1420,54 @@ int hrt_jacobi_plan_set_split(void* plan, const int32_t* remote_mask) {
     return build_split(p);
 }
 
+// IPC push mode for cross-process faces (the push table's remote entries
+// must point into the neighbours' IPC-mapped ghost planes).  remote_mask as
+// for set_split; arrived: this process's n_nbr flag slots (device, zeroed,
+// IPC-exported so neighbours can publish into them); remote_slots: host array
+// of the n_nbr device addresses of our slot in each neighbour's flags.
+int hrt_jacobi_plan_set_ipc(void* plan, const int32_t* remote_mask, uint64_t* arrived, int n_nbr,
+                            const uint64_t* remote_slots, uint64_t timeout_ns) {
+    HRT_CHECK_ARG(plan && remote_mask && arrived && remote_slots && n_nbr > 0, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    p->remote_mask.assign(remote_mask, remote_mask + p->nchunks);
+    rc = build_split(p);
+    if (rc) return rc;
+    cudaFree(p->d_remote_slots);
+    p->d_remote_slots = nullptr;
+    HRT_CUDA(cudaMalloc(&p->d_remote_slots, sizeof(uint64_t) * n_nbr));
+    HRT_CUDA(cudaMemcpy(p->d_remote_slots, remote_slots, sizeof(uint64_t) * n_nbr,
+                        cudaMemcpyHostToDevice));
+    if (!p->d_edge_done) {
+        HRT_CUDA(cudaMalloc(&p->d_edge_done, 2 * sizeof(unsigned int)));
+        HRT_CUDA(cudaMalloc(&p->d_err, sizeof(int)));
+    }
+    HRT_CUDA(cudaMemset(p->d_edge_done, 0, 2 * sizeof(unsigned int)));
+    HRT_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+    p->d_arrived = reinterpret_cast<unsigned long long*>(arrived);
+    p->n_nbr = n_nbr;
+    p->timeout_ns = timeout_ns ? timeout_ns : 30000000000ULL;
+    p->ipc = true;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    return HRT_OK;
+}
+
+// Synchronises; *err = 1 if an edge tile timed out waiting for a neighbour.
+int hrt_jacobi_plan_ipc_error(void* plan, int* err) {
+    HRT_CHECK_ARG(plan && err, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    *err = 0;
+    if (!p->d_err) return HRT_OK;
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaMemcpy(err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    return HRT_OK;
+}
+
 // Mark the ghost planes stale (the next step runs the full halo pass first).
 int hrt_jacobi_plan_invalidate_ghosts(void* plan) {
     HRT_CHECK_ARG(plan, "null plan");
@@ -1404,7 +1572,7 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
     if (rc) return rc;
     cudaStream_t s = as_stream(stream)->s;
     unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
-    if (mode == 0 || r != nullptr) {
+    if (mode == 0 || r != nullptr || p->ipc_on()) {  // IPC step tags are per launch
         for (int64_t k = 0; k < n; ++k) {
             rc = do_step(p, s, first + k, r);
             if (rc) return rc;
@@ -1464,7 +1632,7 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
     }
     HRT_CUDA(cudaEventRecord(ev[0], s));
     const bool push = p->push_on();
-    const bool split = p->split_on();
+    const bool split = p->split_on() || p->ipc_on();
     for (int64_t k = 0; k < n; ++k) {
         const int64_t step = first + k;
         const int parity = (int)(step & 1);
@@ -1523,6 +1691,10 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_push);
     cudaFree(p->d_tiles_edge);
     cudaFree(p->d_tiles_inner);
+    cudaFree(p->d_tiles_all);
+    cudaFree(p->d_remote_slots);
+    cudaFree(p->d_edge_done);
+    cudaFree(p->d_err);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);

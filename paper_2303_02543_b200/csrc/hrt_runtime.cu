@@ -517,6 +517,32 @@ int hrt_memset_async(void* stream, void* dst, int value, uint64_t bytes) {
     return HRT_OK;
 }
 
+// ---- CUDA IPC: map another process's device allocation (same node) ----
+
+int hrt_ipc_get_handle(const void* base, uint8_t* out64) {
+    HRT_CHECK_ARG(base && out64, "null argument");
+    cudaIpcMemHandle_t h;
+    HRT_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(base)));
+    memcpy(out64, &h, sizeof(h));
+    return HRT_OK;
+}
+
+int hrt_ipc_open_handle(int gpu, const uint8_t* in64, void** ptr) {
+    HRT_CHECK_ARG(in64 && ptr, "null argument");
+    int rc = use_device(gpu);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, in64, sizeof(h));
+    HRT_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return HRT_OK;
+}
+
+int hrt_ipc_close_handle(void* ptr) {
+    if (!ptr) return HRT_OK;
+    HRT_CUDA(cudaIpcCloseMemHandle(ptr));
+    return HRT_OK;
+}
+
 int hrt_pointer_device(const void* ptr, int* gpu) {
     HRT_CHECK_ARG(gpu, "null out pointer");
     cudaPointerAttributes a;

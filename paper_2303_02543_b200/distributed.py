@@ -19,7 +19,9 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
-from .jacobi import ChunkGrid, JacobiSolver
+from .devices import DevicePool
+from .errors import HrtError
+from .jacobi import ChunkGrid, JacobiSolver, _arr, face_plane, opposite
 
 
 def env_rank() -> tuple[int, int, int]:
@@ -71,7 +73,84 @@ class DistributedJacobi(JacobiSolver):
         if comm is None and world > 1:
             comm = nccl_comm(rank, world, gpu)
         self.world = world
+        self._ipc_maps: list[int] = []
         super().__init__(grid, gpus=[gpu], rank=rank, comm=comm, rows=rows, variant=variant)
+        self.ipc = False
+        if world > 1 and self.push and self.n_remote and os.environ.get("HRT_IPC", "1") != "0":
+            self._setup_ipc(gpu)
+
+    def _setup_ipc(self, gpu: int) -> None:
+        """Fused compute + communication across processes: map the neighbour
+        ranks' chunk arenas with CUDA IPC, point the push table's remote faces
+        at their ghost planes (stores over NVLink from the update kernel) and
+        give every rank one flag slot per neighbour for the per-step
+        handshake.  NCCL remains only for priming ghosts after an upload and
+        for the residual all-reduce."""
+        import torch.distributed as dist
+
+        L = self.layout
+        g = self.used_gpus[0]
+        mine = [lin for lin in self.owned if self.placement[lin] == g]
+        nbr_ranks = sorted({self.rank_of[nb] for lin in mine
+                            for nb in self.grid.chunks[lin].neighbors.values()
+                            if nb not in self.placement})
+        self._flags = DevicePool(g, 4096)
+        N.call("hrt_memset_async", self.streams[g].h, ctypes.c_void_p(self._flags.base), 0, 4096)
+        self.streams[g].synchronize()
+        h_pool = ctypes.create_string_buffer(64)
+        h_flags = ctypes.create_string_buffer(64)
+        N.call("hrt_ipc_get_handle", ctypes.c_void_p(self.pools[g].base), h_pool)
+        N.call("hrt_ipc_get_handle", ctypes.c_void_p(self._flags.base), h_flags)
+        info = (self.rank, h_pool.raw, self.pools[g].base, h_flags.raw,
+                {lin: self.bufs[lin] for lin in mine}, nbr_ranks)
+        every = [None] * self.world
+        dist.all_gather_object(every, info)
+        mapped_pool, mapped_flags = {}, {}
+        for q in nbr_ranks:
+            _, hp, base_q, hf, _, _ = every[q]
+            pp, pf = ctypes.c_void_p(), ctypes.c_void_p()
+            N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(hp, 64), ctypes.byref(pp))
+            N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(hf, 64), ctypes.byref(pf))
+            mapped_pool[q] = (pp.value, base_q)
+            mapped_flags[q] = pf.value
+            self._ipc_maps += [pp.value, pf.value]
+
+        def remote_buf(nb: int, p: int) -> int:
+            q = self.rank_of[nb]
+            mp, base_q = mapped_pool[q]
+            return mp + (every[q][4][nb][p] - base_q)
+
+        table = (N.Push * max(len(mine), 1))()
+        masks = []
+        for i, lin in enumerate(mine):
+            m = 0
+            for f in range(4):
+                nb = self.grid.chunks[lin].neighbors.get(f)
+                if nb is None:
+                    continue
+                for p in (0, 1):
+                    buf = self.bufs[nb][p] if nb in self.placement else remote_buf(nb, p)
+                    addr, _, _, _, s1 = face_plane(L, buf, opposite(f), ghost=True)
+                    table[i].ptr[f][p] = addr
+                table[i].stride[f] = s1
+                if nb not in self.placement:
+                    m |= 1 << f
+            masks.append(m)
+        N.call("hrt_jacobi_plan_set_push", self.plans[g], ctypes.byref(table))
+        slots = [mapped_flags[q] + 8 * every[q][5].index(self.rank) for q in nbr_ranks]
+        N.call("hrt_jacobi_plan_set_ipc", self.plans[g], _arr(ctypes.c_int32, masks),
+               ctypes.c_void_p(self._flags.base), len(nbr_ranks), _arr(ctypes.c_uint64, slots),
+               ctypes.c_uint64(30_000_000_000))
+        self.ipc = True
+        dist.barrier()
+
+    def check_ipc(self) -> None:
+        """Raise if an edge tile timed out waiting for a neighbour rank."""
+        if self.ipc:
+            err = ctypes.c_int()
+            N.call("hrt_jacobi_plan_ipc_error", self.plans[self.used_gpus[0]], ctypes.byref(err))
+            if err.value:
+                raise HrtError("IPC step handshake timed out (a neighbour rank stalled)")
 
     def global_residual_history(self) -> np.ndarray:
         """Per-step max over all ranks (one NCCL max all-reduce of the
@@ -84,7 +163,17 @@ class DistributedJacobi(JacobiSolver):
         return self.residual_history()
 
     def close(self) -> None:
+        if self._ipc_maps:
+            import torch.distributed as dist
+
+            self.sync()
+            dist.barrier()  # nobody still pushes into memory about to be unmapped/freed
         super().close()
+        for ptr in self._ipc_maps:
+            N.lib().hrt_ipc_close_handle(ctypes.c_void_p(ptr))
+        if self._ipc_maps:
+            dist.barrier()  # every mapping closed before any arena is freed
+        self._ipc_maps = []
         if self.comm:
             N.lib().hrt_nccl_destroy(ctypes.c_void_p(self.comm))
             self.comm = None
