@@ -180,6 +180,9 @@ def run_ours(args):
     rank, world, local = init_process("nccl") if args.gpus > 1 else (0, 1, 0)
     N.require_gpu(local)
     wl = workload(args.workload, world)
+    if args.grid:
+        wl["grid"] = tuple(int(x) for x in args.grid.split(","))
+        wl["desc"] += f" [grid override {args.grid}]"
     iters = args.iters or wl["iters"]
     X, Y, Z = wl["domain"]
     cells = X * Y * Z
@@ -364,6 +367,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--variant", type=int, default=None, help="slab kernel: 0 LDG, 1 TMA")
     ap.add_argument("--rows", type=int, default=None)
+    ap.add_argument("--grid", default=None, help="chunk grid override, e.g. 16,1,1")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per update launch (from profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
