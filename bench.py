@@ -41,7 +41,10 @@ sys.path.insert(0, ROOT)
 METRIC = "Jacobi GLUPS at 1/2/4/8 B200 (% HBM roofline); halo msg GB/s vs size"
 UNIT = "GLUPS"
 BYTES_PER_UPDATE = 16  # read u once, write u' once (float64)
-CFG3_GRIDS = {1: (2, 4, 1), 2: (4, 4, 1), 4: (8, 4, 1), 8: (8, 8, 1)}
+# cfg3: 8 chunks per GPU as x-bands (the reference's rank = lin*ranks//n with
+# x-fastest lin): faces between processes are contiguous rows, pushed by the
+# update kernel straight into the neighbour's ghost row over NVLink (IPC)
+CFG3_GRIDS = {n: (8 * n, 1, 1) for n in (1, 2, 4, 8)}
 
 
 def workload(name: str, n: int):

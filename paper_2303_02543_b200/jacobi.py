@@ -493,7 +493,9 @@ class JacobiSolver:
             # overlap the NCCL exchange with the tiles that do not feed it
             masks = [sum(1 << f for f, nb in self.grid.chunks[lin].neighbors.items()
                          if f < 4 and nb not in self.placement) for lin in mine]
-            if any(masks) and os.environ.get("HRT_SPLIT", "1") != "0":
+            # (measured on 2-4 B200s: no gain — NCCL's kernels find no free SM
+            # slots while the inner tiles run — so opt-in only)
+            if any(masks) and os.environ.get("HRT_SPLIT", "0") != "0":
                 N.call("hrt_jacobi_plan_set_split", self.plans[g],
                        _arr(ctypes.c_int32, masks))
 
