@@ -306,13 +306,52 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(wl, args.cpu_budget)
     else:
         line["cpu_baseline"] = None
+    solver.close()
+    if world == 1 and args.workload == "auto" and not args.no_scaling_baseline:
+        # N>1 lines measure cfg3 (strong scaling); give the same workload at
+        # N=1 so per-N efficiency can be read on one configuration
+        line["scaling_baseline"] = scaling_baseline(args, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    solver.close()
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def scaling_baseline(args, gpu: int):
+    """cfg3 (the N>1 workload) on this one GPU, device-timed, 2 jobs."""
+    import ctypes
+
+    from paper_2303_02543_b200 import _native as N
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    wl = workload("cfg3", 1)
+    s = JacobiSolver(ChunkGrid(wl["domain"], grid=wl["grid"]), gpus=[gpu])
+    s.upload(nonneg=True)
+    f = s._field()
+    st = s.streams[gpu]
+
+    def job():
+        s._chunk_copies(True, 0, f)
+        s.steps_done = 0
+        return s.run_timed(wl["iters"], residual=True)
+
+    job()
+    t0 = st.record()
+    n = 2
+    for _ in range(n):
+        job()
+    t1 = st.record()
+    st.synchronize()
+    ms = ctypes.c_float()
+    N.call("hrt_token_elapsed_ms", ctypes.c_uint64(t0.token_id), ctypes.c_uint64(t1.token_id),
+           ctypes.byref(ms))
+    s.close()
+    X, Y, _ = wl["domain"]
+    return {"workload": wl["desc"], "value": round(X * Y * wl["iters"] * n / (ms.value / 1e3) / 1e9, 2),
+            "unit": UNIT, "note": "the N>1 bench lines run this workload; read scaling "
+                                  "efficiency against this value, not against cfg2's"}
 
 
 def run_reference(args):
@@ -374,6 +413,7 @@ def main():
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per update launch (from profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scaling-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-budget", type=float, default=3.0)
     args = ap.parse_args()
