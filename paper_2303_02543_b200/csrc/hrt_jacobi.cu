@@ -661,10 +661,13 @@ slab_update_tma4_kernel(SlabArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// volume update: general (X,Y,Z) domains; element (i,j,k) at
-// base + origin + i*sx + j*sy + k.  Threads tile (j,k), march i.
-
-constexpr int VOL_TX = 32, VOL_TY = 4;
+// volume update, TMA variant.  Tile: V_CW consumer warps = V_CW y-rows
+// (j0 .. j0+V_CW-1) x 64 z-columns (two per lane), marching planes i along x.
+// Stage q holds plane i0-1+q of the tile plus its y/z halo: V_CW+2 row spans
+// of z = k0-2 .. k0+65, one 1D bulk copy each (rows 16-byte aligned by the
+// layout).  A thread keeps the x window (plane i-1, i, i+1 at its (j,k)) in
+// registers and reads the y/z neighbours of plane i from its stage, which is
+// released once plane i is computed.  Sum order (((((xm+xp)+ym)+yp)+zm)+zp).
 
 struct VolArgs {
     const ChunkBufs* chunks;   // block table, or null: single chunk (du -> dw)
@@ -677,6 +680,153 @@ struct VolArgs {
     int flat;                  // ez == 1 stored with z ghosts: threads tile j only
     unsigned long long* resid;
 };
+
+constexpr int V_CW = 8;
+constexpr int V_ZW = 64;               // z columns per tile
+constexpr int V_ZROW = V_ZW + 4;       // + k0-2, k0-1, k0+64, k0+65
+constexpr int V_ROWS = V_CW + 2;       // y rows per stage (with halo)
+constexpr int V_STAGES = 8;
+
+template <bool RESID>
+__global__ void __launch_bounds__(32 * (V_CW + 1))
+volume_update_tma_kernel(VolArgs a) {
+    __shared__ alignas(128) double ring[V_STAGES][V_ROWS][V_ZROW];
+    __shared__ alignas(8) uint64_t full[V_STAGES], empty[V_STAGES];
+    __shared__ double red[V_CW];
+
+    const int64_t per_chunk = a.tiles_i * a.tiles_j * a.tiles_k;
+    const int64_t t = blockIdx.x;
+    const int64_t c = t / per_chunk;
+    int64_t rem = t - c * per_chunk;
+    const int64_t ti = rem / (a.tiles_j * a.tiles_k);
+    rem -= ti * a.tiles_j * a.tiles_k;
+    const int64_t tj = rem / a.tiles_k;
+    const int64_t tk = rem - tj * a.tiles_k;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    const int64_t k0 = 1 + tk * V_ZW;
+    const int64_t klast = min(k0 + V_ZW - 1, a.ez);
+    const uint32_t bytes = (uint32_t)((((klast - k0 + 4) + 1) & ~int64_t(1)) * 8);
+    const int64_t j0 = 1 + tj * V_CW;
+    // stage rows j0-1 .. j0+V_CW, but never beyond the ghost row ey+1
+    const int64_t nyr64 = a.ey + 2 - (j0 - 1);
+    const int nyr = nyr64 < V_ROWS ? (int)nyr64 : V_ROWS;
+    const int64_t i0 = 1 + ti * a.rows;
+    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+    const int nplanes = (int)(i1 - i0 + 3);
+    const double* __restrict__ u = a.chunks[c].b[a.parity] + a.origin;
+
+    if (tid == 0) {
+        for (int s = 0; s < V_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], V_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == V_CW) {
+        if (lane == 0) {
+            const double* src = u + (i0 - 1) * a.sx + (j0 - 1) * a.sy + (k0 - 2);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int q = 0; q < nplanes; ++q) {
+                if (q >= V_STAGES) mbar_wait(&empty[s], ph ^ 1);
+                mbar_expect_tx(&full[s], bytes * (uint32_t)nyr);
+                for (int r = 0; r < nyr; ++r)
+                    tma_row_load(&ring[s][r][0], src + r * a.sy, bytes, &full[s]);
+                src += a.sx;
+                if (++s == V_STAGES) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        return;
+    }
+
+    const int64_t j = j0 + warp;
+    const int64_t k = k0 + 2 * lane;
+    const bool act = (j <= a.ey) && (k <= a.ez);
+    const bool both = act && (k + 1 <= a.ez);
+    const int r = warp + 1;   // this thread's row in a stage
+    const int p = 2 * lane + 2;
+    double* __restrict__ wr = a.chunks[c].b[a.parity ^ 1] + a.origin + i0 * a.sx + j * a.sy + k;
+    double rmax = 0.0;
+    // stage / phase of the plane being read as "dn" and of the "mid" plane
+    int s = 0, sm = 0;
+    uint32_t ph = 0;
+    auto center = [&](int st) -> double2 {
+        return *reinterpret_cast<const double2*>(&ring[st][r][p]);
+    };
+    auto advance = [&]() {
+        if (++s == V_STAGES) {
+            s = 0;
+            ph ^= 1;
+        }
+    };
+    auto release = [&](int st) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs next TMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    };
+
+    mbar_wait(&full[s], ph);
+    double2 up = center(s);  // plane i0-1: only its centre is needed
+    release(s);
+    advance();
+    mbar_wait(&full[s], ph);
+    double2 mid = center(s);
+    sm = s;
+    advance();
+    for (int q = 2; q < nplanes; ++q) {
+        mbar_wait(&full[s], ph);
+        const double2 dn = center(s);
+        const double2 ym = *reinterpret_cast<const double2*>(&ring[sm][r - 1][p]);
+        const double2 yp = *reinterpret_cast<const double2*>(&ring[sm][r + 1][p]);
+        const double zm = ring[sm][r][p - 1];
+        const double zp = ring[sm][r][p + 2];
+        release(sm);
+        sm = s;
+        advance();
+        if (act) {
+            const double ox = div6(sum6(up.x, dn.x, ym.x, yp.x, zm, mid.y));
+            if (both) {
+                const double oy = div6(sum6(up.y, dn.y, ym.y, yp.y, mid.x, zp));
+                *reinterpret_cast<double2*>(wr) = make_double2(ox, oy);
+                if (RESID)
+                    rmax = fmax(rmax, fmax(fabs(__dsub_rn(ox, mid.x)), fabs(__dsub_rn(oy, mid.y))));
+            } else {
+                wr[0] = ox;
+                if (RESID) rmax = fmax(rmax, fabs(__dsub_rn(ox, mid.x)));
+            }
+        }
+        wr += a.sx;
+        up = mid;
+        mid = dn;
+    }
+
+    if (RESID) {
+        rmax = warp_max(rmax);
+        if (lane == 0) red[warp] = rmax;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * V_CW));
+        if (tid == 0) {
+            double m2 = red[0];
+#pragma unroll
+            for (int q = 1; q < V_CW; ++q) m2 = fmax(m2, red[q]);
+            resid_max(a.resid, m2);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// volume update: general (X,Y,Z) domains; element (i,j,k) at
+// base + origin + i*sx + j*sy + k.  Threads tile (j,k), march i.
+
+constexpr int VOL_TX = 32, VOL_TY = 4;
 
 __global__ void __launch_bounds__(VOL_TX * VOL_TY)
 volume_update_kernel(VolArgs a) {
@@ -1122,9 +1272,20 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.dw = nullptr;
         a.flat = 0;
         a.resid = resid;
+        // TMA ring variant needs 16-byte aligned z rows (origin odd, sy even)
+        const bool tma = p->variant != 0 && (L.origin % 2 == 1) && (L.stride[1] % 2 == 0);
+        if (tma) {
+            a.tiles_j = (a.ey + V_CW - 1) / V_CW;
+            a.tiles_k = (a.ez + V_ZW - 1) / V_ZW;
+        }
         const int64_t grid = (int64_t)p->nchunks * a.tiles_i * a.tiles_j * a.tiles_k;
         if (grid == 0) return HRT_OK;
-        volume_update_kernel<<<(unsigned)grid, dim3(VOL_TX, VOL_TY), 0, s>>>(a);
+        if (tma && resid)
+            volume_update_tma_kernel<true><<<(unsigned)grid, 32 * (V_CW + 1), 0, s>>>(a);
+        else if (tma)
+            volume_update_tma_kernel<false><<<(unsigned)grid, 32 * (V_CW + 1), 0, s>>>(a);
+        else
+            volume_update_kernel<<<(unsigned)grid, dim3(VOL_TX, VOL_TY), 0, s>>>(a);
     }
     HRT_CUDA(cudaGetLastError());
     return HRT_OK;
@@ -1328,7 +1489,7 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
         return cuda_fail(e, "plan tables");
     }
     // rows per CTA: enough CTAs to fill the GPU several times over
-    p->rows = layout->ndim == 2 ? 64 : 16;
+    p->rows = layout->ndim == 2 ? 64 : 32;
     *plan = p;
     return HRT_OK;
 }

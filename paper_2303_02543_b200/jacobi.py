@@ -138,11 +138,13 @@ def chunk_layout(ext, slab: bool) -> N.ChunkLayout:
         L.origin = 15
         L.elems = (ex + 2) * sx
     else:
-        sy = ez + 2
+        # z rows padded like slab rows: ghost z at element 15 so interior
+        # z = 1 is 128-byte aligned; the TMA variant's spans reach z = ez+2
+        sy = -(-(ez + 20) // 16) * 16
         sx = (ey + 2) * sy
         L.ndim = 3
         L.stride[0], L.stride[1], L.stride[2] = sx, sy, 1
-        L.origin = 0
+        L.origin = 15
         L.elems = (ex + 2) * sx
     return L
 

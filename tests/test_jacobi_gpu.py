@@ -153,6 +153,25 @@ def test_arbitrary_initial_data_guarded_division(hrt, oracle, dom, grid):
         assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
 
 
+@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("dom,grid,steps", [((40, 36, 70), (2, 3, 2), 17),
+                                            ((130, 21, 150), (1, 1, 1), 9),
+                                            ((9, 200, 5), (3, 4, 1), 12)])
+def test_volume_kernels_bitwise(hrt, oracle, variant, dom, grid, steps):
+    """3D chunks with partial y (8-row) and z (64-column) tiles: the TMA ring
+    volume kernel (default) and the plain one, field + residual vs oracle."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    s = JacobiSolver(ChunkGrid(dom, grid=grid), variant=variant)
+    s.upload()
+    s.run(steps)
+    got, res = s.download(), s.residual_history()
+    s.close()
+    ref, rref = oracle.jacobi_c(dom, steps, residual=True)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(res, rref)
+
+
 def test_tma_ring_race_regression(hrt):
     """16384^2, 8x8 chunks, 10 steps, repeated: without the async-proxy fence
     between the consumers' shared-memory reads and the producer's next TMA
