@@ -10,9 +10,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-for dom, grid in [((512, 512, 512), (2, 2, 2)), ((1024, 1024, 768), (2, 2, 2)),
-                  ((1024, 1024, 768), (1, 1, 1))]:
-    s = JacobiSolver(ChunkGrid(dom, grid=grid))
+rows_list = [int(r) for r in os.environ.get("ROWS", "0").split(",")]
+cases = [((512, 512, 512), (2, 2, 2)), ((1024, 1024, 768), (2, 2, 2)),
+         ((1024, 1024, 768), (1, 1, 1))]
+if os.environ.get("QUICK"):
+    cases = cases[1:2]
+for (dom, grid), rows in [(c, r) for c in cases for r in rows_list]:
+    print(f"rows={rows or 'default'}", end=" ")
+    s = JacobiSolver(ChunkGrid(dom, grid=grid), rows=rows or None)
     s.upload()
     s.run_timed(3)
     up, ha, tot = s.run_timed(steps)
