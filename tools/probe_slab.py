@@ -26,9 +26,13 @@ for variant, rows in [(v, r) for v in variants for r in rows_list]:
     upd_gbs = 16 * cells * steps / (up / 1e3) / 1e9
     print(f"rows={rows}: total {tot/steps:.3f} ms/step  update {up/steps:.3f} ms  halo {ha/steps:.4f} ms"
           f"  GLUPS {glups:.1f}  update-kernel {upd_gbs:.0f} GB/s", flush=True)
-    t0 = time.perf_counter()
-    s.run(steps, residual=False, graph=True)
-    s.sync()
-    dt = time.perf_counter() - t0
-    print(f"   graph run: {dt/steps*1e3:.3f} ms/step GLUPS {cells*steps/dt/1e9:.1f}", flush=True)
+    for resid, graph in ((False, True), (False, False), (True, False)):
+        s.run(2, residual=resid, graph=graph)
+        s.sync()
+        t0 = time.perf_counter()
+        s.run(steps, residual=resid, graph=graph)
+        s.sync()
+        dt = time.perf_counter() - t0
+        print(f"   run(residual={resid}, graph={graph}): {dt/steps*1e3:.3f} ms/step "
+              f"GLUPS {cells*steps/dt/1e9:.1f}", flush=True)
     s.close()
