@@ -1765,7 +1765,10 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
     if (rc) return rc;
     cudaStream_t s = as_stream(stream)->s;
     unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
-    if (mode == 0 || r != nullptr || p->ipc_on()) {  // IPC step tags are per launch
+    // IPC step tags are per launch; in push mode graph replays measured 40 %
+    // slower than direct launches on B200 (cause not yet identified; the
+    // max-shared carveout did not change it), so push mode launches directly
+    if (mode == 0 || r != nullptr || p->ipc_on() || p->push_on()) {
         for (int64_t k = 0; k < n; ++k) {
             rc = do_step(p, s, first + k, r);
             if (rc) return rc;
