@@ -1,0 +1,140 @@
+"""Host-side logic on CPU (no device calls): chunk decomposition vs the
+reference's rules, HBM layout and face-plane address math, the dependency
+tracker's edges, ping-pong size parsing, report writers and error mapping."""
+
+import json
+
+import numpy as np
+import pytest
+
+from paper_2303_02543_b200 import errors as E
+from paper_2303_02543_b200.jacobi import (FACES, ChunkGrid, _contiguous, chunk_layout, face_plane,
+                                          opposite, remote_faces, remote_ops)
+from paper_2303_02543_b200.objects import AccessMode, HeteroObject
+from paper_2303_02543_b200.pingpong import parse_sizes
+from paper_2303_02543_b200.reporting import BenchReport
+from paper_2303_02543_b200.runtime import DependencyTracker, _DepNode
+
+
+def test_opposite_faces():
+    assert [opposite(f) for f in range(6)] == [1, 0, 3, 2, 5, 4]  # jacobi.py:44-46
+    assert FACES[3] == (1, 1)
+
+
+def test_chunk_grid_matches_oracle_decomposition(oracle):
+    for dom, kw in [((8, 8, 8), dict(ranks=2, devices_per_rank=2, od=2)),
+                    ((48, 40, 1), dict(grid=(6, 5, 1), devices_per_rank=8)),
+                    ((64, 64, 64), dict(grid=(2, 2, 2), ranks=3))]:
+        g = ChunkGrid(dom, **kw)
+        ref = oracle.chunk_layout(dom, **kw)
+        for ch, r in zip(g.chunks, ref):
+            assert ch.lin == r["lin"] and ch.coord == r["coord"] and ch.offsets == r["offsets"]
+            assert ch.rank == r["rank"] and ch.device_local == r["device_local"]
+            assert ch.neighbors == r["neighbors"]
+
+
+def test_chunk_grid_errors():
+    with pytest.raises(E.HrtError, match="not divisible"):
+        ChunkGrid((10, 10, 1), grid=(3, 1, 1))
+    with pytest.raises(E.HrtError):
+        ChunkGrid((0, 10, 1))
+
+
+def _element(L, base, i, j, k):
+    kk = k * L.stride[2] if L.ndim == 3 else 0
+    return (base // 8) + L.origin + i * L.stride[0] + j * L.stride[1] + kk
+
+
+@pytest.mark.parametrize("ext,slab", [((7, 33, 1), True), ((2048, 2048, 1), True),
+                                      ((5, 6, 7), False), ((3, 4, 130), False)])
+def test_layout_alignment_and_planes(ext, slab):
+    L = chunk_layout(ext, slab)
+    ex, ey, ez = ext
+    # interior (1,1[,1]) 16-byte aligned, every row stride even (16-byte rows)
+    assert (L.origin + L.stride[0] + L.stride[1] + (L.stride[2] if not slab else 0)) % 2 == 0
+    assert L.stride[0] % 2 == 0 and (slab or L.stride[1] % 2 == 0)
+    # TMA spans reach element ey+2 (slab) / ez+2 (volume) inside the row
+    fast = ey if slab else ez
+    row = L.stride[0] if slab else L.stride[1]
+    assert L.origin + fast + 2 < row
+    base = 4096
+    for f in range(4 if slab else 6):
+        axis, side = FACES[f]
+        for ghost in (True, False):
+            addr, n0, n1, s0, s1 = face_plane(L, base, f, ghost)
+            idx = (0 if side == 0 else ext[axis] + 1) if ghost else (1 if side == 0 else ext[axis])
+            start = [1, 1, 1]
+            start[axis] = idx
+            if slab:
+                start[2] = 0
+            assert addr // 8 == _element(L, base, *start)
+            others = [a for a in range(2 if slab else 3) if a != axis]
+            assert n1 == ext[others[-1]]
+            assert s1 == L.stride[others[-1]]
+            if not slab:
+                assert n0 == ext[others[0]] and s0 == L.stride[others[0]]
+    # the ghost row of a slab (x face) is contiguous, the ghost column is not
+    if slab:
+        assert _contiguous(*face_plane(L, base, 0, True)[1:])
+        assert not _contiguous(*face_plane(L, base, 2, True)[1:]) or ex == 1
+
+
+def test_remote_faces_x_bands_are_rows():
+    g = ChunkGrid((32768, 32768, 1), ranks=4, grid=(32, 1, 1))
+    for r in range(4):
+        ops = remote_ops(g, r)
+        assert all(FACES[f][0] == 0 for _, _, _, f, _ in ops)  # rows only
+        assert all(n == 32768 for *_, n in ops)
+    assert remote_faces(g, 0) == [(7, 1, 8), (8, 0, 7)]
+
+
+def test_dependency_tracker_edges():
+    """RAW, WAR, WAW per object (runtime.py:167-190)."""
+    t = DependencyTracker()
+    obj = HeteroObject(1, (4,), dtype=np.float64)
+    w1, r1, r2, w2, r3 = (_DepNode(i, True) for i in range(5))
+    assert t.register(w1, obj, AccessMode.WRITE) == set()
+    assert t.register(r1, obj, AccessMode.READ) == {w1}          # RAW
+    assert t.register(r2, obj, AccessMode.READ) == {w1}
+    assert t.register(w2, obj, AccessMode.WRITE) == {w1, r1, r2}  # WAW + WAR
+    r1.done = True
+    assert t.register(r3, obj, AccessMode.READ) == {w2}
+    w2.done = True
+    other = HeteroObject(2, (4,), dtype=np.float64)
+    assert t.register(_DepNode(9, True), other, AccessMode.READ_WRITE) == set()
+
+
+def test_hetero_object_sizes_and_errors():
+    o = HeteroObject(3, (10, 4, 2), dtype=np.float64)
+    assert o.total_size == 640 and o.element_size == 8
+    with pytest.raises(E.HrtError):
+        HeteroObject(4, (0,), dtype=np.uint8)
+    with pytest.raises(E.HrtError):
+        HeteroObject(5, (1, 2, 3, 4), dtype=np.uint8)
+    with pytest.raises(E.HrtError):
+        HeteroObject(6, (3,))
+
+
+def test_parse_sizes():
+    assert parse_sizes("8..64") == [8, 16, 32, 64]          # pingpong.py:35-45
+    assert parse_sizes("8,100,4096") == [8, 100, 4096]
+
+
+def test_bench_report_writers(tmp_path):
+    rep = BenchReport("pingpong", columns=["size_bytes", "iters"])
+    rep.add(size_bytes=8, iters=3, extra="ignored")
+    p = tmp_path / "r.csv"
+    rep.write(str(p))
+    assert p.read_text().splitlines() == ["size_bytes,iters", "8,3"]
+    q = tmp_path / "r.json"
+    rep.write(str(q))
+    assert json.loads(q.read_text())["rows"][0]["size_bytes"] == 8
+    assert rep.csv_text() == "size_bytes,iters\n8,3\n"
+
+
+def test_error_codes_map_to_reference_exceptions():
+    for rc, cls in [(-2, E.OutOfDeviceMemory), (-3, E.DoubleFree), (-4, E.InvalidLocation),
+                    (-5, E.UnknownToken), (-6, E.KernelError), (-1, E.HrtError)]:
+        with pytest.raises(cls):
+            E.raise_for(rc, "x")
+    assert issubclass(E.OutOfDeviceMemory, E.HrtError)
