@@ -223,6 +223,10 @@ int hrt_jacobi_ghost_fill(void *stream, double *base, const hrt_chunk_layout_t *
 /* float(np.sum(a)) bit-exact (jacobi.py:436): numpy pairwise summation on
  * the GPU; synchronises the stream */
 int hrt_np_sum(void *stream, const double *a, int64_t n, double *out);
+/* dst[i] = dst[i]*7 + src[i] + salt (mod 256), src nullable: a
+ * read-modify-write task body for runtime ordering tests (the reference's
+ * writer_body, test_acceptance.py:310-312) */
+int hrt_mix_u8(void *stream, uint8_t *dst, const uint8_t *src, int64_t n, int salt);
 /* self-check of the Markstein division used by the update kernel against
  * IEEE division: n hashed samples (mode 0 uniform [0,6), 1 near 1/2/3/6,
  * 2 random finite bit patterns); synchronises */

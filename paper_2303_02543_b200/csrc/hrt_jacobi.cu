@@ -2041,6 +2041,28 @@ int hrt_np_sum(void* stream, const double* a, int64_t n, double* out) {
     return HRT_OK;
 }
 
+// dst[i] = dst[i]*7 + src[i] + salt (mod 256): a read-modify-write task body
+// for the runtime's randomized serial-equivalence tests (the reference's
+// writer_body, test_acceptance.py:310-312, on device)
+__global__ void mix_u8_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                              int64_t n, int salt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = (uint8_t)(dst[i] * 7u + (src ? src[i] : 0u) + (unsigned)salt);
+}
+
+int hrt_mix_u8(void* stream, uint8_t* dst, const uint8_t* src, int64_t n, int salt) {
+    HRT_CHECK_ARG(stream && dst && n >= 0, "bad mix arguments");
+    if (n == 0) return HRT_OK;
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
+    mix_u8_kernel<<<(unsigned)blocks, 256, 0, st->s>>>(dst, src, n, salt);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
 int hrt_div6_sweep(void* stream, uint64_t seed, int64_t n, int mode, uint64_t* mismatches,
                    double* first_bad) {
     HRT_CHECK_ARG(stream && mismatches, "null argument");

@@ -127,5 +127,22 @@ class Fill(NativeKernel):
                ctypes.c_uint64(v.nbytes))
 
 
+class Mix(NativeKernel):
+    """views [dst] or [src, dst]: dst = dst*7 + src + salt (mod 256)."""
+
+    name = "mix"
+
+    def __init__(self, salt: int = 0):
+        self.salt = int(salt) & 0xFF
+
+    def __call__(self, views, geometry, scratch, stream) -> None:
+        dst = views[-1]
+        src = views[0].ptr if len(views) > 1 else 0
+        if len(views) > 1 and views[0].nbytes < dst.nbytes:
+            raise HrtError("mix: source smaller than destination")
+        N.call("hrt_mix_u8", stream.h, ctypes.c_void_p(dst.ptr), ctypes.c_void_p(src),
+               ctypes.c_int64(dst.nbytes), self.salt)
+
+
 def dtype_of(view) -> np.dtype:
     return np.dtype(getattr(view, "dtype", np.uint8))
