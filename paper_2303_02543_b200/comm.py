@@ -22,14 +22,22 @@ and the three send paths:
   in the frame, H2D upload on the receiver (two staging copies).
 * **inline** (<= 512 B with the 64-byte header, wire.py:137-138): one frame.
 
-The transport is the in-process loopback fabric (transport.py:62-101):
-ranks are in one process and frames are Python objects, so device payloads
-never touch the host on the direct path.
+Two transports.  The in-process loopback fabric (transport.py:62-101):
+ranks share a process and frames are Python objects.  Byte transports
+(:class:`~paper_2303_02543_b200.transport.TcpTransport`, transport.py:
+104-278): frames are the reference's 64-byte headers plus data frames
+(wire.py); a device-aware send puts a :class:`DeviceLocator` (CUDA IPC
+handle of the sender's arena + offset) in the data frame, the receiver
+copies GPU->GPU from the mapped arena and answers with a copy ACK (header
+kind ACK, source device type 1) that completes the sender's read access.
+Either way device payloads never touch the host on the direct path.
 """
 
 from __future__ import annotations
 
 import ctypes
+import os
+import struct
 import time
 from collections import deque
 from dataclasses import dataclass
@@ -41,16 +49,14 @@ from .config import default_recv_cache_bytes
 from .devices import DeviceAllocation, DeviceType, ForeignAllocation, HostRegion, TokenStatus
 from .errors import DeadlockError, HrtError, NotOwner, ProtocolError, TransportClosed
 from .objects import AccessMode, CopyInfo, CopyState, HeteroObject
+from . import _native as N
 from .runtime import AccessOp, Runtime
+from .transport import FT_DATA, FT_HEADER
+from .wire import HEADER_SIZE, DeviceLocator, MessageHeader, MsgKind, decode_header, should_inline
 
-HEADER_SIZE = 64  # wire.py:39
-INLINE_LIMIT = 512  # wire.py:40 (header + payload)
 NONE_INDEX = 0xFFFFFFFFFFFFFFFF
-
-
-def should_inline(payload_size: int) -> bool:
-    """wire.py:137-138"""
-    return HEADER_SIZE + payload_size <= INLINE_LIMIT
+_CORR = struct.Struct("<Q")
+_DEVICE_SRC = 1  # header source_device_type of device-locator frames and their ACKs
 
 
 @dataclass(frozen=True)
@@ -207,6 +213,7 @@ class _Locator:
     host: Optional[np.ndarray]            # host source bytes view
     token: object                         # producer event of the source copy
     on_copied: Callable                   # sender callback(copy_token)
+    ipc: Optional[DeviceLocator] = None   # device source in another process
 
 
 class Comm:
@@ -234,6 +241,11 @@ class Comm:
         self._inflight = 0
         self._pending_gets: dict[int, tuple] = {}
         self._next_corr = 0
+        self._bytes = getattr(transport, "bytes_frames", False)
+        self._pending_in: dict = {}
+        self._await_ack: dict = {}
+        self._ipc_maps: dict = {}
+        self._acks: set = set()
         self._h_exchange = self.register_handler(self._handle_exchange)
 
     # -- registration / world setup ----------------------------------------
@@ -482,6 +494,11 @@ class Comm:
         the copy token (None when nothing needed copying)."""
         reg = self.runtime.registry
         waits = list(wait) + ([loc.token] if loc.token is not None else [])
+        if loc.ipc is not None:  # another process's device memory, mapped over CUDA IPC
+            self.stats.device_copies += 1
+            src = ForeignAllocation(DeviceAllocation(-1, 0, size, ptr=self._ipc_ptr(loc.ipc)),
+                                    loc.ipc.gpu)
+            return reg.enqueue_transfer(src, dst, size, wait=waits)
         if loc.alloc is not None:
             self.stats.device_copies += 1
             src = loc.alloc
@@ -661,13 +678,197 @@ class Comm:
             q = self._outgoing[dst]
             while q and q[0].ready:
                 e = q.popleft()
-                self.transport.send(e.dst, e.frame)
+                if self._bytes:
+                    for ftype, data in self._encode(e.dst, e.frame):
+                        self.transport.send(e.dst, ftype, data)
+                else:
+                    self.transport.send(e.dst, e.frame)
                 work += 1
-        for src, frame in self.transport.poll():
-            self._on_frame(src, frame)
-            work += 1
+        if self._bytes:
+            for src, ftype, data in self.transport.poll():
+                self._decode(src, ftype, data)
+                work += 1
+        else:
+            for src, frame in self.transport.poll():
+                self._on_frame(src, frame)
+                work += 1
         work += self._run_handlers()
         return work
+
+    # -- byte transports: reference headers + data frames -------------------
+
+    def _arena_locator(self, reg, alloc: DeviceAllocation) -> DeviceLocator:
+        dev = reg.device(alloc.device_id)
+        pool = dev.pool
+        handle = getattr(pool, "_ipc_handle", None)
+        if handle is None:
+            buf = ctypes.create_string_buffer(64)
+            N.call("hrt_ipc_get_handle", ctypes.c_void_p(pool.base), buf)
+            handle = pool._ipc_handle = buf.raw
+        return DeviceLocator(handle, alloc.ptr - pool.base, alloc.size, dev.gpu, pool.base,
+                             os.getpid())
+
+    def _ipc_ptr(self, loc: DeviceLocator) -> int:
+        if loc.pid == os.getpid():  # same process: the arena address is ours too
+            return loc.arena_base + loc.offset
+        base = self._ipc_maps.get(loc.ipc_handle)
+        if base is None:
+            p = ctypes.c_void_p()
+            dev_ids = self.runtime.registry.device_ids
+            gpu = self.runtime.registry.gpu_of(dev_ids[0]) if dev_ids else 0
+            N.call("hrt_ipc_open_handle", gpu, ctypes.create_string_buffer(loc.ipc_handle, 64),
+                   ctypes.byref(p))
+            base = self._ipc_maps[loc.ipc_handle] = p.value
+        return base + loc.offset
+
+    def _host_bytes(self, loc: _Locator, size: int) -> bytes:
+        """Payload bytes of a locator (device sources are read back)."""
+        if loc.alloc is not None:
+            if loc.token is not None:
+                loc.token.wait()
+            return np.asarray(loc.registry.region(loc.alloc, size).copy()).tobytes()
+        if loc.host is not None:
+            return np.ascontiguousarray(loc.host).tobytes()[:size]
+        return bytes(size)
+
+    def _frames(self, hdr: MessageHeader, body: bytes):
+        hdr.payload_size = len(body) if hdr.payload_size == 0 else hdr.payload_size
+        if hdr.inline_flag:
+            return [(FT_HEADER, hdr.encode() + body)]
+        return [(FT_HEADER, hdr.encode()), (FT_DATA, _CORR.pack(hdr.correlation_id) + body)]
+
+    def _encode(self, dst: int, frame):
+        kind = frame[0]
+        self._next_corr += 1
+        corr = self._next_corr
+        if kind == "bytes":
+            _, hid, index, data = frame
+            h = MessageHeader(MsgKind.HANDLER, hid, dst, index, len(data), should_inline(len(data)),
+                              corr)
+            return self._frames(h, data)
+        if kind in ("staged", "hetero"):
+            esize, dims, _dtype = frame[3]
+            d3 = tuple(dims) + (0,) * (3 - len(dims))
+            if kind == "staged":
+                data = frame[4]
+                h = MessageHeader(MsgKind.HANDLER_HETERO_META, frame[1], dst, frame[2], len(data),
+                                  should_inline(len(data)), corr, esize, d3)
+                return self._frames(h, data)
+            _, hid, index, meta, size, loc, wait = frame
+            for t in wait:
+                t.wait()
+            if loc.alloc is None:  # host-resident or untouched source: ship bytes
+                data = self._host_bytes(loc, size)
+                loc.on_copied(None)
+                h = MessageHeader(MsgKind.HANDLER_HETERO_META, hid, dst, index, size,
+                                  should_inline(size), corr, esize, d3)
+                return self._frames(h, data)
+            if loc.token is not None:
+                loc.token.wait()  # the receiver copies as soon as the frame arrives
+            dl = self._arena_locator(loc.registry, loc.alloc)
+            dl.size = size
+            self._await_ack[corr] = loc.on_copied
+            h = MessageHeader(MsgKind.HANDLER_HETERO_META, hid, dst, index, size, False, corr,
+                              esize, d3, source_device_type=1)
+            return [(FT_HEADER, h.encode()), (FT_DATA, _CORR.pack(corr) + dl.encode())]
+        if kind == "put":
+            _, hid, oid, size, loc, wait = frame
+            for t in wait:
+                t.wait()
+            data = self._host_bytes(loc, size)
+            loc.on_copied(None)
+            h = MessageHeader(MsgKind.PUT_META, hid, dst, oid, size, should_inline(size), corr)
+            return self._frames(h, data)
+        if kind == "get":
+            _, hid, oid, size, gcorr = frame
+            return [(FT_HEADER, MessageHeader(MsgKind.GET_REQ, hid, dst, oid, size, False,
+                                              gcorr).encode())]
+        if kind == "get_resp":
+            _, hid, gcorr, size, loc, wait = frame
+            for t in wait:
+                t.wait()
+            data = self._host_bytes(loc, size)
+            loc.on_copied(None)
+            h = MessageHeader(MsgKind.PUT_META, hid, dst, NONE_INDEX, size, should_inline(size),
+                              gcorr)
+            return self._frames(h, data)
+        if kind == "ack":  # copy completion of a device-locator message
+            return [(FT_HEADER, MessageHeader(MsgKind.ACK, 0, dst, 0, 0, False, frame[1],
+                                              source_device_type=_DEVICE_SRC).encode())]
+        raise ProtocolError(f"cannot encode frame kind {kind!r}")
+
+    def _decode(self, src: int, ftype: int, data: bytes) -> None:
+        if ftype == FT_HEADER:
+            hdr = decode_header(data)
+            body = data[HEADER_SIZE:HEADER_SIZE + hdr.payload_size] if hdr.inline_flag else None
+            if hdr.msg_kind is MsgKind.ACK:
+                if hdr.source_device_type != _DEVICE_SRC:  # shutdown barrier (comm.py:718)
+                    self._acks.add(src)
+                    return
+                cb = self._await_ack.pop(hdr.correlation_id, None)
+                if cb is None:
+                    raise ProtocolError(f"ACK for unknown message {hdr.correlation_id}")
+                cb(None)
+                return
+            if hdr.msg_kind is MsgKind.GET_REQ:
+                self._on_frame(src, ("get", hdr.handler_id, hdr.target_index, hdr.payload_size,
+                                     hdr.correlation_id))
+                return
+            if body is None:
+                self._pending_in[(src, hdr.correlation_id)] = hdr
+                return
+            self._deliver(src, hdr, body)
+        else:
+            (corr,) = _CORR.unpack_from(data)
+            hdr = self._pending_in.pop((src, corr), None)
+            if hdr is None:
+                raise ProtocolError(f"data frame with unmatched correlation id {corr} from {src}")
+            self._deliver(src, hdr, data[8:])
+
+    def _deliver(self, src: int, hdr: MessageHeader, body: bytes) -> None:
+        k = hdr.msg_kind
+        if k is MsgKind.HANDLER:
+            if len(body) != hdr.payload_size:
+                raise ProtocolError("payload size does not match the header")
+            self._on_frame(src, ("bytes", hdr.handler_id, hdr.target_index, body))
+            return
+        dims = tuple(d for d in hdr.dims if d > 0)
+        if not dims:
+            dims = (max(1, hdr.payload_size // max(1, hdr.element_size)),)
+        meta = (hdr.element_size or 1, dims, None)
+        if k is MsgKind.HANDLER_HETERO_META:
+            if hdr.source_device_type == _DEVICE_SRC:  # device locator: GPU->GPU copy, then ACK
+                dl = DeviceLocator.decode(body)
+                corr = hdr.correlation_id
+
+                def copied(tok, src=src, corr=corr):
+                    if tok is None:
+                        self._queue_ack(src, corr)
+                    else:
+                        self.runtime._watch(tok, lambda t: self._queue_ack(src, corr))
+
+                loc = _Locator(None, None, None, None, copied, ipc=dl)
+                self._on_frame(src, ("hetero", hdr.handler_id, hdr.target_index, meta,
+                                     hdr.payload_size, loc, []))
+            else:
+                self._on_frame(src, ("staged", hdr.handler_id, hdr.target_index, meta, body))
+            return
+        if k is MsgKind.PUT_META:
+            loc = _Locator(None, None, np.frombuffer(body, np.uint8), None, lambda t: None)
+            if hdr.target_index == NONE_INDEX:
+                self._on_frame(src, ("get_resp", hdr.handler_id, hdr.correlation_id,
+                                     hdr.payload_size, loc, []))
+            else:
+                self._on_frame(src, ("put", hdr.handler_id, hdr.target_index, hdr.payload_size,
+                                     loc, []))
+            return
+        raise ProtocolError(f"unexpected message kind {k!r}")
+
+    def _queue_ack(self, dst: int, corr: int) -> None:
+        e = _Outgoing(dst, "ack")
+        e.frame = ("ack", corr)
+        e.ready = True
+        self._queue(e)
 
     def progress(self, advance: bool = True) -> int:
         work = self.runtime.progress(advance=False)
@@ -681,15 +882,37 @@ class Comm:
 
     @property
     def quiescent(self) -> bool:
-        return not self._outgoing_pending() and not self._hq and not self._pending_gets
+        return (not self._outgoing_pending() and not self._hq and not self._pending_gets
+                and not self._await_ack and not self._pending_in)
 
     def flush(self, timeout: float = 60.0) -> None:
         drive([self], until=lambda: not self._outgoing_pending(), timeout=timeout)
 
+    def _send_barrier(self) -> None:
+        self._next_corr += 1
+        hdr = MessageHeader(MsgKind.ACK, 0, self.rank, 0, 0, False, self._next_corr)
+        for r in range(self.world_size):
+            if r != self.rank:
+                self.transport.send(r, FT_HEADER, hdr.encode())
+
+    def _barrier_done(self) -> bool:
+        return self._acks >= set(range(self.world_size)) - {self.rank} and self.transport.flushed()
+
     def shutdown(self, barrier: Optional[bool] = None, timeout: float = 60.0) -> None:
+        """Flush, then close (comm.py:1003-1025).  With ``barrier`` (default
+        for byte transports) every rank first waits for the copy ACKs of its
+        device-locator sends, then sends a barrier ACK to each peer and waits
+        for one from each, so no peer closes while others expect traffic."""
         if self._closed:
             return
         self.flush(timeout)
+        if barrier is None:
+            barrier = self._bytes
+        if barrier and self.world_size > 1:
+            drive([self], until=lambda: not self._await_ack and not self._outgoing_pending(),
+                  timeout=timeout)
+            self._send_barrier()
+            drive([self], until=self._barrier_done, timeout=timeout)
         self._closed = True
         self.transport.close()
 
@@ -700,17 +923,30 @@ def drive(comms: list[Comm], until: Callable[[], bool], timeout: float = 120.0) 
     the oldest outstanding device event of any rank; deadlock only when
     nothing is in flight anywhere."""
     deadline = time.monotonic() + timeout
+    # over sockets, bytes can be in flight in the kernel (or in another
+    # process) with nothing to do here: wait for them until the deadline
+    # (busy-poll for a few ms after the last useful work: a sleep costs the
+    # kernel's timer slack, ~50 us, on every message of a round trip)
+    patient = any(c._bytes for c in comms)
+    busy_since = time.monotonic()
     while not until():
         work = 0
         for c in comms:
             work += c.progress(advance=False)
         if work:
+            busy_since = time.monotonic()
             continue
         for c in comms:
             work += c.runtime.progress(advance=True)
             if work:
                 break
         if work:
+            busy_since = time.monotonic()
+            continue
+        now = time.monotonic()
+        if patient and now <= deadline:
+            if now - busy_since > 5e-3:
+                time.sleep(100e-6)
             continue
         state = "; ".join(
             f"rank {c.rank}: {c.runtime.debug_state()} outgoing="
@@ -732,5 +968,9 @@ def shutdown_all(comms: list[Comm], timeout: float = 60.0) -> None:
     drive(comms, until=lambda: all(c.quiescent for c in comms), timeout=timeout)
     for c in comms:
         c.runtime.synchronize()
+    if any(c._bytes for c in comms) and len(comms) > 1:  # in-process byte world: joint barrier
+        for c in comms:
+            c._send_barrier()
+        drive(comms, until=lambda: all(c._barrier_done() for c in comms), timeout=timeout)
     for c in comms:
         c.shutdown(barrier=False, timeout=timeout)

@@ -61,3 +61,55 @@ def make_loopback_world(cfg: WorldConfig, tracer=None) -> list[Comm]:
 
 
 make_world = make_loopback_world
+
+
+def _free_ports(n: int) -> list:
+    import socket
+
+    socks, ports = [], []
+    for _ in range(n):
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        socks.append(s)
+        ports.append(s.getsockname()[1])
+    for s in socks:
+        s.close()
+    return ports
+
+
+def make_tcp_world(cfg: WorldConfig, tracer=None) -> list[Comm]:
+    """All ranks in this process over localhost TCP (worlds.py:110-123):
+    the byte protocol end to end — reference headers, data frames, and for
+    device-aware sends a CUDA-IPC device locator instead of payload bytes."""
+    from .transport import TcpTransport
+
+    peers = [f"127.0.0.1:{p}" for p in _free_ports(cfg.ranks)]
+    ts = [TcpTransport(r, peers, device_aware=cfg.device_aware) for r in range(cfg.ranks)]
+    while not all([t.establish() for t in ts]):  # every endpoint, every round
+        pass
+    return [Comm(ts[r], build_rank_runtime(cfg, r, DeviceClock(), tracer),
+                 recv_cache_bytes=cfg.recv_cache_bytes) for r in range(cfg.ranks)]
+
+
+def init_from_env(runtime: Runtime, recv_cache_bytes=None) -> Comm:
+    """This process's endpoint from HRT_* variables (comm.py:1053-1082):
+    HRT_TRANSPORT=tcp with HRT_RANK and HRT_PEERS (host:port list) joins a
+    multi-process world; HRT_DEVICE_AWARE=1 selects device locators (CUDA
+    IPC, same node).  Default: a single-rank loopback."""
+    import os
+
+    from .config import env_bool
+    from .errors import HrtError
+    from .transport import TcpTransport
+
+    aware = env_bool("HRT_DEVICE_AWARE")
+    if os.environ.get("HRT_TRANSPORT", "loopback") == "tcp":
+        rank = int(os.environ["HRT_RANK"])
+        peers = [p.strip() for p in os.environ["HRT_PEERS"].split(",") if p.strip()]
+        t = TcpTransport(rank, peers, device_aware=aware)
+        t.establish_blocking()
+        return Comm(t, runtime, recv_cache_bytes=recv_cache_bytes)
+    if int(os.environ.get("HRT_RANKS", "1")) != 1:
+        raise HrtError("multi-rank loopback worlds are built with make_loopback_world")
+    return Comm(LoopbackFabric(1).endpoint(0, device_aware=aware), runtime,
+                recv_cache_bytes=recv_cache_bytes)

@@ -37,6 +37,23 @@ def test_pingpong_byte_identity(path):
         assert rep.meta["staging_copies"] > 0
 
 
+@pytest.mark.parametrize("path", ["direct", "staging"])
+def test_pingpong_over_tcp_world(path):
+    """Same ping-pong through the byte protocol (reference headers over
+    localhost TCP); direct payloads still go GPU->GPU (device locators)."""
+    from paper_2303_02543_b200.pingpong import run_pingpong
+
+    sizes = [8, 448, 449, 4096, 1 << 20]
+    rep = run_pingpong(sizes, iterations=3, path=path, transport="tcp", verify=True)
+    assert [r["size_bytes"] for r in rep.rows] == sizes
+    if path == "direct":
+        # device sources ship as locators; host-resident payloads never occur here
+        assert rep.meta["staging_copies"] == 0
+        assert rep.meta["device_copies"] == 2 * 3 * len(sizes)
+    else:
+        assert rep.meta["staging_copies"] > 0
+
+
 def test_pingpong_payload_sequence_is_the_references():
     """The payload bytes are the reference's (default_rng(99), pingpong.py:107,115)."""
     g = load_golden("pingpong.json")
@@ -46,14 +63,16 @@ def test_pingpong_payload_sequence_is_the_references():
         assert hashlib.sha256(b.tobytes()).hexdigest() == p["sha256"]
 
 
-def test_mp_send_bytes_ordering_and_objects():
+@pytest.mark.parametrize("transport", ["loopback", "tcp"])
+def test_mp_send_bytes_ordering_and_objects(transport):
     from paper_2303_02543_b200.comm import MobileRef, drive, exchange_all, shutdown_all
     from paper_2303_02543_b200.devices import DeviceType
     from paper_2303_02543_b200.native_kernels import Fill
-    from paper_2303_02543_b200.worlds import WorldConfig, make_loopback_world
+    from paper_2303_02543_b200.worlds import WorldConfig, make_loopback_world, make_tcp_world
 
+    make = make_tcp_world if transport == "tcp" else make_loopback_world
     for aware in (True, False):
-        comms = make_loopback_world(WorldConfig(ranks=2, device_aware=aware))
+        comms = make(WorldConfig(ranks=2, device_aware=aware))
         got = []
         hid = [c.register_handler(lambda m, a, ctx: got.append(a)) for c in comms][0]
         for c in comms:
@@ -80,11 +99,13 @@ def test_mp_send_bytes_ordering_and_objects():
         shutdown_all(comms)
 
 
-def test_put_get_roundtrip():
+@pytest.mark.parametrize("transport", ["loopback", "tcp"])
+def test_put_get_roundtrip(transport):
     from paper_2303_02543_b200.comm import GlobalObjectId, drive, exchange_all, shutdown_all
-    from paper_2303_02543_b200.worlds import WorldConfig, make_loopback_world
+    from paper_2303_02543_b200.worlds import WorldConfig, make_loopback_world, make_tcp_world
 
-    comms = make_loopback_world(WorldConfig(ranks=2, device_aware=True))
+    make = make_tcp_world if transport == "tcp" else make_loopback_world
+    comms = make(WorldConfig(ranks=2, device_aware=True))
     for c in comms:
         c.create_mobile_object(b"m")
     exchange_all(comms)

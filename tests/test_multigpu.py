@@ -3,6 +3,7 @@ B200s with chunk faces read over NVLink (peer access), and one process per
 GPU under torchrun with faces exchanged by NCCL send/recv inside
 libhrt_b200 — both bitwise against the oracle."""
 
+import json
 import os
 import subprocess
 import sys
@@ -55,3 +56,19 @@ def test_torchrun_nccl_faces():
            os.path.join(ROOT, "tools", "dist_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert "DIST_CHECK PASS" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
+
+
+def test_two_process_pingpong_over_tcp():
+    """Two processes, TCP byte transport with the reference's headers;
+    direct mode moves payloads GPU->GPU through CUDA IPC device locators
+    (no staging copies on the sender), staged mode through the socket."""
+    env = dict(os.environ, MP_SIZES="8,448,449,65536,4194304", MP_ITERS="3")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541",
+           os.path.join(ROOT, "tools", "mp_pingpong.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert "MP_PINGPONG PASS direct_staging_copies=0" in out.stdout, \
+        out.stdout[-3000:] + out.stderr[-3000:]
+    rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith('{"mode"')]
+    assert sorted({(r["mode"], r["size"]) for r in rows}) == sorted(
+        (m, s) for m in ("direct", "staged") for s in (8, 448, 449, 65536, 4194304))
