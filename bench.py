@@ -235,19 +235,29 @@ def run_ours(args):
     barrier(world)
     value = cells * iters * args.steps / (region_ms / 1e3) / 1e9
 
-    # roofline of the dominant kernel (slab update): per-launch algorithmic
-    # bytes / average launch duration (events around every launch)
-    avg_upd_ms = upd / (args.steps * iters)
-    achieved = BYTES_PER_UPDATE * my_cells / (avg_upd_ms / 1e3) / 1e9
+    # roofline of the dominant kernel: per-launch algorithmic bytes / average
+    # launch duration (CUDA events around every launch on the solver stream).
+    # Persistent mode runs all iterations of a job in one wavefront launch.
+    persistent = bool(getattr(solver, "persistent", False))
+    launches_per_job = 1 if persistent else iters
+    steps_per_launch = iters // launches_per_job
+    avg_upd_ms = upd / (args.steps * launches_per_job)
+    bytes_per_launch = BYTES_PER_UPDATE * my_cells * steps_per_launch
+    achieved = bytes_per_launch / (avg_upd_ms / 1e3) / 1e9
     peak, peak_src = peaks()
+    cw = 2 if grid.ext[1] <= 256 else 4
+    kname = (f"slab_wave_kernel<false,true,{cw}>" if persistent else
+             {None: f"slab_update_tma4_kernel<false,true,{cw},push>",
+              2: f"slab_update_tma4_kernel<false,true,{cw},push>",
+              1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant])
+    if grid.slab is False:
+        kname = "volume_update_tma_kernel<true>"
+    traffic = args.traffic if args.traffic is not None else _recorded_traffic(wl["name"], world)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
-                "traffic": args.traffic if args.traffic is not None else
-                _recorded_traffic(wl["name"], world),
-                "kernel": {None: "slab_update_tma4_kernel<false,true>",
-                           2: "slab_update_tma4_kernel<false,true>",
-                           1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant],
-                "bytes_per_launch": BYTES_PER_UPDATE * my_cells,
+                "traffic": traffic * steps_per_launch if traffic else None,
+                "kernel": kname, "steps_per_launch": steps_per_launch,
+                "bytes_per_launch": bytes_per_launch,
                 "avg_launch_ms": round(avg_upd_ms, 5), "peak_source": peak_src,
                 "update_share_of_step": round(upd / tot, 4) if tot else None,
                 "halo_share_of_step": round(halo / tot, 4) if tot else None}
@@ -297,7 +307,9 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "what": "JacobiSolver.upload(pinned) + run(iters) + download(pinned) + residual"},
-        "gpu_launches": 2 * iters * args.steps,
+        # per job: field_copy_kernel (reset) + halo_copy_kernel (ghost
+        # priming) + the update launches
+        "gpu_launches": (2 + launches_per_job) * args.steps,
         "halo_faces_per_gpu": solver.n_faces, "remote_messages_per_gpu": solver.n_remote,
         "tasks_per_s": round(len(grid.chunks) * iters * args.steps / (region_ms / 1e3), 1),
         "clocks": clk.summary(),
@@ -426,12 +438,15 @@ def main():
 
 
 def _recorded_traffic(workload: str, world: int):
-    """DRAM read+write bytes per update launch from the committed ncu capture
-    of the same workload on one GPU (profiles/traffic.json), else None."""
+    """DRAM read+write bytes per iteration of the dominant kernel from the
+    committed ncu capture of the same workload on one GPU
+    (profiles/traffic.json), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             entry = json.load(fh).get(workload)
-        return entry["bytes_per_launch"] if entry and world == 1 else None
+        if not entry or world != 1:
+            return None
+        return entry["bytes_per_launch"] / entry.get("steps_per_launch", 1)
     except Exception:
         return None
 

@@ -182,6 +182,15 @@ int hrt_jacobi_plan_set_split(void *plan, const int32_t *remote_mask);
 int hrt_jacobi_plan_set_ipc(void *plan, const int32_t *remote_mask, uint64_t *arrived, int n_nbr,
                             const uint64_t *remote_slots, uint64_t timeout_ns);
 int hrt_jacobi_plan_ipc_error(void *plan, int *err);
+/* Persistent dataflow mode for one-plan slab push runs (replaces the
+ * reference's per-step barrier `_try_finish_step`, jacobi.py:241-273, with
+ * per-CTA step counters on the device): nbr4[4*c + f] = plan-local index of
+ * chunk c's neighbour across face f (N,S,W,E; the reference's FACES order,
+ * jacobi.py:41-46) or -1.  NULL disables.  timeout_ns 0 = 10 s per wait. */
+int hrt_jacobi_plan_set_persistent(void *plan, const int32_t *nbr4, uint64_t timeout_ns);
+/* Synchronises; *err = 0 ok, 1 IPC edge wait timed out, 2 persistent
+ * dependency wait timed out (results void). */
+int hrt_jacobi_plan_error(void *plan, int *err);
 int hrt_jacobi_plan_field_copy(void *plan, void *stream, double *field, int64_t FY, int64_t FZ,
                                int parity, int to_chunks);
 /* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,

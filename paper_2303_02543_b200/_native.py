@@ -98,6 +98,8 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_split": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_set_ipc": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_u64]),
     "hrt_jacobi_plan_ipc_error": (c_int, [c_void_p, P(c_int)]),
+    "hrt_jacobi_plan_set_persistent": (c_int, [c_void_p, P(ctypes.c_int32), c_u64]),
+    "hrt_jacobi_plan_error": (c_int, [c_void_p, P(c_int)]),
     "hrt_ipc_get_handle": (c_int, [c_void_p, c_char_p]),
     "hrt_ipc_open_handle": (c_int, [c_int, c_char_p, P(c_void_p)]),
     "hrt_ipc_close_handle": (c_int, [c_void_p]),

@@ -393,9 +393,7 @@ slab_update_tma_kernel(SlabArgs a) {
 // Markstein's correction is exactly IEEE division without the range check.
 
 constexpr int T4_CONSUMER_WARPS = 4;
-constexpr int T4_THREADS = 32 * (T4_CONSUMER_WARPS + 1);
 constexpr int T4_COLS = 128 * T4_CONSUMER_WARPS;  // 4 columns per consumer thread
-constexpr int T4_ROW = T4_COLS + 4;
 constexpr int T4_STAGES = 11;  // 11 x 4128 B ring: within the 48 KB static limit
 
 __device__ __forceinline__ double div6_fast(double s) {
@@ -457,84 +455,48 @@ __device__ void sync_signal_neighbours(const SlabArgs& a) {
     }
 }
 
-template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, bool PUSH = false,
-          int STAGES = T4_STAGES>
-__global__ void __launch_bounds__(32 * (CW + 1))
-slab_update_tma4_kernel(SlabArgs a) {
-    __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
-    __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES];
-    __shared__ double red[CW];
-
-    int64_t c, rb, cb;
-    if (a.tiles) {  // explicit tile subset (split schedule)
-        const int* tt = a.tiles + 3 * (int64_t)blockIdx.x;
-        c = tt[0];
-        rb = tt[1];
-        cb = tt[2];
-    } else {
-        const int64_t per_chunk = a.tiles_r * a.tiles_c;
-        const int64_t t = blockIdx.x;
-        c = t / per_chunk;
-        const int64_t rem = t - c * per_chunk;
-        rb = rem / a.tiles_c;
-        cb = rem - rb * a.tiles_c;
-    }
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-
+// Producer side of the ring for one (chunk c, column block cb) strip, rows
+// i0-1 .. i1+1 of buffer `parity`: one bulk copy per row into stage s.
+template <int CW, int STAGES>
+__device__ __forceinline__ void t4_produce(const SlabArgs& a, double (*ring)[128 * CW + 4],
+                                           uint64_t* full, uint64_t* empty, int& s, uint32_t& ph,
+                                           int64_t c, int64_t cb, int64_t i0, int64_t i1,
+                                           int parity) {
     const int64_t j0 = 1 + cb * (128 * CW);
-    if (j0 > a.ey) return;  // (uniform) no interior columns in this tile
     const int64_t last = min(j0 + (128 * CW) - 1, a.ey);
     const uint32_t bytes = (uint32_t)((((last - j0 + 4) + 1) & ~int64_t(1)) * 8);
-    const int64_t i0 = 1 + rb * a.rows;
-    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
     const int nrows = (int)(i1 - i0 + 3);
     const int64_t sx = a.sx;
-    // cross-process edge tile (IPC push mode): wait until every remote
-    // neighbour finished its edge tiles of the previous step — their pushes
-    // into our ghost planes have landed (RAW) and they no longer read the
-    // ghost planes we are about to push into (WAR).  Inner tiles never wait.
-    const bool xedge = a.arrived != nullptr && (int64_t)blockIdx.x < a.n_edge;
-
-    if (tid == 0) {
-        if (xedge) sync_wait_neighbours(a);
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CW);
+    const double* src = a.chunks[c].b[parity] + a.origin + (i0 - 1) * sx + (j0 - 2);
+    for (int q = 0; q < nrows; ++q) {
+        mbar_wait(&empty[s], ph ^ 1);  // (a fresh barrier passes parity 1 at once)
+        mbar_expect_tx(&full[s], bytes);
+        tma_row_load(&ring[s][0], src, bytes, &full[s]);
+        src += sx;
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    __syncthreads();
+}
 
-    if (warp == CW) {
-        if (lane == 0) {
-            const double* src = a.chunks[c].b[a.parity] + a.origin + (i0 - 1) * sx + (j0 - 2);
-            int s = 0;
-            uint32_t ph = 0;
-            for (int q = 0; q < nrows; ++q) {
-                if (q >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], bytes);
-                tma_row_load(&ring[s][0], src, bytes, &full[s]);
-                src += sx;
-                if (++s == STAGES) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-        return;
-    }
-
+// Consumer side for the same strip: output rows i0 .. i1 into buffer
+// parity^1 (+ the fused halo push), residual folded into rmax.
+template <bool GUARD, bool RESID, int CW, bool PUSH, int STAGES>
+__device__ __forceinline__ void t4_consume(const SlabArgs& a, double (*ring)[128 * CW + 4],
+                                           uint64_t* full, uint64_t* empty, int& s, uint32_t& ph,
+                                           int64_t c, int64_t cb, int64_t i0, int64_t i1,
+                                           int parity, double& rmax) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int64_t j0 = 1 + cb * (128 * CW);
+    const int nrows = (int)(i1 - i0 + 3);
+    const int64_t sx = a.sx;
     const int64_t j = j0 + 4 * tid;
     const int64_t nv64 = a.ey - j + 1;
     const int nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);  // valid columns
     const int p = 4 * tid + 2;
-    double* __restrict__ wr = a.chunks[c].b[a.parity ^ 1] + a.origin + i0 * sx + j;
-    double rmax = 0.0;
-    int s = 0;
-    uint32_t ph = 0;
+    double* __restrict__ wr = a.chunks[c].b[parity ^ 1] + a.origin + i0 * sx + j;
     // push targets of this chunk for the buffer being written (face order
     // north, south, west, east = FACES 0..3); null: domain face
     // (row planes are contiguous in both targets: in-buffer ghost rows and
@@ -545,14 +507,14 @@ slab_update_tma4_kernel(SlabArgs a) {
     int qrow_n = -1, qrow_s = -1, ke = 0;
     if (PUSH) {
         const ChunkPush* cp = a.push + c;
-        const int wp = a.parity ^ 1;
+        const int wp = parity ^ 1;
         pn = cp->ptr[0][wp];
         ps = cp->ptr[1][wp];
         double* pw = cp->ptr[2][wp];
         double* pe = cp->ptr[3][wp];
         sw = cp->stride[2];
         se = cp->stride[3];
-        if (pn && i0 == 1) qrow_n = 2;                 // output row 1 is this tile's first
+        if (pn && i0 == 1) qrow_n = 2;                      // output row 1 is this strip's first
         if (ps && i1 == a.ex) qrow_s = (int)(i1 - i0) + 2;  // output row ex is its last
         pw_on = pw != nullptr && j == 1;
         pe_on = pe != nullptr && nv > 0 && j + nv - 1 == a.ey;
@@ -644,6 +606,64 @@ slab_update_tma4_kernel(SlabArgs a) {
         lx = dl;
         ry = dr;
     }
+}
+
+template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, bool PUSH = false,
+          int STAGES = T4_STAGES>
+__global__ void __launch_bounds__(32 * (CW + 1))
+slab_update_tma4_kernel(SlabArgs a) {
+    __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
+    __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES];
+    __shared__ double red[CW];
+
+    int64_t c, rb, cb;
+    if (a.tiles) {  // explicit tile subset (split schedule)
+        const int* tt = a.tiles + 3 * (int64_t)blockIdx.x;
+        c = tt[0];
+        rb = tt[1];
+        cb = tt[2];
+    } else {
+        const int64_t per_chunk = a.tiles_r * a.tiles_c;
+        const int64_t t = blockIdx.x;
+        c = t / per_chunk;
+        const int64_t rem = t - c * per_chunk;
+        rb = rem / a.tiles_c;
+        cb = rem - rb * a.tiles_c;
+    }
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    const int64_t j0 = 1 + cb * (128 * CW);
+    if (j0 > a.ey) return;  // (uniform) no interior columns in this tile
+    const int64_t i0 = 1 + rb * a.rows;
+    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+    // cross-process edge tile (IPC push mode): wait until every remote
+    // neighbour finished its edge tiles of the previous step — their pushes
+    // into our ghost planes have landed (RAW) and they no longer read the
+    // ghost planes we are about to push into (WAR).  Inner tiles never wait.
+    const bool xedge = a.arrived != nullptr && (int64_t)blockIdx.x < a.n_edge;
+
+    if (tid == 0) {
+        if (xedge) sync_wait_neighbours(a);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    int s = 0;
+    uint32_t ph = 0;
+    if (warp == CW) {
+        if (lane == 0) t4_produce<CW, STAGES>(a, ring, full, empty, s, ph, c, cb, i0, i1, a.parity);
+        return;
+    }
+    double rmax = 0.0;
+    t4_consume<GUARD, RESID, CW, PUSH, STAGES>(a, ring, full, empty, s, ph, c, cb, i0, i1,
+                                               a.parity, rmax);
 
     if (RESID) {
         rmax = warp_max(rmax);
@@ -662,6 +682,171 @@ slab_update_tma4_kernel(SlabArgs a) {
         __threadfence_system();
         asm volatile("bar.sync 2, %0;" ::"n"(32 * CW));
         if (tid == 0) sync_signal_neighbours(a);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent wavefront slab kernel (many steps per launch).  Resident CTAs
+// claim tickets from one global counter; ticket t is tile (t mod T) of step
+// (t div T), tiles as in slab_update_tma4_kernel (chunk, row block, column
+// block).  A tile of step k runs once it and its four stencil neighbours —
+// across chunk faces through the plan's neighbour table, whose halo pushes
+// it receives — have published step k-1 in their per-tile counters: RAW on
+// their new values and pushed ghosts, WAR on the buffer it overwrites.
+// Dynamic claiming balances fast and slow SMs like a normal launch, there is
+// no grid barrier and no per-step launch ramp/tail, and the producer warp
+// prefetches the next tile into the ring while the consumers finish the
+// current one.  Deadlock-free: tickets are claimed in order by co-resident
+// CTAs (cooperative launch), so the oldest unfinished tile's dependencies
+// have all been claimed earlier and finish.  Every dependency spin has a
+// globaltimer timeout that sets *err (the producer then stops waiting but
+// keeps feeding the ring, so the kernel always terminates).
+
+struct WaveArgs {
+    SlabArgs s;
+    const int* nbr;               // [nchunks][4] neighbour chunk (N,S,W,E) or -1
+    unsigned int* done;           // [T] steps completed per tile (absolute)
+    unsigned long long* ticket;   // claim counter, 0 at launch
+    unsigned int base;            // every done[] at launch
+    int nsteps;
+    int parity0;
+    int64_t ntiles;               // T
+    unsigned long long* resid;    // nullable: slots for this launch's steps
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu_u32(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(unsigned int* p, unsigned int v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int WAVE_TQ = 4;  // tile descriptors in flight between producer and consumers
+
+template <bool GUARD, bool RESID, int CW, int STAGES = T4_STAGES>
+__global__ void __launch_bounds__(32 * (CW + 1))
+slab_wave_kernel(WaveArgs wa) {
+    __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
+    __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
+        tq_empty[WAVE_TQ];
+    __shared__ long long tq[WAVE_TQ];
+    const SlabArgs& a = wa.s;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int64_t T = wa.ntiles;
+    const int64_t per_chunk = a.tiles_r * a.tiles_c;
+    const long long total = (long long)T * wa.nsteps;
+
+    if (tid == 0) {
+        for (int k = 0; k < STAGES; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], CW);
+        }
+        for (int k = 0; k < WAVE_TQ; ++k) {
+            mbar_init(&tq_full[k], 1);
+            mbar_init(&tq_empty[k], CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    int s = 0;
+    uint32_t ph = 0;
+    if (warp == CW) {
+        if (lane != 0) return;
+        bool dead = false;
+        int slot = 0;
+        uint32_t tph = 0;
+        for (;;) {
+            const long long t = (long long)atomicAdd(wa.ticket, 1ull);
+            mbar_wait(&tq_empty[slot], tph ^ 1);
+            tq[slot] = t < total ? t : -1;
+            mbar_arrive(&tq_full[slot]);
+            if (++slot == WAVE_TQ) {
+                slot = 0;
+                tph ^= 1;
+            }
+            if (t >= total) break;
+            const int k = (int)(t / T);
+            const int64_t tile = t - (long long)k * T;
+            const int64_t c = tile / per_chunk;
+            const int64_t rem = tile - c * per_chunk;
+            const int64_t rb = rem / a.tiles_c;
+            const int64_t cb = rem - rb * a.tiles_c;
+            if (!dead) {
+                // this tile and its N/S/W/E neighbours must have finished step k-1
+                const int* nb = wa.nbr + 4 * c;
+                const unsigned need = wa.base + (unsigned)k;
+                unsigned long long t0 = 0;
+                auto wait_on = [&](int64_t d) {
+                    if (dead || d < 0) return;
+                    while (ld_acquire_gpu_u32(wa.done + d) < need) {
+                        if (t0 == 0) t0 = globaltimer_ns();
+                        else if (globaltimer_ns() - t0 > a.timeout_ns) {
+                            atomicExch(a.err, 2);
+                            dead = true;
+                            return;
+                        }
+                    }
+                };
+                wait_on(tile);
+                wait_on(rb > 0 ? tile - a.tiles_c
+                        : nb[0] >= 0 ? nb[0] * per_chunk + (a.tiles_r - 1) * a.tiles_c + cb : -1);
+                wait_on(rb < a.tiles_r - 1 ? tile + a.tiles_c
+                        : nb[1] >= 0 ? nb[1] * per_chunk + cb : -1);
+                wait_on(cb > 0 ? tile - 1
+                        : nb[2] >= 0 ? nb[2] * per_chunk + rb * a.tiles_c + (a.tiles_c - 1) : -1);
+                wait_on(cb < a.tiles_c - 1 ? tile + 1
+                        : nb[3] >= 0 ? nb[3] * per_chunk + rb * a.tiles_c : -1);
+                // other CTAs' generic-proxy stores -> our async-proxy reads
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            const int64_t i0 = 1 + rb * a.rows;
+            const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+            t4_produce<CW, STAGES>(a, ring, full, empty, s, ph, c, cb, i0, i1,
+                                   (wa.parity0 + k) & 1);
+        }
+        return;
+    }
+    int slot = 0;
+    uint32_t tph = 0;
+    for (;;) {
+        mbar_wait(&tq_full[slot], tph);
+        const long long t = tq[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tq_empty[slot]);
+        if (++slot == WAVE_TQ) {
+            slot = 0;
+            tph ^= 1;
+        }
+        if (t < 0) break;
+        const int k = (int)(t / T);
+        const int64_t tile = t - (long long)k * T;
+        const int64_t c = tile / per_chunk;
+        const int64_t rem = tile - c * per_chunk;
+        const int64_t rb = rem / a.tiles_c;
+        const int64_t cb = rem - rb * a.tiles_c;
+        const int64_t i0 = 1 + rb * a.rows;
+        const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+        double rmax = 0.0;
+        t4_consume<GUARD, RESID, CW, true, STAGES>(a, ring, full, empty, s, ph, c, cb, i0, i1,
+                                                   (wa.parity0 + k) & 1, rmax);
+        if (RESID && wa.resid) {
+            rmax = warp_max(rmax);
+            if (lane == 0) resid_max(wa.resid + k, rmax);
+        }
+        // our stores -> later async-proxy reads (TMA of any CTA); then one
+        // thread publishes the tile's step once every consumer warp is done
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
+        if (tid == 0) {
+            __threadfence();
+            st_release_gpu_u32(wa.done + tile, wa.base + (unsigned)k + 1u);
+        }
     }
 }
 
@@ -1176,6 +1361,20 @@ struct Plan {
     unsigned long long* graph_resid = nullptr;
     cudaStream_t graph_stream = nullptr;
     std::vector<cudaEvent_t> events;  // run_timed's per-launch events
+    // persistent dataflow mode (single plan, no remote faces): see
+    // slab_wave_kernel
+    bool persist = false;
+    std::vector<int> nbr;          // [nchunks][4] plan-local neighbour chunk or -1
+    int* d_pnbr = nullptr;
+    unsigned int* d_pdone = nullptr;   // per-tile step counters
+    unsigned long long* d_pticket = nullptr;
+    int pgrid = 0;                 // resident CTA slots of the current build (0: not built)
+    int64_t ptiles = 0, pkey = -1;
+    unsigned int pbase = 0;
+    unsigned long long persist_timeout_ns = 10000000000ULL;
+    bool persist_on() const {
+        return persist && push_on() && remote.empty() && !ipc && !nbr.empty();
+    }
 };
 
 static int64_t blocks_for(const hrt_halo_seg_t* segs, int n) {
@@ -1312,6 +1511,14 @@ static void set_carveouts() {
     C4(true, true, 4); C4(true, false, 4); C4(false, true, 4); C4(false, false, 4);
     C4(true, true, 2); C4(true, false, 2); C4(false, true, 2); C4(false, false, 2);
 #undef C4
+    carveout(slab_wave_kernel<true, true, 4>);
+    carveout(slab_wave_kernel<true, false, 4>);
+    carveout(slab_wave_kernel<false, true, 4>);
+    carveout(slab_wave_kernel<false, false, 4>);
+    carveout(slab_wave_kernel<true, true, 2>);
+    carveout(slab_wave_kernel<true, false, 2>);
+    carveout(slab_wave_kernel<false, true, 2>);
+    carveout(slab_wave_kernel<false, false, 2>);
     carveout(slab_update_tma_kernel);
     carveout(volume_update_tma_kernel<true>);
     carveout(volume_update_tma_kernel<false>);
@@ -1413,6 +1620,125 @@ static int build_split(Plan* p) {
                             cudaMemcpyHostToDevice));
     }
     p->split_rows = p->rows;
+    return HRT_OK;
+}
+
+template <int CW>
+static int wave_occupancy(bool guard) {
+    int dev = 0, sms = 0, a = 0, b = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (guard) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave_kernel<true, true, CW>,
+                                                      32 * (CW + 1), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave_kernel<true, false, CW>,
+                                                      32 * (CW + 1), 0);
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave_kernel<false, true, CW>,
+                                                      32 * (CW + 1), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave_kernel<false, false, CW>,
+                                                      32 * (CW + 1), 0);
+    }
+    return std::min(a, b) * sms;
+}
+
+// (Re)build the wavefront tables: per-tile counters and the neighbour table
+static int build_wave(Plan* p, int64_t ntiles) {
+    cudaFree(p->d_pdone);
+    cudaFree(p->d_pnbr);
+    p->d_pdone = nullptr;
+    p->d_pnbr = nullptr;
+    p->pgrid = 0;
+    const bool narrow = p->L.ext[1] <= 256;
+    int G = narrow ? wave_occupancy<2>(!p->nonneg) : wave_occupancy<4>(!p->nonneg);
+    HRT_CUDA(cudaGetLastError());
+    if (G <= 0) {
+        set_error("persistent kernel: no resident CTA slots");
+        return HRT_E_CUDA;
+    }
+    HRT_CUDA(cudaMalloc(&p->d_pdone, sizeof(unsigned int) * std::max<int64_t>(1, ntiles)));
+    HRT_CUDA(cudaMemset(p->d_pdone, 0, sizeof(unsigned int) * std::max<int64_t>(1, ntiles)));
+    HRT_CUDA(cudaMalloc(&p->d_pnbr, sizeof(int) * p->nbr.size()));
+    HRT_CUDA(cudaMemcpy(p->d_pnbr, p->nbr.data(), sizeof(int) * p->nbr.size(),
+                        cudaMemcpyHostToDevice));
+    if (!p->d_pticket) HRT_CUDA(cudaMalloc(&p->d_pticket, sizeof(unsigned long long)));
+    if (!p->d_err) {
+        HRT_CUDA(cudaMalloc(&p->d_err, sizeof(int)));
+        HRT_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+    }
+    p->pbase = 0;
+    p->pgrid = G;
+    p->pkey = ntiles * 4 + (p->nonneg ? 1 : 0);
+    p->ptiles = ntiles;
+    return HRT_OK;
+}
+
+static SlabArgs slab_args(Plan* p, int parity, unsigned long long* resid) {
+    const hrt_chunk_layout_t& L = p->L;
+    SlabArgs a{};
+    a.chunks = p->d_chunks;
+    a.push = p->push_on() ? p->d_push : nullptr;
+    a.parity = parity;
+    a.ex = L.ext[0];
+    a.ey = L.ext[1];
+    a.sx = L.stride[0];
+    a.origin = L.origin;
+    a.rows = p->rows;
+    a.tiles_r = (a.ex + a.rows - 1) / a.rows;
+    a.resid = resid;
+    a.zghost = HRT_BOUNDARY;
+    return a;
+}
+
+// steps [first, first+n) in one persistent wavefront launch
+static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
+                          unsigned long long* resid_base) {
+    if (n <= 0) return HRT_OK;
+    const int parity0 = (int)(first & 1);
+    int rc = prime_ghosts(p, s, parity0);
+    if (rc) return rc;
+    const bool narrow = p->L.ext[1] <= 256;
+    SlabArgs a = slab_args(p, parity0, nullptr);
+    const int cols = narrow ? 256 : T4_COLS;
+    a.tiles_c = (a.ey + cols - 1) / cols;
+    const int64_t T = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
+    if (T == 0) return HRT_OK;
+    if (p->pgrid == 0 || p->ptiles != T || p->pkey != T * 4 + (p->nonneg ? 1 : 0)) {
+        HRT_CUDA(cudaStreamSynchronize(s));  // counters reset: nothing may be in flight
+        rc = build_wave(p, T);
+        if (rc) return rc;
+    }
+    HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
+    WaveArgs wa{};
+    wa.s = a;
+    wa.s.timeout_ns = p->persist_timeout_ns;
+    wa.s.err = p->d_err;
+    wa.nbr = p->d_pnbr;
+    wa.done = p->d_pdone;
+    wa.ticket = p->d_pticket;
+    wa.base = p->pbase;
+    wa.nsteps = (int)n;
+    wa.parity0 = parity0;
+    wa.ntiles = T;
+    wa.resid = resid_base ? resid_base + first : nullptr;
+    const bool guard = !p->nonneg, res = resid_base != nullptr;
+    void* fn;
+    int threads;
+#define WK(G, R, CW) (void*)slab_wave_kernel<G, R, CW>
+    if (narrow) {
+        fn = guard ? (res ? WK(true, true, 2) : WK(true, false, 2))
+                   : (res ? WK(false, true, 2) : WK(false, false, 2));
+        threads = 96;
+    } else {
+        fn = guard ? (res ? WK(true, true, 4) : WK(true, false, 4))
+                   : (res ? WK(false, true, 4) : WK(false, false, 4));
+        threads = 160;
+    }
+#undef WK
+    const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid, T);
+    void* args[] = {&wa};
+    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3((unsigned)threads), args, 0, s));
+    p->pbase += (unsigned)n;
     return HRT_OK;
 }
 
@@ -1704,6 +2030,49 @@ int hrt_jacobi_plan_set_nonneg(void* plan, int nonneg) {
     return HRT_OK;
 }
 
+// Persistent dataflow mode (slab push mode, one plan, no cross-process
+// faces): nbr4 = per chunk (plan order) the plan-local index of its north,
+// south, west, east neighbour or -1.  Runs of steps then execute as one
+// cooperative launch of slab_wave_kernel.  NULL disables.
+int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t timeout_ns) {
+    HRT_CHECK_ARG(plan, "null plan");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    if (!nbr4) {
+        p->persist = false;
+        return HRT_OK;
+    }
+    HRT_CHECK_ARG(p->L.ndim == 2, "persistent mode needs a slab layout");
+    for (int i = 0; i < 4 * p->nchunks; ++i)
+        HRT_CHECK_ARG(nbr4[i] >= -1 && nbr4[i] < p->nchunks, "neighbour index out of range");
+    int coop = 0;
+    HRT_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->gpu));
+    if (!coop) {
+        set_error("persistent mode needs cooperative launch support");
+        return HRT_E_UNSUPPORTED;
+    }
+    HRT_CUDA(cudaDeviceSynchronize());  // no launch of the old build in flight
+    p->nbr.assign(nbr4, nbr4 + 4 * p->nchunks);
+    p->persist = true;
+    p->pgrid = 0;  // rebuilt at the next launch
+    if (timeout_ns) p->persist_timeout_ns = timeout_ns;
+    return HRT_OK;
+}
+
+// Synchronises `plan`'s GPU; *err: 0 ok, 1 an IPC edge tile timed out, 2 a
+// persistent-kernel dependency wait timed out (the result is void).
+int hrt_jacobi_plan_error(void* plan, int* err) {
+    HRT_CHECK_ARG(plan && err, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    *err = 0;
+    if (!p->d_err) return HRT_OK;
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaMemcpy(err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    return HRT_OK;
+}
+
 int hrt_jacobi_plan_set_remote(void* plan, void* comm, const hrt_remote_seg_t* remote,
                                int nremote, const hrt_halo_seg_t* post, int npost) {
     HRT_CHECK_ARG(plan, "null plan");
@@ -1765,6 +2134,7 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
     if (rc) return rc;
     cudaStream_t s = as_stream(stream)->s;
     unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
+    if (p->persist_on()) return launch_persist(p, s, first, n, r);
     // IPC step tags are per launch; in push mode graph replays measured 40 %
     // slower than direct launches on B200 (cause not yet identified; the
     // max-shared carveout did not change it), so push mode launches directly
@@ -1825,6 +2195,25 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
         cudaEvent_t x;
         HRT_CUDA(cudaEventCreate(&x));
         ev.push_back(x);
+    }
+    if (p->persist_on()) {
+        // one launch for all n steps: "update" is the launch, "halo" the
+        // priming pass (only after an upload)
+        HRT_CUDA(cudaEventRecord(ev[0], s));
+        rc = prime_ghosts(p, s, (int)(first & 1));
+        if (rc) return rc;
+        HRT_CUDA(cudaEventRecord(ev[1], s));
+        rc = launch_persist(p, s, first, n, r);
+        if (rc) return rc;
+        HRT_CUDA(cudaEventRecord(ev[2], s));
+        HRT_CUDA(cudaStreamSynchronize(s));
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        if (update_ms) *update_ms = b;
+        if (halo_ms) *halo_ms = a;
+        if (total_ms) *total_ms = n ? a + b : 0.0;
+        return HRT_OK;
     }
     HRT_CUDA(cudaEventRecord(ev[0], s));
     const bool push = p->push_on();
@@ -1891,6 +2280,9 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_remote_slots);
     cudaFree(p->d_edge_done);
     cudaFree(p->d_err);
+    cudaFree(p->d_pnbr);
+    cudaFree(p->d_pdone);
+    cudaFree(p->d_pticket);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);

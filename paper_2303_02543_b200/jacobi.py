@@ -264,7 +264,7 @@ class JacobiSolver:
     def __init__(self, grid: ChunkGrid, gpus: Optional[Sequence[int]] = None,
                  placement: Optional[dict[int, int]] = None, rows: Optional[int] = None,
                  rank: Optional[int] = None, comm=None, variant: Optional[int] = None,
-                 push: Optional[bool] = None):
+                 push: Optional[bool] = None, persistent: Optional[bool] = None):
         N.require_gpu(0)
         if variant is None and os.environ.get("HRT_SLAB_VARIANT"):
             variant = int(os.environ["HRT_SLAB_VARIANT"])
@@ -401,6 +401,14 @@ class JacobiSolver:
             L.ndim == 2 and (variant is None or variant == 2)
         if self.push:
             self._setup_push()
+        # one GPU, no cross-process faces: runs of steps as one persistent
+        # dataflow launch (no per-step launch ramp/tail, no grid barrier)
+        if persistent is None:
+            persistent = os.environ.get("HRT_PERSIST", "1") != "0"
+        self.persistent = bool(persistent) and self.push and len(self.used_gpus) == 1 \
+            and not remote_ops
+        if self.persistent:
+            self._setup_persistent()
         self._init_ghosts()
 
     def _set_nonneg(self, flag: bool) -> None:
@@ -500,6 +508,17 @@ class JacobiSolver:
             if any(masks) and os.environ.get("HRT_SPLIT", "0") != "0":
                 N.call("hrt_jacobi_plan_set_split", self.plans[g],
                        _arr(ctypes.c_int32, masks))
+
+    def _setup_persistent(self) -> None:
+        g = self.used_gpus[0]
+        mine = [lin for lin in self.owned if self.placement[lin] == g]
+        index = {lin: i for i, lin in enumerate(mine)}
+        nbr = []
+        for lin in mine:
+            for f in range(4):
+                nb = self.grid.chunks[lin].neighbors.get(f)
+                nbr.append(index.get(nb, -1) if nb is not None else -1)
+        N.call("hrt_jacobi_plan_set_persistent", self.plans[g], _arr(ctypes.c_int32, nbr), 0)
 
     def _set_offsets(self) -> None:
         for g in self.used_gpus:
@@ -647,6 +666,7 @@ class JacobiSolver:
                steps, ctypes.c_void_p(self.resid[g] if residual else 0), ctypes.byref(up),
                ctypes.byref(ha), ctypes.byref(tot))
         self.steps_done += steps
+        self._check_error()
         return up.value, ha.value, tot.value
 
     def residual_bits(self) -> dict[int, int]:
@@ -671,6 +691,16 @@ class JacobiSolver:
     def sync(self) -> None:
         for st in self.streams.values():
             st.synchronize()
+        self._check_error()
+
+    def _check_error(self) -> None:
+        if self.persistent:
+            err = ctypes.c_int()
+            for plan in self.plans.values():
+                N.call("hrt_jacobi_plan_error", plan, ctypes.byref(err))
+                if err.value:
+                    raise HrtError("persistent step kernel: a dependency wait timed out "
+                                   "(results void)")
 
     def close(self) -> None:
         for p in getattr(self, "plans", {}).values():

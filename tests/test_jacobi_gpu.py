@@ -196,3 +196,58 @@ def test_tma_ring_race_regression(hrt):
             f, r = run((8, 8, 1), variant)
             assert np.array_equal(r, ref_r), (variant, np.nonzero(r != ref_r)[0][:5])
             assert np.array_equal(f, ref_f), variant
+
+
+@pytest.mark.parametrize("dom,grid,steps", [((64, 64, 1), (4, 4, 1), 10),
+                                            ((1000, 1300, 1), (1, 1, 1), 13),
+                                            ((2048, 1536, 1), (2, 3, 1), 37),
+                                            ((512, 2560, 1), (2, 5, 1), 21),
+                                            ((3, 700, 1), (1, 2, 1), 9),
+                                            ((1024, 1024, 1), (32, 32, 1), 25)])
+def test_persistent_dataflow_kernel_bitwise(hrt, oracle, dom, grid, steps):
+    """The persistent dataflow launch (balanced row segments per resident CTA,
+    neighbour step counters instead of per-step launches) against the C
+    oracle and the per-step tile kernel: field + residual bitwise, including
+    runs split over several launches (step counters carry over) and narrow
+    (<= 256 wide) chunks."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    ref, rref = oracle.jacobi_c(dom, steps, residual=True)
+    outs = []
+    for persistent, parts in ((True, [steps]), (True, [steps // 3, steps - steps // 3]),
+                              (False, [steps])):
+        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent)
+        assert s.persistent == persistent
+        s.upload()
+        for n in parts:
+            s.run(n, residual=False)
+        got = s.download()
+        s.close()
+        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent)
+        s.upload()
+        s.run(steps, residual=True)
+        res = s.residual_history()
+        s.sync()
+        s.close()
+        outs.append((got, res))
+    for got, res in outs:
+        assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
+        assert np.array_equal(res, rref)
+
+
+def test_persistent_guarded_division(hrt, oracle):
+    """Signed/tiny/huge initial data through the persistent kernel's guarded
+    instance."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    dom = (96, 600, 1)
+    rng = np.random.default_rng(11)
+    init = rng.standard_normal(dom) * rng.choice([1e-310, 1e-300, 1.0, 1e300], size=dom)
+    s = JacobiSolver(ChunkGrid(dom, grid=(2, 2, 1)), persistent=True)
+    s.upload(init)
+    assert s.nonneg is False and s.persistent
+    s.run(5, residual=False)
+    got = s.download()
+    s.close()
+    ref = oracle.jacobi_reference(dom, 5, initial=init)
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
