@@ -188,6 +188,15 @@ int hrt_jacobi_plan_ipc_error(void *plan, int *err);
  * chunk c's neighbour across face f (N,S,W,E; the reference's FACES order,
  * jacobi.py:41-46) or -1.  NULL disables.  timeout_ns 0 = 10 s per wait. */
 int hrt_jacobi_plan_set_persistent(void *plan, const int32_t *nbr4, uint64_t timeout_ns);
+/* The plan's wavefront tile counters (device address, for CUDA IPC export
+ * to neighbour ranks) and their count. */
+int hrt_jacobi_plan_wave_counters(void *plan, uint64_t *ptr, int64_t *ntiles);
+/* Cross-process wavefront (the reference's halo messages between ranks,
+ * jacobi.py:237 mp_send, as NVLink pushes + per-tile counters): per chunk and
+ * face the peer slot (-1 none) and the neighbour chunk's index in that
+ * peer's plan; peer_done = each peer's counters mapped here. */
+int hrt_jacobi_plan_set_wave_ipc(void *plan, const int32_t *rpeer4, const int32_t *rnbr4,
+                                 const uint64_t *peer_done, int n_peers, uint64_t timeout_ns);
 /* Synchronises; *err = 0 ok, 1 IPC edge wait timed out, 2 persistent
  * dependency wait timed out (results void). */
 int hrt_jacobi_plan_error(void *plan, int *err);

@@ -100,6 +100,9 @@ SIGNATURES = {
     "hrt_jacobi_plan_ipc_error": (c_int, [c_void_p, P(c_int)]),
     "hrt_jacobi_plan_set_persistent": (c_int, [c_void_p, P(ctypes.c_int32), c_u64]),
     "hrt_jacobi_plan_error": (c_int, [c_void_p, P(c_int)]),
+    "hrt_jacobi_plan_wave_counters": (c_int, [c_void_p, P(c_u64), P(c_i64)]),
+    "hrt_jacobi_plan_set_wave_ipc": (c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_int32),
+                                             P(c_u64), c_int, c_u64]),
     "hrt_ipc_get_handle": (c_int, [c_void_p, c_char_p]),
     "hrt_ipc_open_handle": (c_int, [c_int, c_char_p, P(c_void_p)]),
     "hrt_ipc_close_handle": (c_int, [c_void_p]),

@@ -712,6 +712,10 @@ struct WaveArgs {
     int parity0;
     int64_t ntiles;               // T
     unsigned long long* resid;    // nullable: slots for this launch's steps
+    // cross-process faces (CUDA IPC, same tiling on every rank); null: none
+    const int* rnbr;              // [nchunks][4] chunk index in the neighbour rank's plan
+    const int* rpeer;             // [nchunks][4] peer slot or -1
+    unsigned int* const* peer_done;  // [peers] mapped tile counters of each peer
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_gpu_u32(const unsigned int* p) {
@@ -793,15 +797,39 @@ slab_wave_kernel(WaveArgs wa) {
                         }
                     }
                 };
+                // a neighbour rank's tile (IPC-mapped counters, system scope)
+                auto wait_remote = [&](int f, int64_t off) {
+                    if (dead || !wa.rpeer || wa.rpeer[4 * c + f] < 0) return;
+                    const unsigned int* q = wa.peer_done[wa.rpeer[4 * c + f]] +
+                                            (int64_t)wa.rnbr[4 * c + f] * per_chunk + off;
+                    unsigned int v;
+                    for (;;) {
+                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];"
+                                     : "=r"(v) : "l"(q) : "memory");
+                        if (v >= need) break;
+                        if (t0 == 0) t0 = globaltimer_ns();
+                        else if (globaltimer_ns() - t0 > a.timeout_ns) {
+                            atomicExch(a.err, 2);
+                            dead = true;
+                            return;
+                        }
+                    }
+                };
+                const int64_t offN = (a.tiles_r - 1) * a.tiles_c + cb, offS = cb;
+                const int64_t offW = rb * a.tiles_c + (a.tiles_c - 1), offE = rb * a.tiles_c;
                 wait_on(tile);
-                wait_on(rb > 0 ? tile - a.tiles_c
-                        : nb[0] >= 0 ? nb[0] * per_chunk + (a.tiles_r - 1) * a.tiles_c + cb : -1);
-                wait_on(rb < a.tiles_r - 1 ? tile + a.tiles_c
-                        : nb[1] >= 0 ? nb[1] * per_chunk + cb : -1);
-                wait_on(cb > 0 ? tile - 1
-                        : nb[2] >= 0 ? nb[2] * per_chunk + rb * a.tiles_c + (a.tiles_c - 1) : -1);
-                wait_on(cb < a.tiles_c - 1 ? tile + 1
-                        : nb[3] >= 0 ? nb[3] * per_chunk + rb * a.tiles_c : -1);
+                if (rb > 0) wait_on(tile - a.tiles_c);
+                else if (nb[0] >= 0) wait_on(nb[0] * per_chunk + offN);
+                else wait_remote(0, offN);
+                if (rb < a.tiles_r - 1) wait_on(tile + a.tiles_c);
+                else if (nb[1] >= 0) wait_on(nb[1] * per_chunk + offS);
+                else wait_remote(1, offS);
+                if (cb > 0) wait_on(tile - 1);
+                else if (nb[2] >= 0) wait_on(nb[2] * per_chunk + offW);
+                else wait_remote(2, offW);
+                if (cb < a.tiles_c - 1) wait_on(tile + 1);
+                else if (nb[3] >= 0) wait_on(nb[3] * per_chunk + offE);
+                else wait_remote(3, offE);
                 // other CTAs' generic-proxy stores -> our async-proxy reads
                 asm volatile("fence.proxy.async.global;" ::: "memory");
             }
@@ -840,12 +868,25 @@ slab_wave_kernel(WaveArgs wa) {
             if (lane == 0) resid_max(wa.resid + k, rmax);
         }
         // our stores -> later async-proxy reads (TMA of any CTA); then one
-        // thread publishes the tile's step once every consumer warp is done
+        // thread publishes the tile's step once every consumer warp is done.
+        // Tiles on a cross-process face pushed over NVLink into a neighbour
+        // rank's memory: system-scope fence + release for those.
+        const int* rp = wa.rpeer ? wa.rpeer + 4 * c : nullptr;
+        const bool xedge = rp && ((rb == 0 && rp[0] >= 0) || (rb == a.tiles_r - 1 && rp[1] >= 0) ||
+                                  (cb == 0 && rp[2] >= 0) || (cb == a.tiles_c - 1 && rp[3] >= 0));
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (xedge) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
         if (tid == 0) {
-            __threadfence();
-            st_release_gpu_u32(wa.done + tile, wa.base + (unsigned)k + 1u);
+            const unsigned v = wa.base + (unsigned)k + 1u;
+            if (xedge) {
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
+                             : "memory");
+            } else {
+                __threadfence();
+                st_release_gpu_u32(wa.done + tile, v);
+            }
         }
     }
 }
@@ -1371,9 +1412,14 @@ struct Plan {
     int pgrid = 0;                 // resident CTA slots of the current build (0: not built)
     int64_t ptiles = 0, pkey = -1;
     unsigned int pbase = 0;
+    // wavefront across processes: neighbour ranks' tile counters (IPC)
+    bool wave_ipc = false;
+    int* d_rnbr = nullptr;
+    int* d_rpeer = nullptr;
+    unsigned int** d_peer_done = nullptr;
     unsigned long long persist_timeout_ns = 10000000000ULL;
     bool persist_on() const {
-        return persist && push_on() && remote.empty() && !ipc && !nbr.empty();
+        return persist && push_on() && !nbr.empty() && (wave_ipc || (remote.empty() && !ipc));
     }
 };
 
@@ -1644,10 +1690,17 @@ static int wave_occupancy(bool guard) {
 
 // (Re)build the wavefront tables: per-tile counters and the neighbour table
 static int build_wave(Plan* p, int64_t ntiles) {
-    cudaFree(p->d_pdone);
-    cudaFree(p->d_pnbr);
-    p->d_pdone = nullptr;
-    p->d_pnbr = nullptr;
+    // the counters keep their values (all == pbase between launches) unless
+    // the tile count changes; with cross-process waves they are IPC-mapped
+    // by the neighbours and must never move
+    if (p->d_pdone && p->ptiles != ntiles) {
+        if (p->wave_ipc) {
+            set_error("wavefront tiling changed after the counters were shared over IPC");
+            return HRT_E_INVALID;
+        }
+        cudaFree(p->d_pdone);
+        p->d_pdone = nullptr;
+    }
     p->pgrid = 0;
     const bool narrow = p->L.ext[1] <= 256;
     int G = narrow ? wave_occupancy<2>(!p->nonneg) : wave_occupancy<4>(!p->nonneg);
@@ -1656,21 +1709,33 @@ static int build_wave(Plan* p, int64_t ntiles) {
         set_error("persistent kernel: no resident CTA slots");
         return HRT_E_CUDA;
     }
-    HRT_CUDA(cudaMalloc(&p->d_pdone, sizeof(unsigned int) * std::max<int64_t>(1, ntiles)));
-    HRT_CUDA(cudaMemset(p->d_pdone, 0, sizeof(unsigned int) * std::max<int64_t>(1, ntiles)));
-    HRT_CUDA(cudaMalloc(&p->d_pnbr, sizeof(int) * p->nbr.size()));
-    HRT_CUDA(cudaMemcpy(p->d_pnbr, p->nbr.data(), sizeof(int) * p->nbr.size(),
-                        cudaMemcpyHostToDevice));
+    if (!p->d_pdone) {
+        HRT_CUDA(cudaMalloc(&p->d_pdone, sizeof(unsigned int) * std::max<int64_t>(1, ntiles)));
+        HRT_CUDA(cudaMemset(p->d_pdone, 0, sizeof(unsigned int) * std::max<int64_t>(1, ntiles)));
+        p->pbase = 0;
+    }
+    if (!p->d_pnbr) {
+        HRT_CUDA(cudaMalloc(&p->d_pnbr, sizeof(int) * p->nbr.size()));
+        HRT_CUDA(cudaMemcpy(p->d_pnbr, p->nbr.data(), sizeof(int) * p->nbr.size(),
+                            cudaMemcpyHostToDevice));
+    }
     if (!p->d_pticket) HRT_CUDA(cudaMalloc(&p->d_pticket, sizeof(unsigned long long)));
     if (!p->d_err) {
         HRT_CUDA(cudaMalloc(&p->d_err, sizeof(int)));
         HRT_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
     }
-    p->pbase = 0;
     p->pgrid = G;
     p->pkey = ntiles * 4 + (p->nonneg ? 1 : 0);
     p->ptiles = ntiles;
     return HRT_OK;
+}
+
+static int64_t wave_tiles(const Plan* p, int64_t* tiles_c_out = nullptr) {
+    const int64_t ex = p->L.ext[0], ey = p->L.ext[1];
+    const int cols = ey <= 256 ? 256 : T4_COLS;
+    const int64_t tc = (ey + cols - 1) / cols;
+    if (tiles_c_out) *tiles_c_out = tc;
+    return (int64_t)p->nchunks * ((ex + p->rows - 1) / p->rows) * tc;
 }
 
 static SlabArgs slab_args(Plan* p, int parity, unsigned long long* resid) {
@@ -1699,9 +1764,7 @@ static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     if (rc) return rc;
     const bool narrow = p->L.ext[1] <= 256;
     SlabArgs a = slab_args(p, parity0, nullptr);
-    const int cols = narrow ? 256 : T4_COLS;
-    a.tiles_c = (a.ey + cols - 1) / cols;
-    const int64_t T = (int64_t)p->nchunks * a.tiles_r * a.tiles_c;
+    const int64_t T = wave_tiles(p, &a.tiles_c);
     if (T == 0) return HRT_OK;
     if (p->pgrid == 0 || p->ptiles != T || p->pkey != T * 4 + (p->nonneg ? 1 : 0)) {
         HRT_CUDA(cudaStreamSynchronize(s));  // counters reset: nothing may be in flight
@@ -1721,6 +1784,11 @@ static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     wa.parity0 = parity0;
     wa.ntiles = T;
     wa.resid = resid_base ? resid_base + first : nullptr;
+    if (p->wave_ipc) {
+        wa.rnbr = p->d_rnbr;
+        wa.rpeer = p->d_rpeer;
+        wa.peer_done = p->d_peer_done;
+    }
     const bool guard = !p->nonneg, res = resid_base != nullptr;
     void* fn;
     int threads;
@@ -1745,6 +1813,9 @@ static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
 static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
     const int parity = (int)(step & 1);
     unsigned long long* slot = resid_base ? resid_base + step : nullptr;
+    // persistent mode: a single step is a one-step wavefront launch, so the
+    // tile counters (shared with neighbour ranks) stay the only protocol
+    if (p->persist_on()) return launch_persist(p, s, step, 1, resid_base);
     if (p->ipc_on()) {
         // one launch, edge tiles first: they wait for / signal the
         // neighbour processes and push over NVLink; no NCCL in the step
@@ -2054,6 +2125,8 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     }
     HRT_CUDA(cudaDeviceSynchronize());  // no launch of the old build in flight
     p->nbr.assign(nbr4, nbr4 + 4 * p->nchunks);
+    cudaFree(p->d_pnbr);
+    p->d_pnbr = nullptr;
     p->persist = true;
     p->pgrid = 0;  // rebuilt at the next launch
     if (timeout_ns) p->persist_timeout_ns = timeout_ns;
@@ -2070,6 +2143,53 @@ int hrt_jacobi_plan_error(void* plan, int* err) {
     int rc = use_device(p->gpu);
     if (rc) return rc;
     HRT_CUDA(cudaMemcpy(err, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    return HRT_OK;
+}
+
+// The plan's wavefront tile counters (allocated now if needed) for export to
+// neighbour ranks over CUDA IPC; *ntiles = their count.
+int hrt_jacobi_plan_wave_counters(void* plan, uint64_t* ptr, int64_t* ntiles) {
+    HRT_CHECK_ARG(plan && ptr && ntiles, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG(p->persist, "enable persistent mode first");
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    const int64_t T = wave_tiles(p);
+    if (!p->d_pdone || p->ptiles != T) {
+        rc = build_wave(p, T);
+        if (rc) return rc;
+    }
+    *ptr = reinterpret_cast<uint64_t>(p->d_pdone);
+    *ntiles = T;
+    return HRT_OK;
+}
+
+// Cross-process wavefront: for each chunk (plan order) and face, the peer
+// slot (or -1) and the neighbour chunk's index in that peer's plan;
+// peer_done[slot] = the peer's tile counters mapped into this process.
+// Every rank must use the same layout, rows and chunk order per rank.
+int hrt_jacobi_plan_set_wave_ipc(void* plan, const int32_t* rpeer4, const int32_t* rnbr4,
+                                 const uint64_t* peer_done, int n_peers, uint64_t timeout_ns) {
+    HRT_CHECK_ARG(plan && rpeer4 && rnbr4 && peer_done && n_peers > 0, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG(p->persist && p->d_pdone, "export the wave counters first");
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    for (int i = 0; i < 4 * p->nchunks; ++i)
+        HRT_CHECK_ARG(rpeer4[i] >= -1 && rpeer4[i] < n_peers, "peer slot out of range");
+    cudaFree(p->d_rnbr);
+    cudaFree(p->d_rpeer);
+    cudaFree(p->d_peer_done);
+    const size_t n4 = sizeof(int) * 4 * (size_t)std::max(1, p->nchunks);
+    HRT_CUDA(cudaMalloc(&p->d_rnbr, n4));
+    HRT_CUDA(cudaMalloc(&p->d_rpeer, n4));
+    HRT_CUDA(cudaMalloc(&p->d_peer_done, sizeof(void*) * n_peers));
+    HRT_CUDA(cudaMemcpy(p->d_rnbr, rnbr4, sizeof(int) * 4 * p->nchunks, cudaMemcpyHostToDevice));
+    HRT_CUDA(cudaMemcpy(p->d_rpeer, rpeer4, sizeof(int) * 4 * p->nchunks, cudaMemcpyHostToDevice));
+    HRT_CUDA(cudaMemcpy(p->d_peer_done, peer_done, sizeof(void*) * n_peers,
+                        cudaMemcpyHostToDevice));
+    p->wave_ipc = true;
+    if (timeout_ns) p->persist_timeout_ns = timeout_ns;
     return HRT_OK;
 }
 
@@ -2283,6 +2403,9 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_pnbr);
     cudaFree(p->d_pdone);
     cudaFree(p->d_pticket);
+    cudaFree(p->d_rnbr);
+    cudaFree(p->d_rpeer);
+    cudaFree(p->d_peer_done);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);

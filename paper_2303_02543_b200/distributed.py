@@ -150,7 +150,54 @@ class DistributedJacobi(JacobiSolver):
                ctypes.c_void_p(self._flags.base), len(nbr_ranks), _arr(ctypes.c_uint64, slots),
                ctypes.c_uint64(30_000_000_000))
         self.ipc = True
+        if os.environ.get("HRT_PERSIST", "1") != "0":
+            self._setup_wave_ipc(g, mine, nbr_ranks)
         dist.barrier()
+
+    def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list) -> None:
+        """Persistent wavefront across processes: every rank exports its
+        per-tile step counters over CUDA IPC; an edge tile waits on the
+        neighbour rank's adjacent tile counter (system scope) instead of a
+        per-step launch + flag handshake.  Tilings agree on all ranks (same
+        layout and rows), chunk order per rank is ``grid.per_rank``."""
+        import torch.distributed as dist
+
+        plan = self.plans[g]
+        index = {lin: i for i, lin in enumerate(mine)}
+        nbr = [index.get(self.grid.chunks[lin].neighbors.get(f), -1)
+               if self.grid.chunks[lin].neighbors.get(f) is not None else -1
+               for lin in mine for f in range(4)]
+        N.call("hrt_jacobi_plan_set_persistent", plan, _arr(ctypes.c_int32, nbr), 0)
+        ptr, ntiles = ctypes.c_uint64(), ctypes.c_int64()
+        N.call("hrt_jacobi_plan_wave_counters", plan, ctypes.byref(ptr), ctypes.byref(ntiles))
+        h = ctypes.create_string_buffer(64)
+        N.call("hrt_ipc_get_handle", ctypes.c_void_p(ptr.value), h)
+        every = [None] * self.world
+        dist.all_gather_object(every, (h.raw, ntiles.value))
+        if len({t for _, t in every}) != 1:
+            raise HrtError(f"wavefront tilings differ across ranks: {[t for _, t in every]}")
+        peer_ptrs = []
+        for q in nbr_ranks:
+            pq = ctypes.c_void_p()
+            N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(every[q][0], 64),
+                   ctypes.byref(pq))
+            self._ipc_maps.append(pq.value)
+            peer_ptrs.append(pq.value)
+        rpeer, rnbr = [], []
+        for lin in mine:
+            for f in range(4):
+                nb = self.grid.chunks[lin].neighbors.get(f)
+                if nb is None or nb in self.placement:
+                    rpeer.append(-1)
+                    rnbr.append(-1)
+                else:
+                    q = self.rank_of[nb]
+                    rpeer.append(nbr_ranks.index(q))
+                    rnbr.append(list(self.grid.per_rank[q]).index(nb))
+        N.call("hrt_jacobi_plan_set_wave_ipc", plan, _arr(ctypes.c_int32, rpeer),
+               _arr(ctypes.c_int32, rnbr), _arr(ctypes.c_uint64, peer_ptrs), len(peer_ptrs),
+               ctypes.c_uint64(30_000_000_000))
+        self.persistent = True
 
     def check_ipc(self) -> None:
         """Raise if an edge tile timed out waiting for a neighbour rank."""

@@ -24,22 +24,26 @@ for dom, grid, steps in cases:
     cg = ChunkGrid(dom, ranks=world, grid=grid)
     s = DistributedJacobi(cg, rank, world, local)
     boxes = []
-    for job in range(2):  # two jobs: re-priming and monotone step tags
+    for job in range(2):  # two jobs: re-priming and monotone step tags / counters
         s.upload()
-        s.run(steps, residual=True)
+        if job == 0:
+            s.run(steps, residual=True)
+            res = s.global_residual_history()
+        else:  # several launches per job: counters carry across launches
+            for n in (steps // 3, 1, steps - steps // 3 - 1):
+                s.run(n, residual=False)
         boxes.append(s.download())
-        res = s.global_residual_history()
         s.check_ipc()
     box = boxes[0]
     same = np.array_equal(boxes[0], boxes[1])
     lo = s.box_lo
-    ipc = s.ipc
+    ipc = (s.ipc, s.persistent)
     s.close()
     flags = [None] * world
     dist.all_gather_object(flags, (same, ipc))
     if rank == 0:
         print(f"  jobs identical on all ranks: {all(f[0] for f in flags)}; "
-              f"ipc push: {[f[1] for f in flags]}", flush=True)
+              f"(ipc push, wavefront): {[f[1] for f in flags]}", flush=True)
         ok_all &= all(f[0] for f in flags)
     parts = [None] * world
     dist.all_gather_object(parts, (lo, box))
