@@ -166,6 +166,18 @@ int hrt_jacobi_plan_set_offsets(void *plan, const int64_t *offs3);
  * a step is then one update launch (+ the NCCL exchange of pushed staging);
  * the full halo pass runs only when ghosts are stale (after an upload) */
 int hrt_jacobi_plan_set_push(void *plan, const hrt_push_t *table);
+/* Contiguous west/east ghost columns ("side arrays", push mode, even chunk
+ * width): per chunk, the arrays holding its own west and east ghost column
+ * for each buffer parity (element i-1 = row i), or null for a domain face
+ * (constant boundary value).  The halo push and the priming pass then
+ * target these instead of the strided in-buffer ghost columns, and the
+ * update kernel streams only the 16-byte-aligned interior row span.
+ * NULL disables. */
+typedef struct hrt_side {
+    uint64_t w[2];
+    uint64_t e[2];
+} hrt_side_t;
+int hrt_jacobi_plan_set_sides(void *plan, const hrt_side_t *table);
 int hrt_jacobi_plan_invalidate_ghosts(void *plan);
 /* overlap for cross-process faces (push mode): remote_mask[c] bit f = face f
  * of chunk c crosses a process; tiles touching such faces run first, then

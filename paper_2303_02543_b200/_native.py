@@ -40,6 +40,12 @@ class Push(ctypes.Structure):
     _fields_ = [("ptr", (c_u64 * 2) * 4), ("stride", c_i64 * 4)]
 
 
+class Side(ctypes.Structure):
+    """hrt_side_t"""
+
+    _fields_ = [("w", c_u64 * 2), ("e", c_u64 * 2)]
+
+
 class RemoteSeg(ctypes.Structure):
     """hrt_remote_seg_t"""
 
@@ -100,6 +106,7 @@ SIGNATURES = {
     "hrt_jacobi_plan_ipc_error": (c_int, [c_void_p, P(c_int)]),
     "hrt_jacobi_plan_set_persistent": (c_int, [c_void_p, P(ctypes.c_int32), c_u64]),
     "hrt_jacobi_plan_error": (c_int, [c_void_p, P(c_int)]),
+    "hrt_jacobi_plan_set_sides": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_wave_counters": (c_int, [c_void_p, P(c_u64), P(c_i64)]),
     "hrt_jacobi_plan_set_wave_ipc": (c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_int32),
                                              P(c_u64), c_int, c_u64]),

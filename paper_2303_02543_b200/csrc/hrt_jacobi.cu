@@ -23,6 +23,7 @@
 //     check it bitwise against IEEE division on the GPU.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -99,9 +100,18 @@ struct ChunkPush {
 };
 static_assert(sizeof(ChunkPush) == sizeof(hrt_push_t), "ChunkPush layout");
 
+// per chunk: its own contiguous west/east ghost columns per parity (null:
+// domain face, constant boundary value)
+struct ChunkSide {
+    const double* w[2];
+    const double* e[2];
+};
+static_assert(sizeof(ChunkSide) == sizeof(hrt_side_t), "ChunkSide layout");
+
 struct SlabArgs {
     const ChunkBufs* chunks;
     const ChunkPush* push;  // null unless the plan pushes its halo
+    const ChunkSide* sides; // null: ghost columns in-buffer (read via the row span)
     const int* tiles;       // null: all tiles (dense); else (chunk, rb, cb) triples
     // cross-process IPC push sync (null arrived: none).  Tiles [0, n_edge)
     // of the tile list touch remote faces.
@@ -464,18 +474,59 @@ __device__ __forceinline__ void t4_produce(const SlabArgs& a, double (*ring)[128
                                            int parity) {
     const int64_t j0 = 1 + cb * (128 * CW);
     const int64_t last = min(j0 + (128 * CW) - 1, a.ey);
-    const uint32_t bytes = (uint32_t)((((last - j0 + 4) + 1) & ~int64_t(1)) * 8);
     const int nrows = (int)(i1 - i0 + 3);
     const int64_t sx = a.sx;
-    const double* src = a.chunks[c].b[parity] + a.origin + (i0 - 1) * sx + (j0 - 2);
-    for (int q = 0; q < nrows; ++q) {
-        mbar_wait(&empty[s], ph ^ 1);  // (a fresh barrier passes parity 1 at once)
-        mbar_expect_tx(&full[s], bytes);
-        tma_row_load(&ring[s][0], src, bytes, &full[s]);
-        src += sx;
-        if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+    // Side-array mode: at a chunk's west/east face the neighbour value comes
+    // from a contiguous ghost column, so the bulk copy covers only the
+    // 16-byte-aligned interior span (no partial 128-byte lines) and this
+    // thread writes the two neighbour values into the ring slots the span
+    // would have used (positions 1 and last-j0+3; the copy never touches
+    // them because chunk widths are even in this mode).  Loads run AH rows
+    // ahead (ld.global.cg: L2, coherent with the pushing CTAs).
+    const bool wside = a.sides != nullptr && cb == 0;
+    const bool eside = a.sides != nullptr && last == a.ey;
+    const double* sw = wside ? a.sides[c].w[parity] : nullptr;
+    const double* se = eside ? a.sides[c].e[parity] : nullptr;
+    const int64_t lo = wside ? j0 : j0 - 2;
+    const int64_t hi = eside ? last : last + 2;
+    const uint32_t bytes = (uint32_t)((((hi - lo + 1) + 1) & ~int64_t(1)) * 8);
+    const int dst0 = wside ? 2 : 0;
+    const int epos = (int)(last - j0) + 3;
+    const double* src = a.chunks[c].b[parity] + a.origin + (i0 - 1) * sx + lo;
+    // row of ring position q is i0-1+q; side element of row r is [r-1]
+    constexpr int AH = 4;  // rows of look-ahead (~1.5 us at the per-CTA row rate)
+    double wv[AH], ev[AH];
+    const bool sides = wside || eside;
+    if (sides) {
+#pragma unroll
+        for (int u = 0; u < AH; ++u) {
+            const int64_t r = i0 - 1 + u;  // rows outside 1..ex are never used
+            const bool ok = u < nrows && r >= 1 && r <= a.ex;
+            wv[u] = !wside ? 0.0 : (sw && ok ? __ldcg(sw + r - 1) : HRT_BOUNDARY);
+            ev[u] = !eside ? 0.0 : (se && ok ? __ldcg(se + r - 1) : HRT_BOUNDARY);
+        }
+    }
+    for (int qb = 0; qb < nrows; qb += AH) {
+#pragma unroll
+        for (int u = 0; u < AH; ++u) {
+            const int q = qb + u;
+            if (q >= nrows) break;
+            mbar_wait(&empty[s], ph ^ 1);  // (a fresh barrier passes parity 1 at once)
+            if (sides) {
+                if (wside) ring[s][1] = wv[u];
+                if (eside) ring[s][epos] = ev[u];
+                const int64_t r = i0 - 1 + q + AH;  // refill this slot AH rows ahead
+                const bool ok = q + AH < nrows && r >= 1 && r <= a.ex;
+                if (wside) wv[u] = (sw && ok) ? __ldcg(sw + r - 1) : HRT_BOUNDARY;
+                if (eside) ev[u] = (se && ok) ? __ldcg(se + r - 1) : HRT_BOUNDARY;
+            }
+            mbar_expect_tx(&full[s], bytes);
+            tma_row_load(&ring[s][dst0], src, bytes, &full[s]);
+            src += sx;
+            if (++s == STAGES) {
+                s = 0;
+                ph ^= 1;
+            }
         }
     }
 }
@@ -610,7 +661,7 @@ __device__ __forceinline__ void t4_consume(const SlabArgs& a, double (*ring)[128
 
 template <bool GUARD, bool RESID, int CW = T4_CONSUMER_WARPS, bool PUSH = false,
           int STAGES = T4_STAGES>
-__global__ void __launch_bounds__(32 * (CW + 1))
+__global__ void __launch_bounds__(32 * (CW + 1), CW == 2 ? 9 : 1)
 slab_update_tma4_kernel(SlabArgs a) {
     __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES];
@@ -730,7 +781,7 @@ __device__ __forceinline__ void st_release_gpu_u32(unsigned int* p, unsigned int
 constexpr int WAVE_TQ = 4;  // tile descriptors in flight between producer and consumers
 
 template <bool GUARD, bool RESID, int CW, int STAGES = T4_STAGES>
-__global__ void __launch_bounds__(32 * (CW + 1))
+__global__ void __launch_bounds__(32 * (CW + 1), CW == 2 ? 9 : 1)
 slab_wave_kernel(WaveArgs wa) {
     __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
@@ -1365,6 +1416,7 @@ struct Plan {
     hrt_halo_seg_t* d_post = nullptr;
     int64_t* d_offs = nullptr;  // chunk origins in the field (field_copy)
     ChunkPush* d_push = nullptr;  // fused halo push table (slab variant 2)
+    ChunkSide* d_sides = nullptr; // contiguous west/east ghost columns (push mode)
     bool ghosts_ready = false;    // ghost planes of the next buffer are current
     bool push_on() const { return d_push != nullptr && L.ndim == 2 && variant == 2; }
     // split schedule (push mode with remote faces): edge tiles first, the
@@ -1418,6 +1470,10 @@ struct Plan {
     int* d_rpeer = nullptr;
     unsigned int** d_peer_done = nullptr;
     unsigned long long persist_timeout_ns = 10000000000ULL;
+    // chunks at most 256 wide run the 2-consumer-warp instances (no idle
+    // threads); HRT_NARROW=0 forces the 4-warp ones (experiments)
+    bool narrow_ok = true;
+    bool narrow_chunk() const { return narrow_ok && L.ext[1] <= 256; }
     bool persist_on() const {
         return persist && push_on() && !nbr.empty() && (wave_ipc || (remote.empty() && !ipc));
     }
@@ -1446,6 +1502,7 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         SlabArgs a{};
         a.chunks = p->d_chunks;
         a.push = p->push_on() ? p->d_push : nullptr;
+        a.sides = p->push_on() && p->variant == 2 ? p->d_sides : nullptr;
         a.tiles = subset == 1   ? p->d_tiles_edge
                   : subset == 2 ? p->d_tiles_inner
                   : subset == 3 ? p->d_tiles_all
@@ -1469,7 +1526,7 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.tiles_r = (a.ex + a.rows - 1) / a.rows;
         // chunks at most 256 wide (e.g. cfg5's 256^2 blocks) use 2 consumer
         // warps per CTA so no thread is idle
-        const bool narrow = p->variant == 2 && a.ey <= 256;
+        const bool narrow = p->variant == 2 && p->narrow_chunk();
         const int cols = p->variant == 2 ? (narrow ? 256 : T4_COLS) : SLAB_COLS;
         a.tiles_c = (a.ey + cols - 1) / cols;
         a.resid = resid;
@@ -1625,7 +1682,7 @@ static int build_split(Plan* p) {
     const hrt_chunk_layout_t& L = p->L;
     const int64_t ex = L.ext[0], ey = L.ext[1];
     const int64_t tr = (ex + p->rows - 1) / p->rows;
-    const int cols = ey <= 256 ? 256 : T4_COLS;
+    const int cols = p->narrow_chunk() ? 256 : T4_COLS;
     const int64_t tc = (ey + cols - 1) / cols;
     std::vector<int> edge, inner;
     for (int64_t c = 0; c < p->nchunks; ++c) {
@@ -1702,7 +1759,7 @@ static int build_wave(Plan* p, int64_t ntiles) {
         p->d_pdone = nullptr;
     }
     p->pgrid = 0;
-    const bool narrow = p->L.ext[1] <= 256;
+    const bool narrow = p->narrow_chunk();
     int G = narrow ? wave_occupancy<2>(!p->nonneg) : wave_occupancy<4>(!p->nonneg);
     HRT_CUDA(cudaGetLastError());
     if (G <= 0) {
@@ -1732,7 +1789,7 @@ static int build_wave(Plan* p, int64_t ntiles) {
 
 static int64_t wave_tiles(const Plan* p, int64_t* tiles_c_out = nullptr) {
     const int64_t ex = p->L.ext[0], ey = p->L.ext[1];
-    const int cols = ey <= 256 ? 256 : T4_COLS;
+    const int cols = p->narrow_chunk() ? 256 : T4_COLS;
     const int64_t tc = (ey + cols - 1) / cols;
     if (tiles_c_out) *tiles_c_out = tc;
     return (int64_t)p->nchunks * ((ex + p->rows - 1) / p->rows) * tc;
@@ -1743,6 +1800,7 @@ static SlabArgs slab_args(Plan* p, int parity, unsigned long long* resid) {
     SlabArgs a{};
     a.chunks = p->d_chunks;
     a.push = p->push_on() ? p->d_push : nullptr;
+    a.sides = p->push_on() ? p->d_sides : nullptr;
     a.parity = parity;
     a.ex = L.ext[0];
     a.ey = L.ext[1];
@@ -1762,7 +1820,7 @@ static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     const int parity0 = (int)(first & 1);
     int rc = prime_ghosts(p, s, parity0);
     if (rc) return rc;
-    const bool narrow = p->L.ext[1] <= 256;
+    const bool narrow = p->narrow_chunk();
     SlabArgs a = slab_args(p, parity0, nullptr);
     const int64_t T = wave_tiles(p, &a.tiles_c);
     if (T == 0) return HRT_OK;
@@ -1919,6 +1977,7 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     set_carveouts();
     // rows per CTA: enough CTAs to fill the GPU several times over
     p->rows = layout->ndim == 2 ? 64 : 32;
+    if (const char* e = getenv("HRT_NARROW")) p->narrow_ok = e[0] != '0';
     *plan = p;
     return HRT_OK;
 }
@@ -1975,6 +2034,27 @@ int hrt_jacobi_plan_set_push(void* plan, const hrt_push_t* table) {
     if (!table || p->nchunks == 0) return HRT_OK;
     HRT_CUDA(cudaMalloc(&p->d_push, sizeof(ChunkPush) * p->nchunks));
     HRT_CUDA(cudaMemcpy(p->d_push, table, sizeof(ChunkPush) * p->nchunks, cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_sides(void* plan, const hrt_side_t* table) {
+    HRT_CHECK_ARG(plan, "null plan");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    HRT_CHECK_ARG(!table || (p->L.ndim == 2 && p->L.ext[1] % 2 == 0),
+                  "side arrays need a slab layout with an even chunk width");
+    cudaFree(p->d_sides);
+    p->d_sides = nullptr;
+    p->ghosts_ready = false;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    if (!table || p->nchunks == 0) return HRT_OK;
+    HRT_CUDA(cudaMalloc(&p->d_sides, sizeof(ChunkSide) * p->nchunks));
+    HRT_CUDA(cudaMemcpy(p->d_sides, table, sizeof(ChunkSide) * p->nchunks,
+                        cudaMemcpyHostToDevice));
     return HRT_OK;
 }
 
@@ -2394,6 +2474,7 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_post);
     cudaFree(p->d_offs);
     cudaFree(p->d_push);
+    cudaFree(p->d_sides);
     cudaFree(p->d_tiles_edge);
     cudaFree(p->d_tiles_inner);
     cudaFree(p->d_tiles_all);

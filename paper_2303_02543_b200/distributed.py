@@ -137,8 +137,11 @@ class DistributedJacobi(JacobiSolver):
                 if nb is None:
                     continue
                 for p in (0, 1):
-                    buf = self.bufs[nb][p] if nb in self.placement else remote_buf(nb, p)
-                    addr, _, _, _, s1 = face_plane(L, buf, opposite(f), ghost=True)
+                    if nb in self.placement:  # (side array or in-buffer ghost plane)
+                        addr, _, _, _, s1 = self._ghost_target(nb, opposite(f), p)
+                    else:  # rows only across processes
+                        addr, _, _, _, s1 = face_plane(L, remote_buf(nb, p), opposite(f),
+                                                       ghost=True)
                     table[i].ptr[f][p] = addr
                 table[i].stride[f] = s1
                 if nb not in self.placement:

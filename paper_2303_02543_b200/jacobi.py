@@ -298,16 +298,33 @@ class JacobiSolver:
             _, n0, n1, s0, s1 = face_plane(L, 0, f, ghost=True)
             staging += n0 * n1 * F64
         staging = -(-staging // 256) * 256 + 256 * 4 * max(1, grid.ranks)
+        # fused halo push (slab variant 2) and, for even chunk widths,
+        # contiguous west/east ghost columns ("side arrays"): pushes and the
+        # kernel's row streams then never touch partial 128-byte lines
+        self.push = bool(push if push is not None else
+                         os.environ.get("HRT_PUSH", "1") != "0") and \
+            L.ndim == 2 and (variant is None or variant == 2)
+        self.side_mode = self.push and grid.ext[1] % 2 == 0 and \
+            os.environ.get("HRT_SIDES", "1") != "0"
+        side_bytes = -(-(grid.ext[0] + 2) * F64 // 256) * 256
         self.pools: dict[int, DevicePool] = {}
         self.bufs: dict[int, tuple[int, int]] = {}
+        self.sides: dict[int, dict[int, tuple[int, int]]] = {}
         for g in self.used_gpus:
             mine = [lin for lin in owned if placement[lin] == g]
             extra = staging if g == self.used_gpus[0] else 0
-            self.pools[g] = DevicePool(g, 2 * len(mine) * self.buf_bytes + extra + 4096)
+            nside = sum(1 for lin in mine for f in (2, 3) if f in grid.chunks[lin].neighbors) \
+                if self.side_mode else 0
+            self.pools[g] = DevicePool(g, 2 * len(mine) * self.buf_bytes + extra + 4096 +
+                                       2 * nside * side_bytes)
             for lin in mine:
                 b0 = self.pools[g].alloc(self.buf_bytes)[2]
                 b1 = self.pools[g].alloc(self.buf_bytes)[2]
                 self.bufs[lin] = (b0, b1)
+                if self.side_mode:
+                    self.sides[lin] = {f: (self.pools[g].alloc(side_bytes)[2],
+                                           self.pools[g].alloc(side_bytes)[2])
+                                       for f in (2, 3) if f in grid.chunks[lin].neighbors}
         for lin in owned:
             g = placement[lin]
             for nb in grid.chunks[lin].neighbors.values():
@@ -356,7 +373,7 @@ class JacobiSolver:
                     pre[g0].append(_seg([pl[0][0], pl[1][0]], [dst, dst], n0, n1, s0, s1, n1, 1))
                     self._push_remote[(nb, opposite(f))] = dst
                 else:  # unpack into c's ghost plane f
-                    pl = [face_plane(L, self.bufs[c][p], f, ghost=True) for p in (0, 1)]
+                    pl = [self._ghost_target(c, f, p) for p in (0, 1)]
                     _, n0, n1, s0, s1 = pl[0]
                     src = st + off * F64
                     post.append(_seg([src, src], [pl[0][0], pl[1][0]], n0, n1, n1, 1, s0, s1))
@@ -396,9 +413,6 @@ class JacobiSolver:
         self.box_lo = tuple(lo)
         self.box = tuple(h - l for l, h in zip(lo, hi))
         self._set_offsets()
-        self.push = bool(push if push is not None else
-                         os.environ.get("HRT_PUSH", "1") != "0") and \
-            L.ndim == 2 and (variant is None or variant == 2)
         if self.push:
             self._setup_push()
         # one GPU, no cross-process faces: runs of steps as one persistent
@@ -429,6 +443,15 @@ class JacobiSolver:
 
     # -- setup --------------------------------------------------------------
 
+    def _ghost_target(self, lin: int, face: int, p: int):
+        """(address, n0, n1, s0, s1) where chunk ``lin``'s ghost plane
+        ``face`` of parity ``p`` lives: its side array (west/east faces in
+        side mode, element i-1 = row i) or the in-buffer ghost plane."""
+        side = self.sides.get(lin, {}).get(face)
+        if side is not None:
+            return side[p], 1, self.layout.ext[0], 0, 1
+        return face_plane(self.layout, self.bufs[lin][p], face, ghost=True)
+
     def _face_seg(self, lin: int, face: int, nb: int) -> N.HaloSeg:
         """Ghost plane `face` of chunk `lin` <- the neighbour's boundary plane,
         for both buffer parities (jacobi.py:213-217 alternate buffers)."""
@@ -436,7 +459,7 @@ class JacobiSolver:
         src, dst = [], []
         for p in (0, 1):
             s_addr, n0, n1, s0, s1 = face_plane(L, self.bufs[nb][p], opposite(face), ghost=False)
-            d_addr, _, _, d0, d1 = face_plane(L, self.bufs[lin][p], face, ghost=True)
+            d_addr, _, _, d0, d1 = self._ghost_target(lin, face, p)
             src.append(s_addr)
             dst.append(d_addr)
         return _seg(src, dst, n0, n1, s0, s1, d0, d1)
@@ -491,8 +514,7 @@ class JacobiSolver:
                         continue
                     if nb in self.placement:
                         for p in (0, 1):
-                            addr, _, _, _, s1 = face_plane(L, self.bufs[nb][p], opposite(f),
-                                                           ghost=True)
+                            addr, _, _, _, s1 = self._ghost_target(nb, opposite(f), p)
                             table[i].ptr[f][p] = addr
                         table[i].stride[f] = s1
                     else:
@@ -500,6 +522,14 @@ class JacobiSolver:
                         table[i].ptr[f][0] = table[i].ptr[f][1] = slot
                         table[i].stride[f] = 1
             N.call("hrt_jacobi_plan_set_push", self.plans[g], ctypes.byref(table))
+            if self.side_mode:
+                sides = (N.Side * max(len(mine), 1))()
+                for i, lin in enumerate(mine):
+                    for f, fld in ((2, "w"), (3, "e")):
+                        pair = self.sides[lin].get(f)
+                        if pair:
+                            getattr(sides[i], fld)[0], getattr(sides[i], fld)[1] = pair
+                N.call("hrt_jacobi_plan_set_sides", self.plans[g], ctypes.byref(sides))
             # overlap the NCCL exchange with the tiles that do not feed it
             masks = [sum(1 << f for f, nb in self.grid.chunks[lin].neighbors.items()
                          if f < 4 and nb not in self.placement) for lin in mine]
