@@ -220,6 +220,15 @@ class DistributedJacobi(JacobiSolver):
                    ctypes.c_void_p(self.resid[g]), n)
         return self.residual_history()
 
+    def allreduce_residual(self) -> None:
+        """Enqueue the cross-rank max of this run's residual history on the
+        solver stream (no host sync; run_jobs' ``after_run`` hook)."""
+        n = self._resid_steps
+        g = self.used_gpus[0]
+        if self.world > 1 and n:
+            N.call("hrt_nccl_allreduce_max_u64", ctypes.c_void_p(self.comm), self.streams[g].h,
+                   ctypes.c_void_p(self.resid[g]), n)
+
     def close(self) -> None:
         if self._ipc_maps:
             import torch.distributed as dist

@@ -699,6 +699,98 @@ class JacobiSolver:
         self._check_error()
         return up.value, ha.value, tot.value
 
+    def run_jobs(self, host_ins: Sequence[PinnedBuffer], host_outs: Sequence[PinnedBuffer],
+                 steps: int, residual: bool = True, nonneg: Optional[bool] = None,
+                 after_run=None, start=None) -> list:
+        """A stream of independent jobs, each ``upload(host_in) -> run(steps)
+        -> download(host_out) + residual history`` (the reference's
+        ``run_jacobi3d`` once per input), pipelined: the next job's H2D and
+        the previous job's D2H run on their own copy streams while this
+        job's steps run, with double-buffered device staging fields.  Every
+        job's bytes still cross PCIe; only the waiting overlaps.  Returns the
+        per-job residual histories (float64 arrays; empty if not residual).
+        ``after_run(solver)`` (optional) runs on the compute stream right
+        after each job's steps (e.g. a cross-rank residual all-reduce).
+        ``start`` (a token) delays the first copy; ``self.jobs_done_token``
+        is recorded after the last D2H (device timing of the whole stream)."""
+        if len(self.used_gpus) != 1:
+            raise HrtError("run_jobs drives one GPU per process")
+        if len(host_ins) != len(host_outs):
+            raise HrtError("one output buffer per input")
+        g = self.used_gpus[0]
+        comp = self.streams[g]
+        nbytes = self.field_elems * F64
+        for b in list(host_ins) + list(host_outs):
+            if b.nbytes < nbytes:
+                raise HrtError(f"host buffer of {b.nbytes} B < field {nbytes} B")
+        if not hasattr(self, "_pipe"):
+            pool = DevicePool(g, 4 * (-(-nbytes // 256) * 256) + 4096)
+            fields = [pool.alloc(max(nbytes, 256))[2] for _ in range(4)]
+            rpool = DevicePool(g, 2 * (-(-max(steps, 1) * 8 // 256) * 256) + 512)
+            self._pipe = {"pool": pool, "in": fields[:2], "out": fields[2:], "rpool": rpool,
+                          "rsteps": max(steps, 1),
+                          "resid": [rpool.alloc(max(steps, 1) * 8)[2] for _ in range(2)],
+                          "h2d": Stream(g, name="jacobi-h2d"), "d2h": Stream(g, name="jacobi-d2h")}
+        pp = self._pipe
+        if steps > pp["rsteps"]:
+            raise HrtError("run_jobs: steps grew since the first call; use a new solver")
+        h2d, d2h = pp["h2d"], pp["d2h"]
+        if nonneg is not None:
+            self._set_nonneg(bool(nonneg))
+        n = len(host_ins)
+        in_free = [None, None]     # scatter of the job that last used the input field
+        out_free = [None, None]    # D2H of the job that last used the output field
+        hists = [np.zeros(steps, dtype=np.uint64) for _ in range(n)]
+        resid_free = [None, None]
+
+        def issue_h2d(j: int):
+            h2d.wait(in_free[j % 2]) if in_free[j % 2] else None
+            N.call("hrt_copy_async", h2d.h, ctypes.c_void_p(pp["in"][j % 2]),
+                   ctypes.c_void_p(host_ins[j].ptr), nbytes)
+            return h2d.record()
+
+        ready = [None] * n
+        if start is not None:
+            h2d.wait(start)
+        if n:
+            ready[0] = issue_h2d(0)
+        for j in range(n):
+            comp.wait(ready[j])
+            self._chunk_copies(True, 0, pp["in"][j % 2])
+            in_free[j % 2] = comp.record()
+            if j + 1 < n:
+                ready[j + 1] = issue_h2d(j + 1)
+            # residual slots of this job (double-buffered against the D2H)
+            if resid_free[j % 2]:
+                comp.wait(resid_free[j % 2])
+            rptr = pp["resid"][j % 2]
+            if residual:
+                N.call("hrt_memset_async", comp.h, ctypes.c_void_p(rptr), 0, steps * 8)
+            self.resid = {g: rptr} if residual else {}
+            self._resid_steps = steps if residual else 0
+            self.steps_done = 0
+            N.call("hrt_jacobi_plan_run", self.plans[g], comp.h, 0, steps,
+                   ctypes.c_void_p(rptr if residual else 0), 0)
+            self.steps_done = steps
+            if after_run is not None:
+                after_run(self)
+            if out_free[j % 2]:
+                comp.wait(out_free[j % 2])
+            self._chunk_copies(False, steps % 2, pp["out"][j % 2])
+            done = comp.record()
+            d2h.wait(done)
+            N.call("hrt_copy_async", d2h.h, ctypes.c_void_p(host_outs[j].ptr),
+                   ctypes.c_void_p(pp["out"][j % 2]), nbytes)
+            if residual:
+                N.call("hrt_copy_async", d2h.h, ctypes.c_void_p(hists[j].ctypes.data),
+                       ctypes.c_void_p(rptr), steps * 8)
+            out_free[j % 2] = resid_free[j % 2] = d2h.record()
+        self.jobs_done_token = d2h.record()
+        d2h.synchronize()
+        comp.synchronize()
+        self._check_error()
+        return [h.view(np.float64) if residual else np.zeros(0) for h in hists]
+
     def residual_bits(self) -> dict[int, int]:
         """device address of each GPU's residual history (uint64 bit patterns)."""
         return dict(self.resid)
