@@ -5,13 +5,16 @@
 ``(BenchReport, checksum, assembled)`` (jacobi.py:281-298).  Two engines:
 
 * ``engine="native"`` (default): every chunk lives in HBM as two ghosted
-  float64 buffers (jacobi.py:382-395); one step is one halo launch (all faces
-  of all chunks on a GPU: neighbour boundary plane read in place, ghost plane
-  written — the reference's pack -> mp_send -> unpack, jacobi.py:219-260,
-  fused into a plane copy) and one update launch over every chunk
-  (_update_body, jacobi.py:70-86), replayed as a CUDA graph.  Chunks on other
-  GPUs of the process are read over NVLink (peer access); chunks of other
-  processes are exchanged with NCCL send/recv (:class:`DistributedJacobi`).
+  float64 buffers (jacobi.py:382-395).  Slabs: the update kernel pushes each
+  chunk's new boundary rows/columns straight into its neighbours' ghost
+  planes (the reference's pack -> mp_send -> unpack, jacobi.py:219-260, as
+  extra stores; west/east ghost columns live in contiguous side arrays), and
+  a run of n steps is ONE persistent wavefront launch (per-tile step
+  counters instead of the per-step barrier _try_finish_step, jacobi.py:
+  241-273).  Chunks of other processes: rows pushed over NVLink into
+  CUDA-IPC-mapped ghost planes with cross-process tile counters
+  (:class:`DistributedJacobi`), or NCCL send/recv for column faces.  3D
+  chunks: one halo launch + one update launch per step.
 * ``engine="tasks"``: the reference's task protocol itself — halo objects,
   pack/unpack/update tasks, ``mp_send`` — executed by the B200 runtime
   (:mod:`.runtime`, :mod:`.comm`); see :mod:`.jacobi_tasks`.
