@@ -69,6 +69,13 @@ def workload(name: str, n: int):
                          f"chains (each block-step needs its neighbours' previous step), 100 "
                          f"iterations on {n} B200",
                     domain=(65536, 65536, 1), grid=(256, 256, 1), iters=100)
+    if name == "paper3d":
+        # the paper's Jacobi3D size, x-bands of 8 chunks per GPU
+        grid = (8 * n, 1, 1)
+        return dict(name="paper3d",
+                    desc=f"Jacobi 3D 1024x1024x768 float64 (7-point), 8 chunks per GPU "
+                         f"(grid {grid[0]}x1x1), 100 iterations on {n} B200",
+                    domain=(1024, 1024, 768), grid=grid, iters=100)
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -140,7 +147,15 @@ def cpu_baseline(wl, budget_s: float = 15.0):
     from oracle import oracle as O
 
     O.build()
-    X, Y, _ = wl["domain"]
+    X, Y, Z = wl["domain"]
+    if Z != 1:  # 3D: the C oracle on the full volume, 2 sweeps
+        t0 = time.perf_counter()
+        O.jacobi_c(wl["domain"], 2)
+        dt = time.perf_counter() - t0
+        return {"value": round(X * Y * Z * 2 / dt / 1e9, 4), "unit": UNIT,
+                "cores": O.cpu_threads(), "kind": "port",
+                "sample": f"{X}x{Y}x{Z} volume, 2 of the {wl['iters']} sweeps incl. allocation "
+                          f"({dt:.1f} s), oracle/jacobi_oracle.c OpenMP, host of the GPU box"}
     slab = O.CpuSlab(X, Y)
     t0 = time.perf_counter()
     slab.sweep(1)
@@ -270,13 +285,14 @@ def run_ours(args):
     e2e_value = e2e_serial = None
     if args.e2e_steps > 0:
         K = args.e2e_steps
-        host_in = [PinnedBuffer(nbytes) for _ in range(2)]
-        for h in host_in:
-            h.array(dtype="float64")[:] = 0.0          # the reference's initial interior
-        host_out = [PinnedBuffer(nbytes) for _ in range(2)]
+        # every job reads the same pinned input (the reference's initial
+        # state) and writes one pinned output buffer (D2Hs are in order)
+        host_in = [PinnedBuffer(nbytes)]
+        host_in[0].array(dtype="float64")[:] = 0.0      # the reference's initial interior
+        host_out = [PinnedBuffer(nbytes)]
         hook = (lambda s: s.allreduce_residual()) if world > 1 else None
-        ins = [host_in[k % 2] for k in range(K)]
-        outs = [host_out[k % 2] for k in range(K)]
+        ins = [host_in[0]] * K
+        outs = [host_out[0]] * K
         solver.run_jobs(ins[:1], outs[:1], iters, residual=True, nonneg=True, after_run=hook)
         barrier(world)
         st.synchronize()
@@ -439,7 +455,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="auto", choices=["auto", "cfg1", "cfg2", "cfg3", "cfg5"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "cfg1", "cfg2", "cfg3", "cfg5", "paper3d"])
     ap.add_argument("--iters", type=int, default=0, help="override iterations per job")
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="jobs in the e2e stream (default: --steps)")

@@ -178,6 +178,15 @@ typedef struct hrt_side {
     uint64_t e[2];
 } hrt_side_t;
 int hrt_jacobi_plan_set_sides(void *plan, const hrt_side_t *table);
+/* Fused halo push for volume (3D) plans: per chunk, face f (-x,+x,-y,+y,
+ * -z,+z) and parity of the buffer being written, the address matching this
+ * chunk's element offset 0 in the neighbour's ghost plane (the kernel stores
+ * boundary cell (i,j,k) at ptr[f][p] + 8*(i*sx + j*sy + k)); 0 for a domain
+ * face.  NULL disables. */
+typedef struct hrt_vpush {
+    uint64_t ptr[6][2];
+} hrt_vpush_t;
+int hrt_jacobi_plan_set_vpush(void *plan, const hrt_vpush_t *table);
 int hrt_jacobi_plan_invalidate_ghosts(void *plan);
 /* overlap for cross-process faces (push mode): remote_mask[c] bit f = face f
  * of chunk c crosses a process; tiles touching such faces run first, then

@@ -46,6 +46,12 @@ class Side(ctypes.Structure):
     _fields_ = [("w", c_u64 * 2), ("e", c_u64 * 2)]
 
 
+class VPush(ctypes.Structure):
+    """hrt_vpush_t"""
+
+    _fields_ = [("ptr", (c_u64 * 2) * 6)]
+
+
 class RemoteSeg(ctypes.Structure):
     """hrt_remote_seg_t"""
 
@@ -107,6 +113,7 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_persistent": (c_int, [c_void_p, P(ctypes.c_int32), c_u64]),
     "hrt_jacobi_plan_error": (c_int, [c_void_p, P(c_int)]),
     "hrt_jacobi_plan_set_sides": (c_int, [c_void_p, c_void_p]),
+    "hrt_jacobi_plan_set_vpush": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_wave_counters": (c_int, [c_void_p, P(c_u64), P(c_i64)]),
     "hrt_jacobi_plan_set_wave_ipc": (c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_int32),
                                              P(c_u64), c_int, c_u64]),

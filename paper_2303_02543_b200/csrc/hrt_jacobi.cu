@@ -31,6 +31,10 @@
 
 #include "hrt_common.cuh"
 
+#ifndef HRT_WAVE_NOFENCE
+#define HRT_WAVE_NOFENCE 0
+#endif
+
 namespace hrt {
 
 // ---------------------------------------------------------------------------
@@ -265,14 +269,32 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// Watchdog: a barrier that has not completed for 20 s means a protocol bug
+// (or a stalled peer); trap so the launch fails loudly instead of hanging
+// the GPU.  The clock is read once per 64 Ki polls.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (mbar_try(bar, parity)) return;
+    unsigned long long t0 = 0;
+    unsigned n = 0;
+    while (!mbar_try(bar, parity)) {
+        if ((++n & 0xFFFFu) == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 20000000000ULL) __trap();
+        }
+    }
 }
 __device__ __forceinline__ void tma_row_load(void* dst, const void* src, uint32_t bytes,
                                              uint64_t* bar) {
@@ -778,6 +800,50 @@ __device__ __forceinline__ void st_release_gpu_u32(unsigned int* p, unsigned int
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Wait until every counter q[d] (null: none) reaches `need`.  The loads are
+// relaxed and independent, so all round trips overlap; one fence afterwards
+// gives them acquire semantics (system scope when any counter lives in
+// another process's memory).  Returns false after a timeout (sets *err).
+template <int ND>
+__device__ __forceinline__ bool wait_counters(const unsigned int* const (&q)[ND],
+                                              const bool (&sys)[ND], unsigned need,
+                                              unsigned long long timeout_ns, int* err) {
+    unsigned v[ND];
+    bool any_sys = false;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        any_sys |= q[d] != nullptr && sys[d];
+        if (!q[d]) v[d] = need;
+        else if (sys[d])
+            asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v[d]) : "l"(q[d]) : "memory");
+        else
+            asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v[d]) : "l"(q[d]) : "memory");
+    }
+    unsigned long long t0 = 0;
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) ok &= v[d] >= need;
+        if (ok) break;
+        if (t0 == 0) t0 = globaltimer_ns();
+        else if (globaltimer_ns() - t0 > timeout_ns) {
+            atomicExch(err, 2);
+            return false;
+        }
+#pragma unroll
+        for (int d = 0; d < ND; ++d)
+            if (v[d] < need) {
+                if (sys[d])
+                    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v[d]) : "l"(q[d]) : "memory");
+                else
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v[d]) : "l"(q[d]) : "memory");
+            }
+    }
+    if (any_sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    return true;
+}
+
 constexpr int WAVE_TQ = 4;  // tile descriptors in flight between producer and consumers
 
 template <bool GUARD, bool RESID, int CW, int STAGES = T4_STAGES>
@@ -836,51 +902,26 @@ slab_wave_kernel(WaveArgs wa) {
                 // this tile and its N/S/W/E neighbours must have finished step k-1
                 const int* nb = wa.nbr + 4 * c;
                 const unsigned need = wa.base + (unsigned)k;
-                unsigned long long t0 = 0;
-                auto wait_on = [&](int64_t d) {
-                    if (dead || d < 0) return;
-                    while (ld_acquire_gpu_u32(wa.done + d) < need) {
-                        if (t0 == 0) t0 = globaltimer_ns();
-                        else if (globaltimer_ns() - t0 > a.timeout_ns) {
-                            atomicExch(a.err, 2);
-                            dead = true;
-                            return;
-                        }
-                    }
-                };
-                // a neighbour rank's tile (IPC-mapped counters, system scope)
-                auto wait_remote = [&](int f, int64_t off) {
-                    if (dead || !wa.rpeer || wa.rpeer[4 * c + f] < 0) return;
-                    const unsigned int* q = wa.peer_done[wa.rpeer[4 * c + f]] +
-                                            (int64_t)wa.rnbr[4 * c + f] * per_chunk + off;
-                    unsigned int v;
-                    for (;;) {
-                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];"
-                                     : "=r"(v) : "l"(q) : "memory");
-                        if (v >= need) break;
-                        if (t0 == 0) t0 = globaltimer_ns();
-                        else if (globaltimer_ns() - t0 > a.timeout_ns) {
-                            atomicExch(a.err, 2);
-                            dead = true;
-                            return;
-                        }
-                    }
-                };
+                // this tile + its N/S/W/E neighbours (inside the chunk, the
+                // adjacent chunk's boundary tile, or another rank's)
                 const int64_t offN = (a.tiles_r - 1) * a.tiles_c + cb, offS = cb;
                 const int64_t offW = rb * a.tiles_c + (a.tiles_c - 1), offE = rb * a.tiles_c;
-                wait_on(tile);
-                if (rb > 0) wait_on(tile - a.tiles_c);
-                else if (nb[0] >= 0) wait_on(nb[0] * per_chunk + offN);
-                else wait_remote(0, offN);
-                if (rb < a.tiles_r - 1) wait_on(tile + a.tiles_c);
-                else if (nb[1] >= 0) wait_on(nb[1] * per_chunk + offS);
-                else wait_remote(1, offS);
-                if (cb > 0) wait_on(tile - 1);
-                else if (nb[2] >= 0) wait_on(nb[2] * per_chunk + offW);
-                else wait_remote(2, offW);
-                if (cb < a.tiles_c - 1) wait_on(tile + 1);
-                else if (nb[3] >= 0) wait_on(nb[3] * per_chunk + offE);
-                else wait_remote(3, offE);
+                const unsigned int* q[5] = {wa.done + tile, nullptr, nullptr, nullptr, nullptr};
+                bool sys[5] = {false, false, false, false, false};
+                auto face = [&](int d, int f, bool inside, int64_t in_tile, int64_t off) {
+                    if (inside) q[d] = wa.done + in_tile;
+                    else if (nb[f] >= 0) q[d] = wa.done + nb[f] * per_chunk + off;
+                    else if (wa.rpeer && wa.rpeer[4 * c + f] >= 0) {
+                        q[d] = wa.peer_done[wa.rpeer[4 * c + f]] +
+                               (int64_t)wa.rnbr[4 * c + f] * per_chunk + off;
+                        sys[d] = true;
+                    }
+                };
+                face(1, 0, rb > 0, tile - a.tiles_c, offN);
+                face(2, 1, rb < a.tiles_r - 1, tile + a.tiles_c, offS);
+                face(3, 2, cb > 0, tile - 1, offW);
+                face(4, 3, cb < a.tiles_c - 1, tile + 1, offE);
+                dead = !wait_counters<5>(q, sys, need, a.timeout_ns, a.err);
                 // other CTAs' generic-proxy stores -> our async-proxy reads
                 asm volatile("fence.proxy.async.global;" ::: "memory");
             }
@@ -925,7 +966,7 @@ slab_wave_kernel(WaveArgs wa) {
         const int* rp = wa.rpeer ? wa.rpeer + 4 * c : nullptr;
         const bool xedge = rp && ((rb == 0 && rp[0] >= 0) || (rb == a.tiles_r - 1 && rp[1] >= 0) ||
                                   (cb == 0 && rp[2] >= 0) || (cb == a.tiles_c - 1 && rp[3] >= 0));
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
         if (xedge) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
         if (tid == 0) {
@@ -935,7 +976,7 @@ slab_wave_kernel(WaveArgs wa) {
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
                              : "memory");
             } else {
-                __threadfence();
+                if (!HRT_WAVE_NOFENCE) __threadfence();
                 st_release_gpu_u32(wa.done + tile, v);
             }
         }
@@ -951,6 +992,15 @@ slab_wave_kernel(WaveArgs wa) {
 // registers and reads the y/z neighbours of plane i from its stage, which is
 // released once plane i is computed.  Sum order (((((xm+xp)+ym)+yp)+zm)+zp).
 
+// Fused halo push for volumes: per chunk, face f (FACES order -x,+x,-y,+y,
+// -z,+z) and parity of the buffer being written, the address that
+// corresponds to this chunk's element offset 0 in the neighbour's ghost
+// plane: target(i,j,k) = ptr[f][p] + (i*sx + j*sy + k).  Null: domain face.
+struct VolPush {
+    double* ptr[6][2];
+};
+static_assert(sizeof(VolPush) == sizeof(hrt_vpush_t), "VolPush layout");
+
 struct VolArgs {
     const ChunkBufs* chunks;   // block table, or null: single chunk (du -> dw)
     const double* du;
@@ -961,6 +1011,7 @@ struct VolArgs {
     int64_t tiles_i, tiles_j, tiles_k;
     int flat;                  // ez == 1 stored with z ghosts: threads tile j only
     unsigned long long* resid;
+    const VolPush* vpush;      // null: no fused push
 };
 
 constexpr int V_CW = 8;
@@ -969,78 +1020,66 @@ constexpr int V_ZROW = V_ZW + 4;       // + k0-2, k0-1, k0+64, k0+65
 constexpr int V_ROWS = V_CW + 2;       // y rows per stage (with halo)
 constexpr int V_STAGES = 8;
 
-template <bool RESID>
-__global__ void __launch_bounds__(32 * (V_CW + 1))
-volume_update_tma_kernel(VolArgs a) {
-    __shared__ alignas(128) double ring[V_STAGES][V_ROWS][V_ZROW];
-    __shared__ alignas(8) uint64_t full[V_STAGES], empty[V_STAGES];
-    __shared__ double red[V_CW];
-
-    const int64_t per_chunk = a.tiles_i * a.tiles_j * a.tiles_k;
-    const int64_t t = blockIdx.x;
-    const int64_t c = t / per_chunk;
-    int64_t rem = t - c * per_chunk;
-    const int64_t ti = rem / (a.tiles_j * a.tiles_k);
-    rem -= ti * a.tiles_j * a.tiles_k;
-    const int64_t tj = rem / a.tiles_k;
-    const int64_t tk = rem - tj * a.tiles_k;
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-
-    const int64_t k0 = 1 + tk * V_ZW;
+// Producer for one volume tile: planes i0-1 .. i1+1, each stage = the tile's
+// V_CW+2 y-rows of z = k0-2 .. k0+65 (one bulk copy per row).
+__device__ __forceinline__ void v_produce(const VolArgs& a, double (*ring)[V_ROWS][V_ZROW],
+                                          uint64_t* full, uint64_t* empty, int& s, uint32_t& ph,
+                                          int64_t c, int64_t i0, int64_t i1, int64_t j0,
+                                          int64_t k0, int parity) {
     const int64_t klast = min(k0 + V_ZW - 1, a.ez);
     const uint32_t bytes = (uint32_t)((((klast - k0 + 4) + 1) & ~int64_t(1)) * 8);
-    const int64_t j0 = 1 + tj * V_CW;
     // stage rows j0-1 .. j0+V_CW, but never beyond the ghost row ey+1
     const int64_t nyr64 = a.ey + 2 - (j0 - 1);
     const int nyr = nyr64 < V_ROWS ? (int)nyr64 : V_ROWS;
-    const int64_t i0 = 1 + ti * a.rows;
-    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
     const int nplanes = (int)(i1 - i0 + 3);
-    const double* __restrict__ u = a.chunks[c].b[a.parity] + a.origin;
-
-    if (tid == 0) {
-        for (int s = 0; s < V_STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], V_CW);
+    const double* src = a.chunks[c].b[parity] + a.origin + (i0 - 1) * a.sx + (j0 - 1) * a.sy +
+                        (k0 - 2);
+    for (int q = 0; q < nplanes; ++q) {
+        mbar_wait(&empty[s], ph ^ 1);  // (a fresh barrier passes parity 1 at once)
+        mbar_expect_tx(&full[s], bytes * (uint32_t)nyr);
+        for (int r = 0; r < nyr; ++r) tma_row_load(&ring[s][r][0], src + r * a.sy, bytes, &full[s]);
+        src += a.sx;
+        if (++s == V_STAGES) {
+            s = 0;
+            ph ^= 1;
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    __syncthreads();
+}
 
-    if (warp == V_CW) {
-        if (lane == 0) {
-            const double* src = u + (i0 - 1) * a.sx + (j0 - 1) * a.sy + (k0 - 2);
-            int s = 0;
-            uint32_t ph = 0;
-            for (int q = 0; q < nplanes; ++q) {
-                if (q >= V_STAGES) mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], bytes * (uint32_t)nyr);
-                for (int r = 0; r < nyr; ++r)
-                    tma_row_load(&ring[s][r][0], src + r * a.sy, bytes, &full[s]);
-                src += a.sx;
-                if (++s == V_STAGES) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-        return;
-    }
-
+// Consumer for the same tile (warp = y-row, lane = 2 z-columns): output
+// planes i0..i1 into buffer parity^1, plus the fused push of boundary cells.
+template <bool GUARD, bool RESID, bool PUSH>
+__device__ __forceinline__ void v_consume(const VolArgs& a, double (*ring)[V_ROWS][V_ZROW],
+                                          uint64_t* full, uint64_t* empty, int& s, uint32_t& ph,
+                                          int64_t c, int64_t i0, int64_t i1, int64_t j0,
+                                          int64_t k0, int parity, double& rmax) {
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nplanes = (int)(i1 - i0 + 3);
     const int64_t j = j0 + warp;
     const int64_t k = k0 + 2 * lane;
     const bool act = (j <= a.ey) && (k <= a.ez);
     const bool both = act && (k + 1 <= a.ez);
     const int r = warp + 1;   // this thread's row in a stage
     const int p = 2 * lane + 2;
-    double* __restrict__ wr = a.chunks[c].b[a.parity ^ 1] + a.origin + i0 * a.sx + j * a.sy + k;
-    double rmax = 0.0;
-    // stage / phase of the plane being read as "dn" and of the "mid" plane
-    int s = 0, sm = 0;
-    uint32_t ph = 0;
+    const int64_t off0 = i0 * a.sx + j * a.sy + k;  // element offset of the first output
+    double* __restrict__ wr = a.chunks[c].b[parity ^ 1] + a.origin + off0;
+    // push faces of this thread as a bitmask (registers are what limits the
+    // volume kernels' occupancy); targets are rebuilt at the rare boundary
+    // stores: x faces at the chunk's first/last plane, y faces for the
+    // boundary rows, z faces for the boundary columns (k = 1 is .x; k = ez
+    // is .x or .y)
+    unsigned pm = 0;
+    if (PUSH && act) {
+        const VolPush* vp = a.vpush + c;
+        const int wp = parity ^ 1;
+        if (i0 == 1 && vp->ptr[0][wp]) pm |= 1u;
+        if (i1 == a.ex && vp->ptr[1][wp]) pm |= 2u;
+        if (j == 1 && vp->ptr[2][wp]) pm |= 4u;
+        if (j == a.ey && vp->ptr[3][wp]) pm |= 8u;
+        if (k == 1 && vp->ptr[4][wp]) pm |= 16u;
+        if ((k == a.ez || k + 1 == a.ez) && vp->ptr[5][wp]) pm |= 32u;
+    }
     auto center = [&](int st) -> double2 {
         return *reinterpret_cast<const double2*>(&ring[st][r][p]);
     };
@@ -1062,7 +1101,7 @@ volume_update_tma_kernel(VolArgs a) {
     advance();
     mbar_wait(&full[s], ph);
     double2 mid = center(s);
-    sm = s;
+    int sm = s;
     advance();
     for (int q = 2; q < nplanes; ++q) {
         mbar_wait(&full[s], ph);
@@ -1075,9 +1114,10 @@ volume_update_tma_kernel(VolArgs a) {
         sm = s;
         advance();
         if (act) {
-            const double ox = div6(sum6(up.x, dn.x, ym.x, yp.x, zm, mid.y));
+            const double ox = div6_t<GUARD>(sum6(up.x, dn.x, ym.x, yp.x, zm, mid.y));
+            double oy = 0.0;
             if (both) {
-                const double oy = div6(sum6(up.y, dn.y, ym.y, yp.y, mid.x, zp));
+                oy = div6_t<GUARD>(sum6(up.y, dn.y, ym.y, yp.y, mid.x, zp));
                 *reinterpret_cast<double2*>(wr) = make_double2(ox, oy);
                 if (RESID)
                     rmax = fmax(rmax, fmax(fabs(__dsub_rn(ox, mid.x)), fabs(__dsub_rn(oy, mid.y))));
@@ -1085,11 +1125,84 @@ volume_update_tma_kernel(VolArgs a) {
                 wr[0] = ox;
                 if (RESID) rmax = fmax(rmax, fabs(__dsub_rn(ox, mid.x)));
             }
+            if (PUSH && pm) {
+                // the reference's pack -> mp_send -> unpack of all six faces
+                // (jacobi.py:102-124, 237) as stores of the producing kernel
+                const VolPush* vp = a.vpush + c;
+                const int wp = parity ^ 1;
+                const int64_t off = off0 + (int64_t)(q - 2) * a.sx;
+                const bool xf = ((pm & 1u) && q == 2) || ((pm & 2u) && q == nplanes - 1);
+                if (xf || (pm & 12u)) {
+                    auto put2 = [&](double* t) {
+                        if (both) *reinterpret_cast<double2*>(t) = make_double2(ox, oy);
+                        else t[0] = ox;
+                    };
+                    if ((pm & 1u) && q == 2) put2(vp->ptr[0][wp] + off);
+                    if ((pm & 2u) && q == nplanes - 1) put2(vp->ptr[1][wp] + off);
+                    if (pm & 4u) put2(vp->ptr[2][wp] + off);
+                    if (pm & 8u) put2(vp->ptr[3][wp] + off);
+                }
+                if (pm & 16u) vp->ptr[4][wp][off] = ox;
+                if (pm & 32u) {
+                    const bool z1y = k + 1 == a.ez;
+                    vp->ptr[5][wp][off + (z1y ? 1 : 0)] = z1y ? oy : ox;
+                }
+            }
         }
         wr += a.sx;
         up = mid;
         mid = dn;
     }
+    release(sm);  // the tile's last plane (the ring continues with the next tile)
+}
+
+template <bool RESID>
+__global__ void __launch_bounds__(32 * (V_CW + 1), 4)
+volume_update_tma_kernel(VolArgs a) {
+    __shared__ alignas(128) double ring[V_STAGES][V_ROWS][V_ZROW];
+    __shared__ alignas(8) uint64_t full[V_STAGES], empty[V_STAGES];
+    __shared__ double red[V_CW];
+
+    const int64_t per_chunk = a.tiles_i * a.tiles_j * a.tiles_k;
+    const int64_t t = blockIdx.x;
+    const int64_t c = t / per_chunk;
+    int64_t rem = t - c * per_chunk;
+    const int64_t ti = rem / (a.tiles_j * a.tiles_k);
+    rem -= ti * a.tiles_j * a.tiles_k;
+    const int64_t tj = rem / a.tiles_k;
+    const int64_t tk = rem - tj * a.tiles_k;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+
+    const int64_t k0 = 1 + tk * V_ZW;
+    const int64_t j0 = 1 + tj * V_CW;
+    const int64_t i0 = 1 + ti * a.rows;
+    const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+
+    if (tid == 0) {
+        for (int s = 0; s < V_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], V_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    int s = 0;
+    uint32_t ph = 0;
+    if (warp == V_CW) {
+        if (lane == 0) v_produce(a, ring, full, empty, s, ph, c, i0, i1, j0, k0, a.parity);
+        return;
+    }
+    double rmax = 0.0;
+    if (a.vpush)
+        v_consume<true, RESID, true>(a, ring, full, empty, s, ph, c, i0, i1, j0, k0, a.parity,
+                                     rmax);
+    else
+        v_consume<true, RESID, false>(a, ring, full, empty, s, ph, c, i0, i1, j0, k0, a.parity,
+                                      rmax);
 
     if (RESID) {
         rmax = warp_max(rmax);
@@ -1100,6 +1213,177 @@ volume_update_tma_kernel(VolArgs a) {
 #pragma unroll
             for (int q = 1; q < V_CW; ++q) m2 = fmax(m2, red[q]);
             resid_max(a.resid, m2);
+        }
+    }
+}
+
+// Persistent wavefront for volumes: the slab protocol (tickets, per-tile
+// step counters, tile-descriptor queue, timeouts) with 6-neighbour tile
+// dependencies — (i, j, k) block neighbours inside a chunk, the adjacent
+// chunk's boundary tile across a face — and the fused 6-face push.
+struct VolWaveArgs {
+    VolArgs v;
+    const int* nbr;               // [nchunks][6] neighbour chunk or -1
+    unsigned int* done;           // [T]
+    unsigned long long* ticket;
+    unsigned int base;
+    int nsteps;
+    int parity0;
+    int64_t ntiles;
+    unsigned long long* resid;
+    unsigned long long timeout_ns;
+    int* err;
+    const int* rnbr;              // [nchunks][6] (cross-process faces) or null
+    const int* rpeer;
+    unsigned int* const* peer_done;
+};
+
+template <bool RESID>
+__global__ void __launch_bounds__(32 * (V_CW + 1), 4)
+volume_wave_kernel(VolWaveArgs wa) {
+    __shared__ alignas(128) double ring[V_STAGES][V_ROWS][V_ZROW];
+    __shared__ alignas(8) uint64_t full[V_STAGES], empty[V_STAGES], tq_full[WAVE_TQ],
+        tq_empty[WAVE_TQ];
+    __shared__ long long tq[WAVE_TQ];
+    __shared__ double red[V_CW];
+    const VolArgs& a = wa.v;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int64_t T = wa.ntiles;
+    const int64_t tjk = a.tiles_j * a.tiles_k;
+    const int64_t per_chunk = a.tiles_i * tjk;
+    const long long total = (long long)T * wa.nsteps;
+
+    if (tid == 0) {
+        for (int k = 0; k < V_STAGES; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], V_CW);
+        }
+        for (int k = 0; k < WAVE_TQ; ++k) {
+            mbar_init(&tq_full[k], 1);
+            mbar_init(&tq_empty[k], V_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto decode = [&](int64_t tile, int64_t& c, int64_t& ti, int64_t& tj, int64_t& tk) {
+        c = tile / per_chunk;
+        int64_t rem = tile - c * per_chunk;
+        ti = rem / tjk;
+        rem -= ti * tjk;
+        tj = rem / a.tiles_k;
+        tk = rem - tj * a.tiles_k;
+    };
+
+    int s = 0;
+    uint32_t ph = 0;
+    if (warp == V_CW) {
+        if (lane != 0) return;
+        bool dead = false;
+        int slot = 0;
+        uint32_t tph = 0;
+        for (;;) {
+            const long long t = (long long)atomicAdd(wa.ticket, 1ull);
+            mbar_wait(&tq_empty[slot], tph ^ 1);
+            tq[slot] = t < total ? t : -1;
+            mbar_arrive(&tq_full[slot]);
+            if (++slot == WAVE_TQ) {
+                slot = 0;
+                tph ^= 1;
+            }
+            if (t >= total) break;
+            const int k = (int)(t / T);
+            const int64_t tile = t - (long long)k * T;
+            int64_t c, ti, tj, tk;
+            decode(tile, c, ti, tj, tk);
+            if (!dead) {
+                const int* nb = wa.nbr + 6 * c;
+                const unsigned need = wa.base + (unsigned)k;
+                auto tix = [&](int64_t cc, int64_t i, int64_t j, int64_t kk) {
+                    return cc * per_chunk + i * tjk + j * a.tiles_k + kk;
+                };
+                const unsigned int* q[7] = {wa.done + tile, nullptr, nullptr, nullptr,
+                                            nullptr, nullptr, nullptr};
+                bool sys[7] = {false, false, false, false, false, false, false};
+                // face f: the adjacent tile inside the chunk if any, else the
+                // neighbour chunk's boundary tile (local or another rank's)
+                auto face = [&](int f, bool inside, int64_t ii, int64_t jj, int64_t kk, int64_t bi,
+                                int64_t bj, int64_t bk) {
+                    const int d = f + 1;
+                    if (inside) q[d] = wa.done + tix(c, ii, jj, kk);
+                    else if (nb[f] >= 0) q[d] = wa.done + tix(nb[f], bi, bj, bk);
+                    else if (wa.rpeer && wa.rpeer[6 * c + f] >= 0) {
+                        q[d] = wa.peer_done[wa.rpeer[6 * c + f]] +
+                               tix(wa.rnbr[6 * c + f], bi, bj, bk);
+                        sys[d] = true;
+                    }
+                };
+                face(0, ti > 0, ti - 1, tj, tk, a.tiles_i - 1, tj, tk);
+                face(1, ti < a.tiles_i - 1, ti + 1, tj, tk, 0, tj, tk);
+                face(2, tj > 0, ti, tj - 1, tk, ti, a.tiles_j - 1, tk);
+                face(3, tj < a.tiles_j - 1, ti, tj + 1, tk, ti, 0, tk);
+                face(4, tk > 0, ti, tj, tk - 1, ti, tj, a.tiles_k - 1);
+                face(5, tk < a.tiles_k - 1, ti, tj, tk + 1, ti, tj, 0);
+                dead = !wait_counters<7>(q, sys, need, wa.timeout_ns, wa.err);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            const int64_t i0 = 1 + ti * a.rows;
+            v_produce(a, ring, full, empty, s, ph, c, i0, min(a.ex, i0 + a.rows - 1),
+                      1 + tj * V_CW, 1 + tk * V_ZW, (wa.parity0 + k) & 1);
+        }
+        return;
+    }
+    int slot = 0;
+    uint32_t tph = 0;
+    for (;;) {
+        mbar_wait(&tq_full[slot], tph);
+        const long long t = tq[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tq_empty[slot]);
+        if (++slot == WAVE_TQ) {
+            slot = 0;
+            tph ^= 1;
+        }
+        if (t < 0) break;
+        const int k = (int)(t / T);
+        const int64_t tile = t - (long long)k * T;
+        int64_t c, ti, tj, tk;
+        decode(tile, c, ti, tj, tk);
+        const int64_t i0 = 1 + ti * a.rows;
+        const int64_t i1 = min(a.ex, i0 + a.rows - 1);
+        double rmax = 0.0;
+        v_consume<true, RESID, true>(a, ring, full, empty, s, ph, c, i0, i1, 1 + tj * V_CW,
+                                     1 + tk * V_ZW, (wa.parity0 + k) & 1, rmax);
+        if (RESID && wa.resid) {  // one atomic per tile (folded at the barrier below)
+            rmax = warp_max(rmax);
+            if (lane == 0) red[warp] = rmax;
+        }
+        const int* rp = wa.rpeer ? wa.rpeer + 6 * c : nullptr;
+        const bool xedge = rp && ((ti == 0 && rp[0] >= 0) || (ti == a.tiles_i - 1 && rp[1] >= 0) ||
+                                  (tj == 0 && rp[2] >= 0) || (tj == a.tiles_j - 1 && rp[3] >= 0) ||
+                                  (tk == 0 && rp[4] >= 0) || (tk == a.tiles_k - 1 && rp[5] >= 0));
+        if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (xedge) __threadfence_system();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * V_CW));
+        if (tid == 0) {
+            if (RESID && wa.resid) {
+                double m2 = red[0];
+#pragma unroll
+                for (int w = 1; w < V_CW; ++w) m2 = fmax(m2, red[w]);
+                resid_max(wa.resid + k, m2);
+            }
+            const unsigned v = wa.base + (unsigned)k + 1u;
+            if (xedge) {
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
+                             : "memory");
+            } else {
+                if (!HRT_WAVE_NOFENCE) __threadfence();
+                st_release_gpu_u32(wa.done + tile, v);
+            }
         }
     }
 }
@@ -1417,8 +1701,14 @@ struct Plan {
     int64_t* d_offs = nullptr;  // chunk origins in the field (field_copy)
     ChunkPush* d_push = nullptr;  // fused halo push table (slab variant 2)
     ChunkSide* d_sides = nullptr; // contiguous west/east ghost columns (push mode)
+    VolPush* d_vpush = nullptr;   // fused 6-face halo push (volume plans, TMA kernel)
     bool ghosts_ready = false;    // ghost planes of the next buffer are current
     bool push_on() const { return d_push != nullptr && L.ndim == 2 && variant == 2; }
+    bool vpush_on() const {
+        return d_vpush != nullptr && L.ndim == 3 && variant != 0 && L.origin % 2 == 1 &&
+               L.stride[1] % 2 == 0;
+    }
+    bool any_push() const { return push_on() || vpush_on(); }
     // split schedule (push mode with remote faces): edge tiles first, the
     // NCCL exchange on `side` overlapped with the inner tiles
     int* d_tiles_edge = nullptr;
@@ -1475,7 +1765,7 @@ struct Plan {
     bool narrow_ok = true;
     bool narrow_chunk() const { return narrow_ok && L.ext[1] <= 256; }
     bool persist_on() const {
-        return persist && push_on() && !nbr.empty() && (wave_ipc || (remote.empty() && !ipc));
+        return persist && any_push() && !nbr.empty() && (wave_ipc || (remote.empty() && !ipc));
     }
 };
 
@@ -1562,7 +1852,7 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
             slab_update_kernel<<<(unsigned)grid, SLAB_THREADS, 0, s>>>(a);
         }
     } else {
-        VolArgs a;
+        VolArgs a{};
         a.chunks = p->d_chunks;
         a.parity = parity;
         a.ex = L.ext[0];
@@ -1579,6 +1869,7 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.dw = nullptr;
         a.flat = 0;
         a.resid = resid;
+        a.vpush = p->vpush_on() ? p->d_vpush : nullptr;
         // TMA ring variant needs 16-byte aligned z rows (origin odd, sy even)
         const bool tma = p->variant != 0 && (L.origin % 2 == 1) && (L.stride[1] % 2 == 0);
         if (tma) {
@@ -1624,6 +1915,8 @@ static void set_carveouts() {
     carveout(slab_wave_kernel<false, false, 2>);
     carveout(slab_update_tma_kernel);
     carveout(volume_update_tma_kernel<true>);
+    carveout(volume_wave_kernel<true>);
+    carveout(volume_wave_kernel<false>);
     carveout(volume_update_tma_kernel<false>);
     cudaGetLastError();
 }
@@ -1670,7 +1963,7 @@ static int launch_remote(Plan* p, cudaStream_t s, int parity) {
 // the remote send staging) itself, so a step is update + remote exchange;
 // the full halo pass runs only when the ghosts are stale (after an upload).
 static int prime_ghosts(Plan* p, cudaStream_t s, int parity) {
-    if (!p->push_on() || p->ghosts_ready) return HRT_OK;
+    if (!p->any_push() || p->ghosts_ready) return HRT_OK;
     int rc = launch_halo(p, s, parity);
     if (rc) return rc;
     p->ghosts_ready = true;
@@ -1760,7 +2053,17 @@ static int build_wave(Plan* p, int64_t ntiles) {
     }
     p->pgrid = 0;
     const bool narrow = p->narrow_chunk();
-    int G = narrow ? wave_occupancy<2>(!p->nonneg) : wave_occupancy<4>(!p->nonneg);
+    int G = 0;
+    if (p->L.ndim == 3) {
+        int dev = 0, sms = 0, a = 0, b = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, volume_wave_kernel<true>, 32 * (V_CW + 1), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, volume_wave_kernel<false>, 32 * (V_CW + 1), 0);
+        G = std::min(a, b) * sms;
+    } else {
+        G = narrow ? wave_occupancy<2>(!p->nonneg) : wave_occupancy<4>(!p->nonneg);
+    }
     HRT_CUDA(cudaGetLastError());
     if (G <= 0) {
         set_error("persistent kernel: no resident CTA slots");
@@ -1789,6 +2092,9 @@ static int build_wave(Plan* p, int64_t ntiles) {
 
 static int64_t wave_tiles(const Plan* p, int64_t* tiles_c_out = nullptr) {
     const int64_t ex = p->L.ext[0], ey = p->L.ext[1];
+    if (p->L.ndim == 3)
+        return (int64_t)p->nchunks * ((ex + p->rows - 1) / p->rows) * ((ey + V_CW - 1) / V_CW) *
+               ((p->L.ext[2] + V_ZW - 1) / V_ZW);
     const int cols = p->narrow_chunk() ? 256 : T4_COLS;
     const int64_t tc = (ey + cols - 1) / cols;
     if (tiles_c_out) *tiles_c_out = tc;
@@ -1813,6 +2119,57 @@ static SlabArgs slab_args(Plan* p, int parity, unsigned long long* resid) {
     return a;
 }
 
+// volume plans: steps [first, first+n) in one volume_wave_kernel launch
+static int launch_persist3(Plan* p, cudaStream_t s, int64_t first, int64_t n,
+                           unsigned long long* resid_base) {
+    const hrt_chunk_layout_t& L = p->L;
+    const int64_t T = wave_tiles(p);
+    if (T == 0) return HRT_OK;
+    int rc;
+    if (p->pgrid == 0 || p->ptiles != T || p->pkey != T * 4 + (p->nonneg ? 1 : 0)) {
+        HRT_CUDA(cudaStreamSynchronize(s));
+        rc = build_wave(p, T);
+        if (rc) return rc;
+    }
+    HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
+    VolWaveArgs wa{};
+    VolArgs& a = wa.v;
+    a.chunks = p->d_chunks;
+    a.parity = (int)(first & 1);
+    a.ex = L.ext[0];
+    a.ey = L.ext[1];
+    a.ez = L.ext[2];
+    a.sx = L.stride[0];
+    a.sy = L.stride[1];
+    a.origin = L.origin;
+    a.rows = p->rows;
+    a.tiles_i = (a.ex + a.rows - 1) / a.rows;
+    a.tiles_j = (a.ey + V_CW - 1) / V_CW;
+    a.tiles_k = (a.ez + V_ZW - 1) / V_ZW;
+    a.vpush = p->d_vpush;
+    wa.nbr = p->d_pnbr;
+    wa.done = p->d_pdone;
+    wa.ticket = p->d_pticket;
+    wa.base = p->pbase;
+    wa.nsteps = (int)n;
+    wa.parity0 = (int)(first & 1);
+    wa.ntiles = T;
+    wa.resid = resid_base ? resid_base + first : nullptr;
+    wa.timeout_ns = p->persist_timeout_ns;
+    wa.err = p->d_err;
+    if (p->wave_ipc) {
+        wa.rnbr = p->d_rnbr;
+        wa.rpeer = p->d_rpeer;
+        wa.peer_done = p->d_peer_done;
+    }
+    void* fn = resid_base ? (void*)volume_wave_kernel<true> : (void*)volume_wave_kernel<false>;
+    const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid, T);
+    void* args[] = {&wa};
+    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (V_CW + 1)), args, 0, s));
+    p->pbase += (unsigned)n;
+    return HRT_OK;
+}
+
 // steps [first, first+n) in one persistent wavefront launch
 static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                           unsigned long long* resid_base) {
@@ -1820,6 +2177,7 @@ static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     const int parity0 = (int)(first & 1);
     int rc = prime_ghosts(p, s, parity0);
     if (rc) return rc;
+    if (p->L.ndim == 3) return launch_persist3(p, s, first, n, resid_base);
     const bool narrow = p->narrow_chunk();
     SlabArgs a = slab_args(p, parity0, nullptr);
     const int64_t T = wave_tiles(p, &a.tiles_c);
@@ -1909,7 +2267,7 @@ static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* re
         HRT_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
         return HRT_OK;
     }
-    if (p->push_on()) {
+    if (p->any_push()) {
         int rc = prime_ghosts(p, s, parity);
         if (rc) return rc;
         rc = launch_update(p, s, parity, slot);
@@ -2058,6 +2416,25 @@ int hrt_jacobi_plan_set_sides(void* plan, const hrt_side_t* table) {
     return HRT_OK;
 }
 
+int hrt_jacobi_plan_set_vpush(void* plan, const hrt_vpush_t* table) {
+    HRT_CHECK_ARG(plan, "null plan");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    HRT_CHECK_ARG(!table || p->L.ndim == 3, "vpush is for volume plans");
+    cudaFree(p->d_vpush);
+    p->d_vpush = nullptr;
+    p->ghosts_ready = false;
+    if (p->graph) {
+        cudaGraphExecDestroy(p->graph);
+        p->graph = nullptr;
+    }
+    if (!table || p->nchunks == 0) return HRT_OK;
+    HRT_CUDA(cudaMalloc(&p->d_vpush, sizeof(VolPush) * p->nchunks));
+    HRT_CUDA(cudaMemcpy(p->d_vpush, table, sizeof(VolPush) * p->nchunks, cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
 // Split schedule for push mode with remote faces: remote_mask[c] has bit f
 // set when face f of chunk c (plan order) crosses a process boundary; tiles
 // touching such faces run first, the NCCL exchange overlaps the rest.
@@ -2194,8 +2571,8 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
         p->persist = false;
         return HRT_OK;
     }
-    HRT_CHECK_ARG(p->L.ndim == 2, "persistent mode needs a slab layout");
-    for (int i = 0; i < 4 * p->nchunks; ++i)
+    const int nf = 2 * p->L.ndim;  // faces per chunk: 4 (slab) or 6 (volume)
+    for (int i = 0; i < nf * p->nchunks; ++i)
         HRT_CHECK_ARG(nbr4[i] >= -1 && nbr4[i] < p->nchunks, "neighbour index out of range");
     int coop = 0;
     HRT_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->gpu));
@@ -2204,7 +2581,7 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
         return HRT_E_UNSUPPORTED;
     }
     HRT_CUDA(cudaDeviceSynchronize());  // no launch of the old build in flight
-    p->nbr.assign(nbr4, nbr4 + 4 * p->nchunks);
+    p->nbr.assign(nbr4, nbr4 + nf * p->nchunks);
     cudaFree(p->d_pnbr);
     p->d_pnbr = nullptr;
     p->persist = true;
@@ -2255,17 +2632,18 @@ int hrt_jacobi_plan_set_wave_ipc(void* plan, const int32_t* rpeer4, const int32_
     HRT_CHECK_ARG(p->persist && p->d_pdone, "export the wave counters first");
     int rc = use_device(p->gpu);
     if (rc) return rc;
-    for (int i = 0; i < 4 * p->nchunks; ++i)
+    const int nf = 2 * p->L.ndim;
+    for (int i = 0; i < nf * p->nchunks; ++i)
         HRT_CHECK_ARG(rpeer4[i] >= -1 && rpeer4[i] < n_peers, "peer slot out of range");
     cudaFree(p->d_rnbr);
     cudaFree(p->d_rpeer);
     cudaFree(p->d_peer_done);
-    const size_t n4 = sizeof(int) * 4 * (size_t)std::max(1, p->nchunks);
+    const size_t n4 = sizeof(int) * nf * (size_t)std::max(1, p->nchunks);
     HRT_CUDA(cudaMalloc(&p->d_rnbr, n4));
     HRT_CUDA(cudaMalloc(&p->d_rpeer, n4));
     HRT_CUDA(cudaMalloc(&p->d_peer_done, sizeof(void*) * n_peers));
-    HRT_CUDA(cudaMemcpy(p->d_rnbr, rnbr4, sizeof(int) * 4 * p->nchunks, cudaMemcpyHostToDevice));
-    HRT_CUDA(cudaMemcpy(p->d_rpeer, rpeer4, sizeof(int) * 4 * p->nchunks, cudaMemcpyHostToDevice));
+    HRT_CUDA(cudaMemcpy(p->d_rnbr, rnbr4, n4, cudaMemcpyHostToDevice));
+    HRT_CUDA(cudaMemcpy(p->d_rpeer, rpeer4, n4, cudaMemcpyHostToDevice));
     HRT_CUDA(cudaMemcpy(p->d_peer_done, peer_done, sizeof(void*) * n_peers,
                         cudaMemcpyHostToDevice));
     p->wave_ipc = true;
@@ -2338,7 +2716,7 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
     // IPC step tags are per launch; in push mode graph replays measured 40 %
     // slower than direct launches on B200 (cause not yet identified; the
     // max-shared carveout did not change it), so push mode launches directly
-    if (mode == 0 || r != nullptr || p->ipc_on() || p->push_on()) {
+    if (mode == 0 || r != nullptr || p->ipc_on() || p->any_push()) {
         for (int64_t k = 0; k < n; ++k) {
             rc = do_step(p, s, first + k, r);
             if (rc) return rc;
@@ -2416,7 +2794,7 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
         return HRT_OK;
     }
     HRT_CUDA(cudaEventRecord(ev[0], s));
-    const bool push = p->push_on();
+    const bool push = p->any_push();
     const bool split = p->split_on() || p->ipc_on();
     for (int64_t k = 0; k < n; ++k) {
         const int64_t step = first + k;
@@ -2475,6 +2853,7 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_offs);
     cudaFree(p->d_push);
     cudaFree(p->d_sides);
+    cudaFree(p->d_vpush);
     cudaFree(p->d_tiles_edge);
     cudaFree(p->d_tiles_inner);
     cudaFree(p->d_tiles_all);
@@ -2533,7 +2912,7 @@ int hrt_jacobi_chunk_update(void* stream, const double* u, double* nxt, int64_t 
     Stream* st = as_stream(stream);
     int rc = use_device(st->gpu);
     if (rc) return rc;
-    VolArgs a;
+    VolArgs a{};
     a.chunks = nullptr;
     a.du = u;
     a.dw = nxt;

@@ -67,7 +67,7 @@ class DistributedJacobi(JacobiSolver):
 
     def __init__(self, grid: ChunkGrid, rank: int, world: int, gpu: int,
                  comm: Optional[int] = None, rows: Optional[int] = None,
-                 variant: Optional[int] = None):
+                 variant: Optional[int] = None, vpush: Optional[bool] = None):
         if grid.ranks != world:
             raise ValueError("grid.ranks must equal the world size")
         if comm is None and world > 1:
@@ -83,9 +83,14 @@ class DistributedJacobi(JacobiSolver):
         cross = [(f, ch.rank, grid.chunks[nb].rank) for ch in grid.chunks
                  for f, nb in ch.neighbors.items() if grid.chunks[nb].rank != ch.rank]
         rows_only = bool(cross) and all(f in (0, 1) for f, _, _ in cross)
-        if (world > 1 and self.push and rows_only
-                and os.environ.get("HRT_IPC", "1") != "0"):
-            self._setup_ipc(gpu)
+        if world > 1 and rows_only and os.environ.get("HRT_IPC", "1") != "0":
+            if self.push:
+                self._setup_ipc(gpu)
+            elif (self.layout.ndim == 3 and variant != 0
+                  and (vpush if vpush is not None else os.environ.get("HRT_VPUSH", "0") == "1")
+                  and os.environ.get("HRT_PUSH", "1") != "0"
+                  and os.environ.get("HRT_PERSIST", "1") != "0"):
+                self._setup_ipc3(gpu)
 
     def _setup_ipc(self, gpu: int) -> None:
         """Fused compute + communication across processes: map the neighbour
@@ -157,6 +162,43 @@ class DistributedJacobi(JacobiSolver):
             self._setup_wave_ipc(g, mine, nbr_ranks)
         dist.barrier()
 
+    def _setup_ipc3(self, gpu: int) -> None:
+        """Volumes split along x between processes: map the neighbour ranks'
+        chunk arenas, push boundary planes into their ghost planes from the
+        update kernel (6-face vpush table) and run the persistent wavefront
+        with cross-process tile counters.  NCCL primes ghosts after uploads
+        and reduces the residual."""
+        import torch.distributed as dist
+
+        g = self.used_gpus[0]
+        mine = [lin for lin in self.owned if self.placement[lin] == g]
+        nbr_ranks = sorted({self.rank_of[nb] for lin in mine
+                            for nb in self.grid.chunks[lin].neighbors.values()
+                            if nb not in self.placement})
+        h_pool = ctypes.create_string_buffer(64)
+        N.call("hrt_ipc_get_handle", ctypes.c_void_p(self.pools[g].base), h_pool)
+        every = [None] * self.world
+        dist.all_gather_object(every, (h_pool.raw, self.pools[g].base,
+                                       {lin: self.bufs[lin] for lin in mine}))
+        mapped = {}
+        for q in nbr_ranks:
+            hp, base_q, _ = every[q]
+            pp = ctypes.c_void_p()
+            N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(hp, 64), ctypes.byref(pp))
+            mapped[q] = (pp.value, base_q)
+            self._ipc_maps.append(pp.value)
+
+        def remote_buf(nb: int, p: int) -> int:
+            q = self.rank_of[nb]
+            mp, base_q = mapped[q]
+            return mp + (every[q][2][nb][p] - base_q)
+
+        self._setup_vpush(remote_buf)
+        self.vpush = True
+        self.ipc = True
+        self._setup_wave_ipc(g, mine, nbr_ranks)
+        dist.barrier()
+
     def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list) -> None:
         """Persistent wavefront across processes: every rank exports its
         per-tile step counters over CUDA IPC; an edge tile waits on the
@@ -167,9 +209,10 @@ class DistributedJacobi(JacobiSolver):
 
         plan = self.plans[g]
         index = {lin: i for i, lin in enumerate(mine)}
+        nf = 2 * self.layout.ndim
         nbr = [index.get(self.grid.chunks[lin].neighbors.get(f), -1)
                if self.grid.chunks[lin].neighbors.get(f) is not None else -1
-               for lin in mine for f in range(4)]
+               for lin in mine for f in range(nf)]
         N.call("hrt_jacobi_plan_set_persistent", plan, _arr(ctypes.c_int32, nbr), 0)
         ptr, ntiles = ctypes.c_uint64(), ctypes.c_int64()
         N.call("hrt_jacobi_plan_wave_counters", plan, ctypes.byref(ptr), ctypes.byref(ntiles))
@@ -188,7 +231,7 @@ class DistributedJacobi(JacobiSolver):
             peer_ptrs.append(pq.value)
         rpeer, rnbr = [], []
         for lin in mine:
-            for f in range(4):
+            for f in range(nf):
                 nb = self.grid.chunks[lin].neighbors.get(f)
                 if nb is None or nb in self.placement:
                     rpeer.append(-1)

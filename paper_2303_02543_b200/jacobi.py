@@ -267,7 +267,8 @@ class JacobiSolver:
     def __init__(self, grid: ChunkGrid, gpus: Optional[Sequence[int]] = None,
                  placement: Optional[dict[int, int]] = None, rows: Optional[int] = None,
                  rank: Optional[int] = None, comm=None, variant: Optional[int] = None,
-                 push: Optional[bool] = None, persistent: Optional[bool] = None):
+                 push: Optional[bool] = None, persistent: Optional[bool] = None,
+                 vpush: Optional[bool] = None):
         N.require_gpu(0)
         if variant is None and os.environ.get("HRT_SLAB_VARIANT"):
             variant = int(os.environ["HRT_SLAB_VARIANT"])
@@ -418,12 +419,20 @@ class JacobiSolver:
         self._set_offsets()
         if self.push:
             self._setup_push()
+        # volumes: fused 6-face push + wavefront (opt-in: measured slower than
+        # tile launches + halo pass on B200 at 1024x1024x768)
+        if vpush is None:
+            vpush = os.environ.get("HRT_VPUSH", "0") == "1"
+        self.vpush = bool(vpush) and push is not False and \
+            L.ndim == 3 and variant != 0 and not remote_ops
+        if self.vpush:
+            self._setup_vpush()
         # one GPU, no cross-process faces: runs of steps as one persistent
         # dataflow launch (no per-step launch ramp/tail, no grid barrier)
         if persistent is None:
             persistent = os.environ.get("HRT_PERSIST", "1") != "0"
-        self.persistent = bool(persistent) and self.push and len(self.used_gpus) == 1 \
-            and not remote_ops
+        self.persistent = bool(persistent) and (self.push or self.vpush) and \
+            len(self.used_gpus) == 1 and not remote_ops
         if self.persistent:
             self._setup_persistent()
         self._init_ghosts()
@@ -542,13 +551,42 @@ class JacobiSolver:
                 N.call("hrt_jacobi_plan_set_split", self.plans[g],
                        _arr(ctypes.c_int32, masks))
 
+    def _vpush_target(self, nb_buf: int, face: int) -> int:
+        """Address matching our element offset 0 in the neighbour's ghost
+        plane for ``face`` (hrt_vpush_t): the neighbour's buffer shifted by
+        (ghost index - our boundary index) along the face axis."""
+        L = self.layout
+        axis, side = FACES[face]
+        e = L.ext[axis]
+        b, gi = (1, e + 1) if side == 0 else (e, 0)
+        return nb_buf + F64 * (L.origin + (gi - b) * L.stride[axis])
+
+    def _setup_vpush(self, remote_buf=None) -> None:
+        """Fused halo push for volume chunks: every face whose neighbour is
+        in this process (or, with ``remote_buf``, IPC-mapped from another)."""
+        for g in self.used_gpus:
+            mine = [lin for lin in self.owned if self.placement[lin] == g]
+            table = (N.VPush * max(len(mine), 1))()
+            for i, lin in enumerate(mine):
+                for f in range(6):
+                    nb = self.grid.chunks[lin].neighbors.get(f)
+                    if nb is None:
+                        continue
+                    for p in (0, 1):
+                        buf = self.bufs[nb][p] if nb in self.placement else \
+                            (remote_buf(nb, p) if remote_buf else None)
+                        if buf is None:
+                            raise HrtError("vpush: a face crosses processes without a mapping")
+                        table[i].ptr[f][p] = self._vpush_target(buf, f)
+            N.call("hrt_jacobi_plan_set_vpush", self.plans[g], ctypes.byref(table))
+
     def _setup_persistent(self) -> None:
         g = self.used_gpus[0]
         mine = [lin for lin in self.owned if self.placement[lin] == g]
         index = {lin: i for i, lin in enumerate(mine)}
         nbr = []
         for lin in mine:
-            for f in range(4):
+            for f in range(2 * self.layout.ndim):
                 nb = self.grid.chunks[lin].neighbors.get(f)
                 nbr.append(index.get(nb, -1) if nb is not None else -1)
         N.call("hrt_jacobi_plan_set_persistent", self.plans[g], _arr(ctypes.c_int32, nbr), 0)
@@ -727,10 +765,13 @@ class JacobiSolver:
             if b.nbytes < nbytes:
                 raise HrtError(f"host buffer of {b.nbytes} B < field {nbytes} B")
         if not hasattr(self, "_pipe"):
-            pool = DevicePool(g, 4 * (-(-nbytes // 256) * 256) + 4096)
-            fields = [pool.alloc(max(nbytes, 256))[2] for _ in range(4)]
+            # two staging fields: job j's H2D lands in field j%2, is scattered
+            # into the chunks, and the same field then receives job j's
+            # gather for the D2H (the H2D of job j+2 waits for that D2H)
+            pool = DevicePool(g, 2 * (-(-nbytes // 256) * 256) + 4096)
+            fields = [pool.alloc(max(nbytes, 256))[2] for _ in range(2)]
             rpool = DevicePool(g, 2 * (-(-max(steps, 1) * 8 // 256) * 256) + 512)
-            self._pipe = {"pool": pool, "in": fields[:2], "out": fields[2:], "rpool": rpool,
+            self._pipe = {"pool": pool, "in": fields, "out": fields, "rpool": rpool,
                           "rsteps": max(steps, 1),
                           "resid": [rpool.alloc(max(steps, 1) * 8)[2] for _ in range(2)],
                           "h2d": Stream(g, name="jacobi-h2d"), "d2h": Stream(g, name="jacobi-d2h")}
@@ -747,7 +788,12 @@ class JacobiSolver:
         resid_free = [None, None]
 
         def issue_h2d(j: int):
-            h2d.wait(in_free[j % 2]) if in_free[j % 2] else None
+            # the field is free once the job that used it two jobs ago has
+            # been scattered AND downloaded (in == out field)
+            if in_free[j % 2]:
+                h2d.wait(in_free[j % 2])
+            if out_free[j % 2]:
+                h2d.wait(out_free[j % 2])
             N.call("hrt_copy_async", h2d.h, ctypes.c_void_p(pp["in"][j % 2]),
                    ctypes.c_void_p(host_ins[j].ptr), nbytes)
             return h2d.record()

@@ -203,7 +203,11 @@ def test_tma_ring_race_regression(hrt):
                                             ((2048, 1536, 1), (2, 3, 1), 37),
                                             ((512, 2560, 1), (2, 5, 1), 21),
                                             ((3, 700, 1), (1, 2, 1), 9),
-                                            ((1024, 1024, 1), (32, 32, 1), 25)])
+                                            ((1024, 1024, 1), (32, 32, 1), 25),
+                                            ((40, 36, 70), (2, 3, 2), 17),
+                                            ((130, 21, 150), (1, 1, 1), 9),
+                                            ((9, 200, 5), (3, 4, 1), 12),
+                                            ((64, 64, 132), (2, 2, 3), 10)])
 def test_persistent_dataflow_kernel_bitwise(hrt, oracle, dom, grid, steps):
     """The persistent dataflow launch (balanced row segments per resident CTA,
     neighbour step counters instead of per-step launches) against the C
@@ -214,16 +218,17 @@ def test_persistent_dataflow_kernel_bitwise(hrt, oracle, dom, grid, steps):
 
     ref, rref = oracle.jacobi_c(dom, steps, residual=True)
     outs = []
+    vp = len(dom) == 3 and dom[2] > 1  # volumes: the opt-in fused push + wavefront
     for persistent, parts in ((True, [steps]), (True, [steps // 3, steps - steps // 3]),
                               (False, [steps])):
-        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent)
+        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent, vpush=vp)
         assert s.persistent == persistent
         s.upload()
         for n in parts:
             s.run(n, residual=False)
         got = s.download()
         s.close()
-        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent)
+        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent, vpush=vp)
         s.upload()
         s.run(steps, residual=True)
         res = s.residual_history()

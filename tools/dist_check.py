@@ -18,11 +18,12 @@ rank, world, local = init_process("nccl")
 # y faces (strided: packed), x faces (contiguous rows: direct), 3D z faces
 cases = [((1024, 1024, 1), (4, 4, 1), 60), ((600, 520, 1), (3, 2 * world, 1), 77),
          ((512, 300, 1), (2 * world, 1, 1), 45), ((48, 40, 32), (2, 2, world), 21),
-         ((4096, 4096, 1), (8, 8, 1), 130)]
+         ((4096, 4096, 1), (8, 8, 1), 130), ((64, 40, 48), (2 * world, 1, 1), 15)]
 ok_all = True
 for dom, grid, steps in cases:
     cg = ChunkGrid(dom, ranks=world, grid=grid)
-    s = DistributedJacobi(cg, rank, world, local)
+    # 3D x-bands: the opt-in fused push + cross-process wavefront
+    s = DistributedJacobi(cg, rank, world, local, vpush=(grid == (2 * world, 1, 1) and dom[2] > 1))
     boxes = []
     for job in range(2):  # two jobs: re-priming and monotone step tags / counters
         s.upload()
