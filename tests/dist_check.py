@@ -1,7 +1,7 @@
 """Multi-process parity check (run under torchrun, one process per GPU):
 DistributedJacobi with NCCL faces vs the C oracle, field and residual.
 
-torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/dist_check.py
+torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_check.py
 """
 import os
 import sys
