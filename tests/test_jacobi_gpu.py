@@ -153,8 +153,9 @@ def test_arbitrary_initial_data_guarded_division(hrt, oracle, dom, grid):
         assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
 
 
-@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("dom,grid,steps", [((40, 36, 70), (2, 3, 2), 17),
+                                            ((20, 17, 300), (1, 1, 2), 11),
                                             ((130, 21, 150), (1, 1, 1), 9),
                                             ((9, 200, 5), (3, 4, 1), 12)])
 def test_volume_kernels_bitwise(hrt, oracle, variant, dom, grid, steps):
