@@ -94,6 +94,9 @@ int hrt_host_free(void *ptr);
 int hrt_host_register(void *ptr, uint64_t bytes);
 int hrt_host_unregister(void *ptr);
 int hrt_copy_async(void *stream, void *dst, const void *src, uint64_t bytes);   /* H2D/D2H/D2D (UVA) */
+/* SM-driven copy kernel on stream's GPU; dst/src may be peer (NVLink)
+ * addresses, 16-byte aligned.  blocks <= 0: automatic. */
+int hrt_copy_sm_async(void *stream, void *dst, const void *src, uint64_t bytes, int blocks);
 int hrt_copy_peer_async(void *stream, void *dst, int dst_gpu, const void *src, int src_gpu,
                         uint64_t bytes);                                         /* NVLink peer copy */
 int hrt_copy2d_async(void *stream, void *dst, uint64_t dpitch, const void *src, uint64_t spitch,

@@ -496,6 +496,57 @@ int hrt_copy_peer_async(void* stream, void* dst, int dst_gpu, const void* src, i
     return HRT_OK;
 }
 
+}  // extern "C"
+
+namespace hrt {
+// SM-driven copy over NVLink (either pointer may live on a peer GPU): each
+// thread moves 4 x 16 bytes per iteration with independent loads in flight;
+// a head/tail in 8-byte then 1-byte units covers unaligned sizes.
+__global__ void __launch_bounds__(512) sm_copy_kernel(uint8_t* __restrict__ dst,
+                                                      const uint8_t* __restrict__ src,
+                                                      uint64_t n16, uint64_t tail_from,
+                                                      uint64_t bytes) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n16; i += 4 * stride) {
+        const uint4 a = __ldcs(s + i), b = __ldcs(s + i + stride), c = __ldcs(s + i + 2 * stride),
+                    e = __ldcs(s + i + 3 * stride);
+        __stcs(d + i, a);
+        __stcs(d + i + stride, b);
+        __stcs(d + i + 2 * stride, c);
+        __stcs(d + i + 3 * stride, e);
+    }
+    for (; i < n16; i += stride) __stcs(d + i, __ldcs(s + i));
+    const uint64_t t = tail_from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < bytes) dst[t] = src[t];
+}
+}  // namespace hrt
+
+extern "C" {
+
+// cudaMemcpyPeerAsync replacement for GPU<->GPU messages: an SM copy kernel
+// on `stream`'s GPU (peer access to the other side must be enabled).  Needs
+// 16-byte aligned pointers for the vector part.
+int hrt_copy_sm_async(void* stream, void* dst, const void* src, uint64_t bytes, int blocks) {
+    HRT_CHECK_ARG(stream, "null stream");
+    if (bytes == 0) return HRT_OK;
+    HRT_CHECK_ARG(dst && src, "null copy pointer");
+    HRT_CHECK_ARG(((uintptr_t)dst | (uintptr_t)src) % 16 == 0, "sm copy needs 16-byte alignment");
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    const uint64_t n16 = bytes / 16;
+    const uint64_t nb = blocks > 0 ? (uint64_t)blocks
+                                   : std::min<uint64_t>(148 * 4, (n16 + 511) / 512 + 1);
+    hrt::sm_copy_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
+        reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), n16, n16 * 16,
+        bytes);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
 int hrt_copy2d_async(void* stream, void* dst, uint64_t dpitch, const void* src, uint64_t spitch,
                      uint64_t width, uint64_t height) {
     HRT_CHECK_ARG(stream, "null stream");

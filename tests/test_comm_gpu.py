@@ -144,3 +144,37 @@ def test_task_engine_ladder_bitwise(ladder, name):
     assert repr(cs) == e["checksum"]
     if e["kwargs"].get("device_aware"):
         assert sum(s["staging_copies"] for s in rep.meta["stats"]) == 0
+
+
+@pytest.mark.parametrize("push", [False, True])
+def test_sm_copy_kernel_bytes(push):
+    """hrt_copy_sm_async (SM copy over NVLink, pull on the destination or
+    push from the source) moves exactly the bytes, odd sizes included."""
+    import ctypes
+
+    from paper_2303_02543_b200 import _native as N
+    from paper_2303_02543_b200.devices import DevicePool, Stream
+
+    n = N.gpu_count()
+    src_gpu, dst_gpu = 0, (1 if n > 1 else 0)
+    if src_gpu != dst_gpu:
+        N.call("hrt_enable_peer_access", dst_gpu, src_gpu)
+        N.call("hrt_enable_peer_access", src_gpu, dst_gpu)
+    rng = np.random.default_rng(3)
+    for size in (1, 17, 4096 + 9, (3 << 20) + 5):
+        data = rng.integers(0, 256, size=size, dtype=np.uint8)
+        sp, dp = DevicePool(src_gpu, size + 4096), DevicePool(dst_gpu, size + 4096)
+        s_ptr, d_ptr = sp.alloc(size)[2], dp.alloc(size)[2]
+        st_src, st_dst = Stream(src_gpu), Stream(dst_gpu)
+        N.call("hrt_copy_async", st_src.h, ctypes.c_void_p(s_ptr),
+               ctypes.c_void_p(data.ctypes.data), size)
+        st_src.synchronize()
+        st = st_src if push else st_dst
+        N.call("hrt_copy_sm_async", st.h, ctypes.c_void_p(d_ptr), ctypes.c_void_p(s_ptr),
+               ctypes.c_uint64(size), 0)
+        st.synchronize()
+        out = np.empty(size, np.uint8)
+        N.call("hrt_copy_async", st_dst.h, ctypes.c_void_p(out.ctypes.data),
+               ctypes.c_void_p(d_ptr), size)
+        st_dst.synchronize()
+        assert np.array_equal(out, data), size
