@@ -60,6 +60,38 @@ for dom, grid, steps in cases:
         print(f"dist_check world={world} dom={dom} grid={grid} steps={steps}: "
               f"field {'OK' if np.array_equal(full, ref) else 'DIFF'} "
               f"resid {'OK' if np.array_equal(res, rres) else 'DIFF'}", flush=True)
+# full cfg3 size: the N-rank x-band run (IPC wavefront) against one GPU,
+# field bands and residual history bitwise (rank 0 solves the whole domain
+# on its own GPU after the distributed run)
+if os.environ.get("DIST_CHECK_FULL", "1") != "0":
+    dom, steps = (32768, 32768, 1), 40
+    cg = ChunkGrid(dom, ranks=world, grid=(8 * world, 1, 1))
+    s = DistributedJacobi(cg, rank, world, local)
+    s.upload()
+    s.run(steps, residual=True)
+    band, lo = s.download(), s.box_lo
+    res = s.global_residual_history()
+    ipc = (s.ipc, s.persistent)
+    s.close()
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, band.shape, float(band.sum()), band[::97, ::89].copy()))
+    if rank == 0:
+        from paper_2303_02543_b200.jacobi import JacobiSolver
+
+        one = JacobiSolver(ChunkGrid(dom, grid=(8, 1, 1)), gpus=[local])
+        one.upload()
+        one.run(steps, residual=True)
+        full = one.download()
+        r1 = one.residual_history()
+        one.close()
+        ok = np.array_equal(res, r1)
+        for (l0, shape, ssum, sample) in parts:
+            ref = full[l0[0]:l0[0] + shape[0], l0[1]:l0[1] + shape[1]]
+            ok &= float(ref.sum()) == ssum and np.array_equal(ref[::97, ::89], sample)
+        ok &= np.array_equal(band, full[lo[0]:lo[0] + band.shape[0]])
+        ok_all &= ok
+        print(f"dist_check world={world} full cfg3 {dom} steps={steps} (ipc, wavefront)={ipc}: "
+              f"{'OK' if ok else 'DIFF'}", flush=True)
 dist.barrier()
 if rank == 0:
     print("DIST_CHECK", "PASS" if ok_all else "FAIL", flush=True)

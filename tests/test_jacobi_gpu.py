@@ -288,3 +288,36 @@ def test_run_jobs_pipeline_matches_serial(hrt, oracle):
         assert np.array_equal(hists[k], s2.residual_history()), k
         s2.close()
     s.close()
+
+
+def test_full_size_cfg3_and_cfg5_properties(hrt):
+    """BASELINE's largest single-GPU shapes, through size-independent
+    properties (the oracle would take hours): cfg3 32768^2 — x-band (8x1) vs
+    y-band (1x8) decompositions bitwise equal in field, checksum and
+    residual history, exact x-mirror symmetry ((xm+xp) commutes; y-mirror
+    and transpose are not exact under the reference's sum order); cfg5
+    65536^2 in 65,536 chunks of 256^2 — equal to the same domain in 64
+    chunks of 8192^2.
+    Residuals are non-increasing after the first sweep (monotone Jacobi on
+    this problem) and the field stays in (0, 1]."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    def solve(dom, grid, steps):
+        s = JacobiSolver(ChunkGrid(dom, grid=grid))
+        s.upload()
+        s.run(steps, residual=True)
+        out = s.download(), s.checksum(), s.residual_history()
+        s.close()
+        return out
+
+    a, ca, ra = solve((32768, 32768, 1), (8, 1, 1), 60)
+    b, cb, rb = solve((32768, 32768, 1), (1, 8, 1), 60)
+    assert np.array_equal(a, b) and ca == cb and np.array_equal(ra, rb)
+    assert np.array_equal(a, a[::-1])
+    assert a.min() >= 0.0 and a.max() <= 1.0
+    assert np.all(ra[1:] <= ra[:-1])
+    del a, b
+    c, cc, rc = solve((65536, 65536, 1), (256, 256, 1), 12)
+    d, cd, rd = solve((65536, 65536, 1), (8, 8, 1), 12)
+    assert np.array_equal(c, d) and cc == cd and np.array_equal(rc, rd)
+    assert np.array_equal(c, c[::-1])
