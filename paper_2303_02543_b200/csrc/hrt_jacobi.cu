@@ -2333,8 +2333,11 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     // stream launches (measured: a graph replay of the push kernel ran 40 %
     // slower without this).
     set_carveouts();
-    // rows per CTA: enough CTAs to fill the GPU several times over
-    p->rows = layout->ndim == 2 ? 64 : 32;
+    // rows (slab) / planes (volume) per CTA tile.  Volumes: 64 planes halves
+    // the x-halo planes re-read from DRAM (x-adjacent tiles run ~tiles_j *
+    // tiles_k tiles apart, after L2 has dropped them): paper3d 344.6 -> 352
+    // GLUPS; 128 planes leaves too few tiles (319)
+    p->rows = 64;
     if (const char* e = getenv("HRT_NARROW")) p->narrow_ok = e[0] != '0';
     *plan = p;
     return HRT_OK;
