@@ -147,6 +147,7 @@ def cpu_baseline(wl, budget_s: float = 15.0):
     from oracle import oracle as O
 
     O.build()
+    O.use_all_host_threads()
     X, Y, Z = wl["domain"]
     if Z != 1:  # 3D: the C oracle on the full volume, 2 sweeps
         t0 = time.perf_counter()
@@ -415,6 +416,7 @@ def run_reference(args):
     from oracle import oracle as O
 
     O.build()
+    O.use_all_host_threads()
     wl = workload(args.workload, world if args.gpus > 1 else 1)
     X, Y, _ = wl["domain"]
     slab = O.CpuSlab(X, Y)

@@ -243,6 +243,17 @@ int oracle_jacobi2d_sweeps(int64_t X, int64_t Y, int64_t steps) {
     return oracle_jacobi2d(X, Y, steps, NULL, NULL);
 }
 
+/* Use n OpenMP threads from now on (launchers such as torchrun export
+ * OMP_NUM_THREADS=1; the CPU baseline wants every host thread). */
+void oracle_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);
