@@ -431,10 +431,12 @@ class JacobiSolver:
         # dataflow launch (no per-step launch ramp/tail, no grid barrier)
         if persistent is None:
             persistent = os.environ.get("HRT_PERSIST", "1") != "0"
-        self.persistent = bool(persistent) and (self.push or self.vpush) and \
-            len(self.used_gpus) == 1 and not remote_ops
+        self.persistent = bool(persistent) and (self.push or self.vpush) and not remote_ops
         if self.persistent:
-            self._setup_persistent()
+            if len(self.used_gpus) == 1:
+                self._setup_persistent()
+            else:
+                self._setup_persistent_multi()
         self._init_ghosts()
 
     def _set_nonneg(self, flag: bool) -> None:
@@ -580,6 +582,49 @@ class JacobiSolver:
                         table[i].ptr[f][p] = self._vpush_target(buf, f)
             N.call("hrt_jacobi_plan_set_vpush", self.plans[g], ctypes.byref(table))
 
+    def _setup_persistent_multi(self) -> None:
+        """Several GPUs in this process (the reference's in-process ranks):
+        one wavefront launch per GPU per run; a tile on a face shared with
+        another GPU waits on that GPU's tile counter through a peer pointer
+        (NVLink, system-scope acquire) — the same protocol as across
+        processes, without IPC."""
+        nf = 2 * self.layout.ndim
+        mine = {g: [lin for lin in self.owned if self.placement[lin] == g]
+                for g in self.used_gpus}
+        index = {g: {lin: i for i, lin in enumerate(m)} for g, m in mine.items()}
+        counters = {}
+        for g in self.used_gpus:
+            nbr = []
+            for lin in mine[g]:
+                for f in range(nf):
+                    nb = self.grid.chunks[lin].neighbors.get(f)
+                    nbr.append(index[g].get(nb, -1) if nb is not None else -1)
+            N.call("hrt_jacobi_plan_set_persistent", self.plans[g], _arr(ctypes.c_int32, nbr), 0)
+            ptr, nt = ctypes.c_uint64(), ctypes.c_int64()
+            N.call("hrt_jacobi_plan_wave_counters", self.plans[g], ctypes.byref(ptr),
+                   ctypes.byref(nt))
+            counters[g] = ptr.value
+        for g in self.used_gpus:
+            peers = sorted({self.placement[nb] for lin in mine[g]
+                            for nb in self.grid.chunks[lin].neighbors.values()
+                            if self.placement[nb] != g})
+            if not peers:
+                continue
+            rpeer, rnbr = [], []
+            for lin in mine[g]:
+                for f in range(nf):
+                    nb = self.grid.chunks[lin].neighbors.get(f)
+                    h = self.placement.get(nb) if nb is not None else None
+                    if h is None or h == g:
+                        rpeer.append(-1)
+                        rnbr.append(-1)
+                    else:
+                        rpeer.append(peers.index(h))
+                        rnbr.append(index[h][nb])
+            N.call("hrt_jacobi_plan_set_wave_ipc", self.plans[g], _arr(ctypes.c_int32, rpeer),
+                   _arr(ctypes.c_int32, rnbr), _arr(ctypes.c_uint64, [counters[h] for h in peers]),
+                   len(peers), ctypes.c_uint64(30_000_000_000))
+
     def _setup_persistent(self) -> None:
         g = self.used_gpus[0]
         mine = [lin for lin in self.owned if self.placement[lin] == g]
@@ -709,6 +754,17 @@ class JacobiSolver:
             g = self.used_gpus[0]
             N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, first, steps,
                    ctypes.c_void_p(self.resid[g] if residual else 0), 1 if graph else 0)
+        elif self.persistent:
+            # every GPU primes its ghosts (reading its peers' uploaded
+            # interiors) after all uploads, then runs its wavefront; the
+            # cross-GPU tile counters order everything else
+            tok = {g: self.streams[g].record() for g in self.used_gpus}
+            for g in self.used_gpus:
+                for h in self.peer_deps[g]:
+                    self.streams[g].wait(tok[h])
+            for g in self.used_gpus:
+                N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, first, steps,
+                       ctypes.c_void_p(self.resid[g] if residual else 0), 0)
         else:
             prev: dict[int, object] = {}
             for k in range(steps):

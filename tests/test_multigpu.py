@@ -28,19 +28,30 @@ def need_two():
         pytest.skip("needs >= 2 GPUs")
 
 
+@pytest.mark.parametrize("persistent", [True, False])
 @pytest.mark.parametrize("dom,grid,steps", [((1024, 1024, 1), (4, 4, 1), 50),
                                             ((300, 700, 1), (3, 7, 1), 64),
+                                            ((2048, 512, 1), (16, 1, 1), 33),
                                             ((40, 36, 30), (2, 3, 2), 17)])
-def test_single_process_peer_faces(oracle, dom, grid, steps):
+def test_single_process_peer_faces(oracle, dom, grid, steps, persistent):
+    """Several GPUs in one process (the reference's in-process ranks): tile
+    launches with per-step stream waits, or one wavefront launch per GPU
+    with cross-GPU tile counters; runs split over launches."""
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
     n = min(ngpu(), 4)
     s = JacobiSolver(ChunkGrid(dom, ranks=1, devices_per_rank=n, grid=grid),
-                     gpus=list(range(n)))
+                     gpus=list(range(n)), persistent=persistent)
     assert len(s.used_gpus) == n
+    assert s.persistent == (persistent and dom[2] == 1)
+    s.upload()
+    s.run(steps // 2)
+    s.run(steps - steps // 2)
+    got = s.download()
     s.upload()
     s.run(steps)
-    got, res = s.download(), s.residual_history()
+    assert np.array_equal(got, s.download())
+    res = s.residual_history()
     cs = s.checksum()
     s.close()
     ref, rres = oracle.jacobi_c(dom, steps, residual=True)
