@@ -83,7 +83,9 @@ class DistributedJacobi(JacobiSolver):
         cross = [(f, ch.rank, grid.chunks[nb].rank) for ch in grid.chunks
                  for f, nb in ch.neighbors.items() if grid.chunks[nb].rank != ch.rank]
         rows_only = bool(cross) and all(f in (0, 1) for f, _, _ in cross)
-        if world > 1 and rows_only and os.environ.get("HRT_IPC", "1") != "0":
+        # column faces qualify once they are contiguous (side arrays)
+        slab_ok = bool(cross) and self.push and (rows_only or self.side_mode)
+        if world > 1 and os.environ.get("HRT_IPC", "1") != "0" and (slab_ok or rows_only):
             if self.push:
                 self._setup_ipc(gpu)
             elif (self.layout.ndim == 3 and variant != 0
@@ -95,7 +97,8 @@ class DistributedJacobi(JacobiSolver):
     def _setup_ipc(self, gpu: int) -> None:
         """Fused compute + communication across processes: map the neighbour
         ranks' chunk arenas with CUDA IPC, point the push table's remote faces
-        at their ghost planes (stores over NVLink from the update kernel) and
+        at their ghost rows or (columns) contiguous side arrays (stores over
+        NVLink from the update kernel) and
         give every rank one flag slot per neighbour for the per-step
         handshake.  NCCL remains only for priming ghosts after an upload and
         for the residual all-reduce."""
@@ -115,12 +118,13 @@ class DistributedJacobi(JacobiSolver):
         N.call("hrt_ipc_get_handle", ctypes.c_void_p(self.pools[g].base), h_pool)
         N.call("hrt_ipc_get_handle", ctypes.c_void_p(self._flags.base), h_flags)
         info = (self.rank, h_pool.raw, self.pools[g].base, h_flags.raw,
-                {lin: self.bufs[lin] for lin in mine}, nbr_ranks)
+                {lin: self.bufs[lin] for lin in mine}, nbr_ranks,
+                {lin: self.sides.get(lin, {}) for lin in mine})
         every = [None] * self.world
         dist.all_gather_object(every, info)
         mapped_pool, mapped_flags = {}, {}
         for q in nbr_ranks:
-            _, hp, base_q, hf, _, _ = every[q]
+            _, hp, base_q, hf = every[q][:4]
             pp, pf = ctypes.c_void_p(), ctypes.c_void_p()
             N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(hp, 64), ctypes.byref(pp))
             N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(hf, 64), ctypes.byref(pf))
@@ -133,6 +137,17 @@ class DistributedJacobi(JacobiSolver):
             mp, base_q = mapped_pool[q]
             return mp + (every[q][4][nb][p] - base_q)
 
+        def remote_ghost(nb: int, face: int, p: int):
+            """(address, stride) of remote chunk nb's ghost plane `face`:
+            its mapped side array (west/east, side mode) or ghost row."""
+            q = self.rank_of[nb]
+            side = every[q][6].get(nb, {}).get(face)
+            if side is not None:
+                mp, base_q = mapped_pool[q]
+                return mp + (side[p] - base_q), 1
+            addr, _, _, _, s1 = face_plane(L, remote_buf(nb, p), face, ghost=True)
+            return addr, s1
+
         table = (N.Push * max(len(mine), 1))()
         masks = []
         for i, lin in enumerate(mine):
@@ -144,9 +159,8 @@ class DistributedJacobi(JacobiSolver):
                 for p in (0, 1):
                     if nb in self.placement:  # (side array or in-buffer ghost plane)
                         addr, _, _, _, s1 = self._ghost_target(nb, opposite(f), p)
-                    else:  # rows only across processes
-                        addr, _, _, _, s1 = face_plane(L, remote_buf(nb, p), opposite(f),
-                                                       ghost=True)
+                    else:  # another process: mapped ghost row or side array
+                        addr, s1 = remote_ghost(nb, opposite(f), p)
                     table[i].ptr[f][p] = addr
                 table[i].stride[f] = s1
                 if nb not in self.placement:
