@@ -96,6 +96,7 @@ SIGNATURES = {
     "hrt_host_register": (c_int, [c_void_p, c_u64]),
     "hrt_host_unregister": (c_int, [c_void_p]),
     "hrt_copy_async": (c_int, [c_void_p, c_void_p, c_void_p, c_u64]),
+    "hrt_bytes_equal": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, P(c_int)]),
     "hrt_copy_sm_async": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, c_int]),
     "hrt_copy_peer_async": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_u64]),
     "hrt_copy2d_async": (c_int, [c_void_p, c_void_p, c_u64, c_void_p, c_u64, c_u64, c_u64]),

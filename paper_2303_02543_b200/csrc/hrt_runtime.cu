@@ -522,9 +522,54 @@ __global__ void __launch_bounds__(512) sm_copy_kernel(uint8_t* __restrict__ dst,
     const uint64_t t = tail_from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < bytes) dst[t] = src[t];
 }
+// counts differing bytes of a and b (16-byte words, then the tail)
+__global__ void __launch_bounds__(512) bytes_diff_kernel(const uint8_t* __restrict__ a,
+                                                         const uint8_t* __restrict__ b,
+                                                         uint64_t n16, uint64_t bytes,
+                                                         unsigned long long* diff) {
+    const uint4* x = reinterpret_cast<const uint4*>(a);
+    const uint4* y = reinterpret_cast<const uint4*>(b);
+    unsigned long long d = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+        const uint4 u = x[i], v = y[i];
+        d += (u.x != v.x) + (u.y != v.y) + (u.z != v.z) + (u.w != v.w);
+    }
+    const uint64_t t = n16 * 16 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < bytes) d += a[t] != b[t];
+    if (d) atomicAdd(diff, d);
+}
 }  // namespace hrt
 
 extern "C" {
+
+// *equal = 1 when the n bytes at a and b (device or peer addresses, 16-byte
+// aligned) are identical.  Synchronises `stream`.
+int hrt_bytes_equal(void* stream, const void* a, const void* b, uint64_t bytes, int* equal) {
+    HRT_CHECK_ARG(stream && equal, "null argument");
+    *equal = 1;
+    if (bytes == 0) return HRT_OK;
+    HRT_CHECK_ARG(a && b && ((uintptr_t)a | (uintptr_t)b) % 16 == 0,
+                  "bytes_equal needs 16-byte aligned pointers");
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    unsigned long long* d = nullptr;
+    HRT_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), s->s));
+    HRT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s->s));
+    const uint64_t n16 = bytes / 16;
+    const uint64_t nb = std::min<uint64_t>(148 * 4, (n16 + 511) / 512 + 1);
+    hrt::bytes_diff_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
+        reinterpret_cast<const uint8_t*>(a), reinterpret_cast<const uint8_t*>(b), n16, bytes, d);
+    cudaError_t le = cudaGetLastError();
+    unsigned long long h = 0;
+    HRT_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s->s));
+    cudaFreeAsync(d, s->s);
+    HRT_CUDA(cudaStreamSynchronize(s->s));
+    HRT_CUDA(le);
+    *equal = h == 0;
+    return HRT_OK;
+}
 
 // cudaMemcpyPeerAsync replacement for GPU<->GPU messages: an SM copy kernel
 // on `stream`'s GPU (peer access to the other side must be enabled).  Needs
