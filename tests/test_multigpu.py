@@ -60,12 +60,17 @@ def test_single_process_peer_faces(oracle, dom, grid, steps, persistent):
     assert cs == oracle.checksum(ref)
 
 
-def test_torchrun_nccl_faces():
+@pytest.mark.parametrize("persist", ["1", "0"])
+def test_torchrun_nccl_faces(persist):
+    """One process per GPU: the cross-process wavefront (default) or, with
+    HRT_PERSIST=0, per-step tile launches with IPC step flags / NCCL; the
+    full-size cfg3 comparison only in the default mode."""
     n = min(ngpu(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29533",
+           "--master-addr", "127.0.0.1", "--master-port", "2953" + persist,
            os.path.join(ROOT, "tests", "dist_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, HRT_PERSIST=persist, DIST_CHECK_FULL=persist)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert "DIST_CHECK PASS" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
 
 
