@@ -102,6 +102,13 @@ int hrt_bytes_equal(void *stream, const void *a, const void *b, uint64_t bytes, 
 int hrt_copy_sm_async(void *stream, void *dst, const void *src, uint64_t bytes, int blocks);
 int hrt_copy_peer_async(void *stream, void *dst, int dst_gpu, const void *src, int src_gpu,
                         uint64_t bytes);                                         /* NVLink peer copy */
+/* enqueue_transfer in one call (devices.py:446-496): GPU-side waits on the
+ * tokens in waits[0..nwait) (retired tokens are skipped), the copy (method
+ * 0 copy engine, 1 SM kernel, 2 auto: SM kernel for 16-byte aligned
+ * GPU<->GPU copies <= HRT_SM_COPY_MAX bytes, default 64 MiB), then a new
+ * completion token behind it.  peer != 0: src and dst are on different GPUs. */
+int hrt_copy_ordered(void *stream, void *dst, const void *src, uint64_t bytes, int peer,
+                     const uint64_t *waits, int nwait, int method, uint64_t *token);
 int hrt_copy2d_async(void *stream, void *dst, uint64_t dpitch, const void *src, uint64_t spitch,
                      uint64_t width, uint64_t height);
 int hrt_memset_async(void *stream, void *dst, int value, uint64_t bytes);

@@ -99,6 +99,8 @@ SIGNATURES = {
     "hrt_bytes_equal": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, P(c_int)]),
     "hrt_copy_sm_async": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, c_int]),
     "hrt_copy_peer_async": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_u64]),
+    "hrt_copy_ordered": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, c_int, P(c_u64), c_int,
+                                 c_int, P(c_u64)]),
     "hrt_copy2d_async": (c_int, [c_void_p, c_void_p, c_u64, c_void_p, c_u64, c_u64, c_u64]),
     "hrt_memset_async": (c_int, [c_void_p, c_void_p, c_int, c_u64]),
     "hrt_jacobi_plan_create": (c_int, [c_int, P(ChunkLayout), c_int, P(c_u64), P(HaloSeg), c_int,

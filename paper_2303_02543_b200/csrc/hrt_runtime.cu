@@ -9,9 +9,11 @@
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -405,10 +407,30 @@ int hrt_token_query(uint64_t token) {
     return 2;
 }
 
+// Waits poll the event for up to HRT_SPIN_US (default 2000) before the
+// blocking cudaEventSynchronize: a blocking wake-up costs the OS timer slack
+// (~50 us), which doubled small-message round trips whenever the CUDA
+// scheduling heuristic chose to yield.
 int hrt_token_wait(uint64_t token) {
     Token t;
     int rc = find_token(token, &t);
     if (rc) return rc;
+    static const long long spin_ns = [] {
+        const char* e = getenv("HRT_SPIN_US");
+        return (e ? atoll(e) : 2000LL) * 1000LL;
+    }();
+    if (spin_ns > 0) {
+        const auto t0 = std::chrono::steady_clock::now();
+        for (;;) {
+            const cudaError_t e = cudaEventQuery(t.ev);
+            if (e == cudaSuccess) return HRT_OK;
+            if (e != cudaErrorNotReady) HRT_CUDA(e);
+            if (std::chrono::duration_cast<std::chrono::nanoseconds>(
+                    std::chrono::steady_clock::now() - t0).count() > spin_ns)
+                break;
+        }
+        cudaGetLastError();  // clear the sticky not-ready status
+    }
     HRT_CUDA(cudaEventSynchronize(t.ev));
     return HRT_OK;
 }
@@ -589,6 +611,62 @@ int hrt_copy_sm_async(void* stream, void* dst, const void* src, uint64_t bytes, 
         reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), n16, n16 * 16,
         bytes);
     HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
+// One call for a message/transfer copy (the registry's enqueue_transfer,
+// devices.py:446-496): GPU-side waits on `waits`, the copy, and a completion
+// token recorded behind it.  method 0: copy engine (cudaMemcpyAsync over
+// UVA; peer copies ride NVLink), 1: SM pull/push kernel on the stream's GPU
+// (16-byte aligned pointers), 2: automatic — SM kernel for aligned GPU<->GPU
+// copies of at most HRT_SM_COPY_MAX bytes (it beats the copy engine's
+// per-copy latency there, profiles/copy_methods_r01.txt), else the copy
+// engine.  One device switch for the whole sequence: the Python path paid
+// one per native call.
+int hrt_copy_ordered(void* stream, void* dst, const void* src, uint64_t bytes, int peer,
+                     const uint64_t* waits, int nwait, int method, uint64_t* token) {
+    HRT_CHECK_ARG(stream && token, "null argument");
+    HRT_CHECK_ARG(nwait >= 0 && (nwait == 0 || waits), "bad wait list");
+    HRT_CHECK_ARG(bytes == 0 || (dst && src), "null copy pointer");
+    Stream* s = as_stream(stream);
+    int rc = use_device(s->gpu);
+    if (rc) return rc;
+    for (int k = 0; k < nwait; ++k) {
+        Token t;
+        rc = find_token(waits[k], &t);
+        if (rc == HRT_E_UNKNOWN_TOKEN) {  // retired already: nothing to order after
+            continue;
+        }
+        if (rc) return rc;
+        HRT_CUDA(cudaStreamWaitEvent(s->s, t.ev, 0));
+    }
+    if (bytes) {
+        const bool aligned = (((uintptr_t)dst | (uintptr_t)src) % 16) == 0;
+        static const uint64_t sm_max = [] {
+            const char* e = getenv("HRT_SM_COPY_MAX");
+            return e ? (uint64_t)strtoull(e, nullptr, 10) : (uint64_t)(64ull << 20);
+        }();
+        const bool sm = method == 1 || (method == 2 && peer && aligned && bytes <= sm_max);
+        if (sm) {
+            HRT_CHECK_ARG(aligned, "sm copy needs 16-byte alignment");
+            const uint64_t n16 = bytes / 16;
+            const uint64_t nb = std::min<uint64_t>(148 * 4, (n16 + 511) / 512 + 1);
+            hrt::sm_copy_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
+                reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), n16,
+                n16 * 16, bytes);
+            HRT_CUDA(cudaGetLastError());
+        } else {
+            HRT_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s->s));
+        }
+    }
+    cudaEvent_t ev;
+    rc = take_event(s->gpu, cudaEventDefault, &ev);
+    if (rc) return rc;
+    HRT_CUDA(cudaEventRecord(ev, s->s));
+    std::lock_guard<std::mutex> g(g_tok_mu);
+    const uint64_t id = ++g_next_token;
+    g_tokens[id] = Token{ev, s->gpu};
+    *token = id;
     return HRT_OK;
 }
 

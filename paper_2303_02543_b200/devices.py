@@ -27,6 +27,7 @@ bench/jacobi.py:232) target the B200; ``DeviceType.B200`` is an alias.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 from enum import Enum
@@ -416,6 +417,11 @@ class DeviceClock:
         if token.status is TokenStatus.PENDING:
             self._outstanding.append(token)
 
+    def track_pending(self, token: CompletionToken) -> None:
+        """A token recorded just now (no status query: it is pending or
+        will be found complete by the next service pass)."""
+        self._outstanding.append(token)
+
     def schedule(self, token: CompletionToken, end_time: float) -> None:
         self.track(token)
 
@@ -566,6 +572,8 @@ class DeviceRegistry:
         self._devices: dict[int, _Device] = {}
         self._tokens: dict[int, CompletionToken] = {}
         self._peer_enabled: set[tuple[int, int]] = set()
+        # hrt_copy_ordered method: 0 copy engine, 1 SM kernel, 2 auto
+        self.copy_method = int(os.environ.get("HRT_COPY_METHOD", "2"))
 
     # -- registration ----------------------------------------------------
 
@@ -681,22 +689,25 @@ class DeviceRegistry:
         else:
             dev = self.device(sd)
             stream = dev.d2h
-        for t in wait or ():
-            stream.wait(t)
         t0 = self.clock.now
+        peer = 0
         if size:
             g_s = sd[1] if isinstance(sd, tuple) else (self.gpu_of(sd) if sd is not None else None)
-            g_d = self.gpu_of(dd) if dd is not None else None
+            g_d = dev.gpu if dd is not None else None
             if g_s is not None and g_d is not None and g_s != g_d:
                 self.enable_peer(g_d, g_s)
-                N.call("hrt_copy_peer_async", stream.h, ctypes.c_void_p(dp), g_d,
-                       ctypes.c_void_p(sp), g_s, ctypes.c_uint64(size))
-            else:
-                N.call("hrt_copy_async", stream.h, ctypes.c_void_p(dp), ctypes.c_void_p(sp),
-                       ctypes.c_uint64(size))
-        token = stream.record(TokenKind.TRANSFER, dev.device_id)
+                peer = 1
+        # waits + copy + token in one native call (hrt_copy_ordered); GPU<->GPU
+        # copies up to 64 MiB run as an SM pull/push kernel (lower latency
+        # than the copy engine there), larger ones on the copy engine
+        waits = [t.token_id for t in (wait or ()) if t is not None and t._native]
+        tid = ctypes.c_uint64()
+        N.call("hrt_copy_ordered", stream.h, ctypes.c_void_p(dp), ctypes.c_void_p(sp),
+               ctypes.c_uint64(size), peer, (ctypes.c_uint64 * len(waits))(*waits) if waits else None,
+               len(waits), self.copy_method, ctypes.byref(tid))
+        token = CompletionToken(tid.value, TokenKind.TRANSFER, dev.device_id)
         self._tokens[token.token_id] = token
-        self.clock.track(token)
+        self.clock.track_pending(token)
         self.tracer.emit("transfer", device=dev.device_id, stream=stream.name, start=t0,
                          end=t0, size=size)
         return token

@@ -840,7 +840,11 @@ class JacobiSolver:
         n = len(host_ins)
         in_free = [None, None]     # scatter of the job that last used the input field
         out_free = [None, None]    # D2H of the job that last used the output field
-        hists = [np.zeros(steps, dtype=np.uint64) for _ in range(n)]
+        # residual histories land in pinned memory: a D2H into pageable
+        # memory blocks the host until it is done, which would hold back
+        # the next job's launches by a whole field download
+        hpin = PinnedBuffer(max(n * steps * 8, 8))
+        hists = [hpin.array(np.uint64)[j * steps:(j + 1) * steps] for j in range(n)]
         resid_free = [None, None]
 
         def issue_h2d(j: int):
@@ -894,7 +898,9 @@ class JacobiSolver:
         d2h.synchronize()
         comp.synchronize()
         self._check_error()
-        return [h.view(np.float64) if residual else np.zeros(0) for h in hists]
+        out = [h.view(np.float64).copy() if residual else np.zeros(0) for h in hists]
+        hpin.close()
+        return out
 
     def residual_bits(self) -> dict[int, int]:
         """device address of each GPU's residual history (uint64 bit patterns)."""

@@ -178,3 +178,49 @@ def test_sm_copy_kernel_bytes(push):
                ctypes.c_void_p(d_ptr), size)
         st_dst.synchronize()
         assert np.array_equal(out, data), size
+
+
+@pytest.mark.parametrize("method", [0, 1, 2])
+def test_copy_ordered_waits_and_bytes(method):
+    """hrt_copy_ordered (enqueue_transfer in one call): the copy runs after
+    its wait tokens — a producer on another stream writes the source first —
+    and moves exactly the bytes with the copy engine (0), the SM kernel (1)
+    or the automatic choice (2); retired wait tokens are skipped."""
+    import ctypes
+
+    from paper_2303_02543_b200 import _native as N
+    from paper_2303_02543_b200.devices import DevicePool, Stream
+
+    n = N.gpu_count()
+    src_gpu, dst_gpu = 0, (1 if n > 1 else 0)
+    if src_gpu != dst_gpu:
+        N.call("hrt_enable_peer_access", dst_gpu, src_gpu)
+        N.call("hrt_enable_peer_access", src_gpu, dst_gpu)
+    rng = np.random.default_rng(5)
+    for size in (16, 4096, (2 << 20) + 16, 3 << 20):
+        data = rng.integers(0, 256, size=size, dtype=np.uint8)
+        sp, dp = DevicePool(src_gpu, size + 4096), DevicePool(dst_gpu, size + 4096)
+        s_ptr, d_ptr = sp.alloc(size)[2], dp.alloc(size)[2]
+        st_src, st_dst = Stream(src_gpu), Stream(dst_gpu)
+        # producer: memset then upload on the source's stream, not synchronised
+        N.call("hrt_memset_async", st_src.h, ctypes.c_void_p(s_ptr), 0, ctypes.c_uint64(size))
+        N.call("hrt_copy_async", st_src.h, ctypes.c_void_p(s_ptr),
+               ctypes.c_void_p(data.ctypes.data), size)
+        prod = st_src.record()
+        done = ctypes.c_uint64()
+        # a retired token in the list (released) must be skipped
+        old = st_dst.record()
+        old.wait()
+        old_id = old.token_id
+        _ = old.status  # latches and releases the native token
+        waits = (ctypes.c_uint64 * 2)(prod.token_id, old_id)
+        N.call("hrt_copy_ordered", st_dst.h, ctypes.c_void_p(d_ptr), ctypes.c_void_p(s_ptr),
+               ctypes.c_uint64(size), int(src_gpu != dst_gpu), waits, 2, method,
+               ctypes.byref(done))
+        assert N.lib().hrt_token_wait(done) == 0
+        N.lib().hrt_token_release(done)
+        out = np.empty(size, np.uint8)
+        N.call("hrt_copy_async", st_dst.h, ctypes.c_void_p(out.ctypes.data),
+               ctypes.c_void_p(d_ptr), size)
+        st_dst.synchronize()
+        assert np.array_equal(out, data), (method, size)

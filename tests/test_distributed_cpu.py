@@ -14,6 +14,7 @@ import torch.multiprocessing as mp
 from paper_2303_02543_b200.jacobi import ChunkGrid, remote_ops
 
 CASES = [((32768, 32768, 1), (4, 4, 1)), ((32768, 32768, 1), (8, 4, 1)),
+         ((32768, 32768, 1), (64, 1, 1)), ((32768, 32768, 1), (8, 8, 1)),
          ((64, 64, 64), (2, 2, 2)), ((48, 40, 1), (6, 5, 1)), ((8, 8, 8), None)]
 
 
@@ -49,7 +50,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_remote_face_pairing_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
