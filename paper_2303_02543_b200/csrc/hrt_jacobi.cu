@@ -27,6 +27,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "hrt_common.cuh"
@@ -1014,11 +1015,23 @@ struct VolArgs {
     const VolPush* vpush;      // null: no fused push
 };
 
-constexpr int V_CW = 8;
+#ifndef HRT_V_CW
+#define HRT_V_CW 8        // consumer warps = y rows per volume tile
+#endif
+#ifndef HRT_V_STAGES
+#define HRT_V_STAGES 8    // ring stages (planes in flight per CTA)
+#endif
+#ifndef HRT_V_MINB
+#define HRT_V_MINB 4      // resident CTAs per SM the register budget targets
+#endif
+constexpr int V_CW = HRT_V_CW;
 constexpr int V_ZW = 64;               // z columns per tile
 constexpr int V_ZROW = V_ZW + 4;       // + k0-2, k0-1, k0+64, k0+65
 constexpr int V_ROWS = V_CW + 2;       // y rows per stage (with halo)
-constexpr int V_STAGES = 8;
+constexpr int V_STAGES = HRT_V_STAGES;
+// the ring lives in dynamic shared memory (more than the 48 KB static cap
+// for taller tiles / deeper rings)
+constexpr size_t V_SMEM = sizeof(double) * V_STAGES * V_ROWS * V_ZROW;
 
 // Producer for one volume tile: planes i0-1 .. i1+1, each stage = the tile's
 // V_CW+2 y-rows of z = k0-2 .. k0+65 (one bulk copy per row).
@@ -1157,9 +1170,10 @@ __device__ __forceinline__ void v_consume(const VolArgs& a, double (*ring)[V_ROW
 }
 
 template <bool RESID>
-__global__ void __launch_bounds__(32 * (V_CW + 1), 4)
+__global__ void __launch_bounds__(32 * (V_CW + 1), HRT_V_MINB)
 volume_update_tma_kernel(VolArgs a) {
-    __shared__ alignas(128) double ring[V_STAGES][V_ROWS][V_ZROW];
+    extern __shared__ __align__(128) unsigned char v_dyn_smem[];
+    auto ring = reinterpret_cast<double (*)[V_ROWS][V_ZROW]>(v_dyn_smem);
     __shared__ alignas(8) uint64_t full[V_STAGES], empty[V_STAGES];
     __shared__ double red[V_CW];
 
@@ -1239,9 +1253,10 @@ struct VolWaveArgs {
 };
 
 template <bool RESID>
-__global__ void __launch_bounds__(32 * (V_CW + 1), 4)
+__global__ void __launch_bounds__(32 * (V_CW + 1), HRT_V_MINB)
 volume_wave_kernel(VolWaveArgs wa) {
-    __shared__ alignas(128) double ring[V_STAGES][V_ROWS][V_ZROW];
+    extern __shared__ __align__(128) unsigned char v_dyn_smem[];
+    auto ring = reinterpret_cast<double (*)[V_ROWS][V_ZROW]>(v_dyn_smem);
     __shared__ alignas(8) uint64_t full[V_STAGES], empty[V_STAGES], tq_full[WAVE_TQ],
         tq_empty[WAVE_TQ];
     __shared__ long long tq[WAVE_TQ];
@@ -1879,9 +1894,9 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         const int64_t grid = (int64_t)p->nchunks * a.tiles_i * a.tiles_j * a.tiles_k;
         if (grid == 0) return HRT_OK;
         if (tma && resid)
-            volume_update_tma_kernel<true><<<(unsigned)grid, 32 * (V_CW + 1), 0, s>>>(a);
+            volume_update_tma_kernel<true><<<(unsigned)grid, 32 * (V_CW + 1), V_SMEM, s>>>(a);
         else if (tma)
-            volume_update_tma_kernel<false><<<(unsigned)grid, 32 * (V_CW + 1), 0, s>>>(a);
+            volume_update_tma_kernel<false><<<(unsigned)grid, 32 * (V_CW + 1), V_SMEM, s>>>(a);
         else
             volume_update_kernel<<<(unsigned)grid, dim3(VOL_TX, VOL_TY), 0, s>>>(a);
     }
@@ -1896,9 +1911,14 @@ static void carveout(K kernel) {
 }
 
 static void set_carveouts() {
-    static bool done = false;  // per process; the attribute is per function
-    if (done) return;
-    done = true;
+    // function attributes are per device context: once per GPU of the process
+    static std::mutex mu;
+    static uint64_t done = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (dev < 64 && (done >> dev) & 1) return;
+    if (dev < 64) done |= 1ull << dev;
 #define C4(G, R, CW)                                       \
     carveout(slab_update_tma4_kernel<G, R, CW, false>);   \
     carveout(slab_update_tma4_kernel<G, R, CW, true>)
@@ -1918,6 +1938,14 @@ static void set_carveouts() {
     carveout(volume_wave_kernel<true>);
     carveout(volume_wave_kernel<false>);
     carveout(volume_update_tma_kernel<false>);
+    cudaFuncSetAttribute(volume_update_tma_kernel<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V_SMEM);
+    cudaFuncSetAttribute(volume_update_tma_kernel<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V_SMEM);
+    cudaFuncSetAttribute(volume_wave_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)V_SMEM);
+    cudaFuncSetAttribute(volume_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)V_SMEM);
     cudaGetLastError();
 }
 
@@ -2058,8 +2086,8 @@ static int build_wave(Plan* p, int64_t ntiles) {
         int dev = 0, sms = 0, a = 0, b = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, volume_wave_kernel<true>, 32 * (V_CW + 1), 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, volume_wave_kernel<false>, 32 * (V_CW + 1), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, volume_wave_kernel<true>, 32 * (V_CW + 1), V_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, volume_wave_kernel<false>, 32 * (V_CW + 1), V_SMEM);
         G = std::min(a, b) * sms;
     } else {
         G = narrow ? wave_occupancy<2>(!p->nonneg) : wave_occupancy<4>(!p->nonneg);
@@ -2165,7 +2193,7 @@ static int launch_persist3(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     void* fn = resid_base ? (void*)volume_wave_kernel<true> : (void*)volume_wave_kernel<false>;
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid, T);
     void* args[] = {&wa};
-    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (V_CW + 1)), args, 0, s));
+    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (V_CW + 1)), args, V_SMEM, s));
     p->pbase += (unsigned)n;
     return HRT_OK;
 }
