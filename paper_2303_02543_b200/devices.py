@@ -695,8 +695,9 @@ class DeviceRegistry:
             g_s = sd[1] if isinstance(sd, tuple) else (self.gpu_of(sd) if sd is not None else None)
             g_d = dev.gpu if dd is not None else None
             if g_s is not None and g_d is not None and g_s != g_d:
-                self.enable_peer(g_d, g_s)
-                peer = 1
+                # SM copies need the mapping; without it the copy engine
+                # still moves the bytes (staged by the driver)
+                peer = 1 if self.enable_peer(g_d, g_s) else 0
         # waits + copy + token in one native call (hrt_copy_ordered); GPU<->GPU
         # copies up to 64 MiB run as an SM pull/push kernel (lower latency
         # than the copy engine there), larger ones on the copy engine
