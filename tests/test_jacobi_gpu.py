@@ -7,6 +7,8 @@ the checksum and the residual history."""
 import ctypes
 import hashlib
 
+import os
+
 import numpy as np
 import pytest
 
@@ -259,17 +261,25 @@ def test_persistent_guarded_division(hrt, oracle):
     assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
 
 
-def test_run_jobs_pipeline_matches_serial(hrt, oracle):
+@pytest.mark.parametrize("dom,grid,steps,njobs,sign", [
+    ((64, 96, 1), (2, 3, 1), 7, 4, 1.0),        # side arrays (even widths)
+    ((66, 99, 1), (2, 3, 1), 9, 3, 1.0),        # odd widths: in-buffer ghost columns
+    ((66, 99, 1), (2, 3, 1), 5, 1, -1.0),       # one job, guarded /6
+    ((512, 512, 1), (2, 2, 1), 70, 2, 1.0),     # 256-wide chunks, several row tiles
+    ((1024, 2048, 1), (4, 4, 1), 40, 3, 1.0),   # 512-wide chunks, multiple column tiles
+])
+def test_run_jobs_pipeline_matches_serial(hrt, oracle, dom, grid, steps, njobs, sign):
     """run_jobs (H2D/D2H of neighbouring jobs overlapped with compute on copy
     streams, double-buffered staging) gives, per job, exactly the field and
-    residual history of a serial upload/run/download."""
+    residual history of a serial upload/run/download, on random data (side
+    arrays and in-buffer ghost columns, narrow and wide chunks, guarded
+    division, one job and several)."""
     from paper_2303_02543_b200.devices import PinnedBuffer
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
-    dom, grid, steps = (64, 96, 1), (2, 3, 1), 7
     rng = np.random.default_rng(5)
-    inits = [np.zeros(dom), rng.random(dom), rng.random(dom) * 3.0, rng.random(dom)]
-    nbytes = 64 * 96 * 8
+    inits = [sign * rng.random(dom) * (1 + k) for k in range(njobs)]
+    nbytes = dom[0] * dom[1] * 8
     ins, outs = [], []
     for a in inits:
         b = PinnedBuffer(nbytes)
@@ -277,7 +287,7 @@ def test_run_jobs_pipeline_matches_serial(hrt, oracle):
         ins.append(b)
         outs.append(PinnedBuffer(nbytes))
     s = JacobiSolver(ChunkGrid(dom, grid=grid))
-    hists = s.run_jobs(ins, outs, steps, residual=True, nonneg=True)
+    hists = s.run_jobs(ins, outs, steps, residual=True, nonneg=sign > 0)
     for k, a in enumerate(inits):
         ref = oracle.jacobi_reference(dom, steps, initial=a)
         got = outs[k].array(np.float64, dom)
