@@ -297,6 +297,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         }
     }
 }
+// A waiter that has nothing else to do (the producer thread when the ring is
+// full): try_wait with a suspend-time hint parks the thread in hardware
+// until the phase completes instead of spinning on issue slots the
+// consumer warps need.
+__device__ __forceinline__ bool mbar_try_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    unsigned long long t0 = 0;
+    while (!mbar_try_sleep(bar, parity)) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > 20000000000ULL) __trap();
+    }
+}
 __device__ __forceinline__ void tma_row_load(void* dst, const void* src, uint32_t bytes,
                                              uint64_t* bar) {
     asm volatile(
@@ -980,6 +1004,342 @@ slab_wave_kernel(WaveArgs wa) {
                 if (!HRT_WAVE_NOFENCE) __threadfence();
                 st_release_gpu_u32(wa.done + tile, v);
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Two steps per pass (temporal blocking) for slabs of one GPU.  A tile of
+// fused step k reads u(t) once — its rows i0-2 .. i1+2 and columns
+// j0-2 .. j0+W+1, straight from whichever chunk owns them (the 3 x 3 chunk
+// neighbourhood: no ghost planes, no pushes) — computes u(t+1) on the tile
+// plus a one-cell rim in registers (cells outside the domain keep the
+// Dirichlet value, as the reference's ghost shell does), then u(t+2) on the
+// tile, and writes only u(t+2): 8 B of HBM per lattice update instead of 16.
+// Every value is produced by the same IEEE operations in the reference's
+// order (the rim cells exactly as their owner computes them), so the field
+// and both residuals per pass stay bitwise identical.  Dependencies: a tile
+// of fused step k needs its 3 x 3 tile neighbourhood done with step k-1
+// (RAW on u(t), and WAR on the buffer it overwrites, which those tiles read
+// as rim); counters count steps (2 per pass).
+
+struct Wave2Args {
+    const ChunkBufs* chunks;
+    const int* nb9;              // [nchunks][9] chunk at (di, dj), (di+1)*3+(dj+1); -1 outside
+    unsigned int* done;          // [T] steps completed per tile (absolute)
+    unsigned long long* ticket;
+    unsigned int base;           // every done[] at launch
+    int nfused;                  // passes (2 steps each)
+    int parity0;                 // buffer holding u(first)
+    int64_t ntiles, ex, ey, sx, origin, rows, tiles_r, tiles_c;
+    unsigned long long* resid;   // nullable: 2 * nfused slots
+    const double* ones;          // a BOUNDARY row source for rows outside the domain
+    unsigned long long timeout_ns;
+    int* err;
+    double zghost;
+};
+
+// rows i0-2 .. i1+2 of u(t) into the ring: the span j0-2 .. j0+W+1 (or the
+// owning chunk's part of it at a chunk's west/east edge, plus 16 bytes from
+// the west/east neighbour chunk's same row), BOUNDARY where outside.
+template <int CW, int STAGES>
+__device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[128 * CW + 4],
+                                           uint64_t* full, uint64_t* empty, int& s,
+                                           uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
+                                           int64_t i1, int parity) {
+    constexpr int W = 128 * CW;
+    const int64_t j0 = 1 + cb * W;
+    const int64_t last = min(j0 + W - 1, a.ey);
+    const int* nb = a.nb9 + 9 * c;
+    const bool wedge = cb == 0, eedge = last == a.ey;
+    const int64_t lo = wedge ? 1 : j0 - 2;
+    const int64_t hi = eedge ? a.ey : last + 2;
+    const uint32_t mbytes = (uint32_t)((hi - lo + 1) * 8);  // even count: ey even
+    const int mpos = (int)(lo - (j0 - 2));
+    const int epos = (int)(last - j0 + 3);
+    const int nrows = (int)(i1 - i0 + 5);
+    for (int q = 0; q < nrows; ++q) {
+        const int64_t r = i0 - 2 + q;
+        const int di = r < 1 ? -1 : (r > a.ex ? 1 : 0);
+        const int64_t rr = r - di * a.ex;
+        const int cr = nb[(di + 1) * 3 + 1];
+        mbar_wait_sleep(&empty[s], ph ^ 1);
+        uint32_t bytes = mbytes;
+        const double* msrc = cr >= 0 ? a.chunks[cr].b[parity] + a.origin + rr * a.sx + lo : a.ones;
+        const double* wsrc = nullptr;
+        const double* esrc = nullptr;
+        if (wedge) {
+            const int cw = cr >= 0 ? nb[(di + 1) * 3 + 0] : -1;
+            if (cw >= 0) {
+                wsrc = a.chunks[cw].b[parity] + a.origin + rr * a.sx + (a.ey - 1);
+                bytes += 16;
+            } else {
+                ring[s][0] = HRT_BOUNDARY;
+                ring[s][1] = HRT_BOUNDARY;
+            }
+        }
+        if (eedge) {
+            const int ce = cr >= 0 ? nb[(di + 1) * 3 + 2] : -1;
+            if (ce >= 0) {
+                esrc = a.chunks[ce].b[parity] + a.origin + rr * a.sx + 1;
+                bytes += 16;
+            } else {
+                ring[s][epos] = HRT_BOUNDARY;
+                ring[s][epos + 1] = HRT_BOUNDARY;
+            }
+        }
+        mbar_expect_tx(&full[s], bytes);
+        tma_row_load(&ring[s][mpos], msrc, mbytes, &full[s]);
+        if (wsrc) tma_row_load(&ring[s][0], wsrc, 16, &full[s]);
+        if (esrc) tma_row_load(&ring[s][epos], esrc, 16, &full[s]);
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+        }
+    }
+}
+
+// u(t+1) on rows i0-1 .. i1+1, columns j-1 .. j+4 of this thread (j = its
+// first column), then u(t+2) on rows i0 .. i1, columns j .. j+3 -> buffer
+// parity^1.  r1 / r2: max |u(t+1)-u(t)| / |u(t+2)-u(t+1)| over own cells.
+// The row loop is unrolled by three with the u(t) and u(t+1) row windows
+// rotating through three register arrays each (no moves); cells outside the
+// domain are masked only in tiles that touch it (a uniform branch).
+template <bool GUARD, bool RESID, int CW, int STAGES>
+__device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[128 * CW + 4],
+                                           uint64_t* full, uint64_t* empty, int& s,
+                                           uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
+                                           int64_t i1, int parity, double& r1, double& r2) {
+    constexpr int W = 128 * CW;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int64_t j0 = 1 + cb * W;
+    const int64_t j = j0 + 4 * tid;
+    const int64_t nv64 = a.ey - j + 1;
+    const int nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);
+    const int p = 4 * tid;  // ring position of column j-2
+    const int nrows = (int)(i1 - i0 + 5);
+    const int* nb = a.nb9 + 9 * c;
+    const bool out_n = nb[1] < 0, out_s = nb[7] < 0;
+    // u(t+1) columns j-1+m (m = 0..5) outside the domain keep BOUNDARY
+    unsigned cghost = 0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+        const int64_t cc = j - 1 + m;
+        if ((cc < 1 && nb[3] < 0) || (cc > a.ey && nb[5] < 0)) cghost |= 1u << m;
+    }
+    // does any u(t+1) value of this tile fall outside the domain?
+    const bool mask = __any_sync(0xffffffffu, cghost != 0) || (out_n && i0 <= 1) ||
+                      (out_s && i1 >= a.ex);
+    double* __restrict__ wr = a.chunks[c].b[parity ^ 1] + a.origin + i0 * a.sx + j;
+    const double zg = a.zghost;
+
+    auto take = [&](double (&v)[8]) {
+        mbar_wait(&full[s], ph);
+        const double2 v01 = *reinterpret_cast<const double2*>(&ring[s][p]);
+        const double2 v23 = *reinterpret_cast<const double2*>(&ring[s][p + 2]);
+        const double2 v45 = *reinterpret_cast<const double2*>(&ring[s][p + 4]);
+        const double2 v67 = *reinterpret_cast<const double2*>(&ring[s][p + 6]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+        }
+        v[0] = v01.x; v[1] = v01.y; v[2] = v23.x; v[3] = v23.y;
+        v[4] = v45.x; v[5] = v45.y; v[6] = v67.x; v[7] = v67.y;
+    };
+
+    // one ring row q: u(t) row r+1 arrives in `dn`; u(t+1) row r (r = i0-3+q)
+    // goes into `u1n` (the slot of row r-3); u(t+2) row r-1 from u1 rows
+    // r-2 (`u1a`), r-1 (`u1b`), r (`u1n`)
+    auto row = [&](const double (&up)[8], const double (&mid)[8], double (&dn)[8],
+                   const double (&u1a)[6], const double (&u1b)[6], double (&u1n)[6], int q) {
+        take(dn);
+        const int64_t r = i0 - 3 + q;
+#pragma unroll
+        for (int m = 0; m < 6; ++m)
+            u1n[m] = div6_t<GUARD>(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], zg, zg));
+        if (mask) {
+            const bool rghost = (r < 1 && out_n) || (r > a.ex && out_s);
+#pragma unroll
+            for (int m = 0; m < 6; ++m)
+                if (rghost || ((cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
+        }
+        if (RESID && r >= i0 && r <= i1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < nv) r1 = fmax(r1, fabs(__dsub_rn(u1n[k + 1], mid[k + 2])));
+        }
+        if (q >= 4) {
+            double o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                o[k] = div6_t<GUARD>(sum6(u1a[k + 1], u1n[k + 1], u1b[k], u1b[k + 2], zg, zg));
+            if (nv == 4) {
+                *reinterpret_cast<double2*>(wr) = make_double2(o[0], o[1]);
+                *reinterpret_cast<double2*>(wr + 2) = make_double2(o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nv) wr[k] = o[k];
+            }
+            if (RESID) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k < nv) r2 = fmax(r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+            }
+            wr += a.sx;
+        }
+    };
+
+    double x0[8], x1[8], x2[8];  // u(t) rows, rotating
+    double y0[6], y1[6], y2[6];  // u(t+1) rows, rotating
+    take(x0);                    // row i0-2
+    take(x1);                    // row i0-1
+    int q = 2;
+    for (; q + 2 < nrows; q += 3) {
+        row(x0, x1, x2, y1, y2, y0, q);
+        row(x1, x2, x0, y2, y0, y1, q + 1);
+        row(x2, x0, x1, y0, y1, y2, q + 2);
+    }
+    if (q < nrows) row(x0, x1, x2, y1, y2, y0, q);
+    if (q + 1 < nrows) row(x1, x2, x0, y2, y0, y1, q + 1);
+}
+
+#ifndef HRT_W2_MINB4
+#define HRT_W2_MINB4 3   // resident CTAs/SM the 4-warp two-step kernel's registers target
+#endif
+#ifndef HRT_W2_MINB2
+#define HRT_W2_MINB2 5   // same for the 2-warp (256-column) instance
+#endif
+template <bool GUARD, bool RESID, int CW, int STAGES = T4_STAGES>
+__global__ void __launch_bounds__(32 * (CW + 1), CW == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
+slab_wave2_kernel(Wave2Args wa) {
+    __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
+    __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
+        tq_empty[WAVE_TQ];
+    __shared__ long long tq[WAVE_TQ];
+    __shared__ double red[2][CW];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int64_t T = wa.ntiles;
+    const int64_t tr = wa.tiles_r, tc = wa.tiles_c;
+    const int64_t per_chunk = tr * tc;
+    const long long total = (long long)T * wa.nfused;
+
+    if (tid == 0) {
+        for (int k = 0; k < STAGES; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], CW);
+        }
+        for (int k = 0; k < WAVE_TQ; ++k) {
+            mbar_init(&tq_full[k], 1);
+            mbar_init(&tq_empty[k], CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    int s = 0;
+    uint32_t ph = 0;
+    if (warp == CW) {
+        if (lane != 0) return;
+        bool dead = false;
+        int slot = 0;
+        uint32_t tph = 0;
+        for (;;) {
+            const long long t = (long long)atomicAdd(wa.ticket, 1ull);
+            mbar_wait(&tq_empty[slot], tph ^ 1);
+            tq[slot] = t < total ? t : -1;
+            mbar_arrive(&tq_full[slot]);
+            if (++slot == WAVE_TQ) {
+                slot = 0;
+                tph ^= 1;
+            }
+            if (t >= total) break;
+            const int k = (int)(t / T);
+            const int64_t tile = t - (long long)k * T;
+            const int64_t c = tile / per_chunk;
+            const int64_t rem = tile - c * per_chunk;
+            const int64_t rb = rem / tc;
+            const int64_t cb = rem - rb * tc;
+            if (!dead) {
+                // the 3 x 3 tile neighbourhood must be done with step base+2k
+                const unsigned need = wa.base + 2u * (unsigned)k;
+                const int* nb = wa.nb9 + 9 * c;
+                const unsigned int* q[9];
+                bool sys[9];
+#pragma unroll
+                for (int d = 0; d < 9; ++d) {
+                    const int64_t r2 = rb + d / 3 - 1, c2 = cb + d % 3 - 1;
+                    const int ci = r2 < 0 ? -1 : (r2 >= tr ? 1 : 0);
+                    const int cj = c2 < 0 ? -1 : (c2 >= tc ? 1 : 0);
+                    const int ch = nb[(ci + 1) * 3 + (cj + 1)];
+                    q[d] = ch < 0 ? nullptr
+                                  : wa.done + (int64_t)ch * per_chunk + (r2 - ci * tr) * tc +
+                                        (c2 - cj * tc);
+                    sys[d] = false;
+                }
+                dead = !wait_counters<9>(q, sys, need, wa.timeout_ns, wa.err);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            const int64_t i0 = 1 + rb * wa.rows;
+            const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
+            w2_produce<CW, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
+                                   (wa.parity0 + k) & 1);
+        }
+        return;
+    }
+    int slot = 0;
+    uint32_t tph = 0;
+    for (;;) {
+        mbar_wait(&tq_full[slot], tph);
+        const long long t = tq[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tq_empty[slot]);
+        if (++slot == WAVE_TQ) {
+            slot = 0;
+            tph ^= 1;
+        }
+        if (t < 0) break;
+        const int k = (int)(t / T);
+        const int64_t tile = t - (long long)k * T;
+        const int64_t c = tile / per_chunk;
+        const int64_t rem = tile - c * per_chunk;
+        const int64_t rb = rem / tc;
+        const int64_t cb = rem - rb * tc;
+        const int64_t i0 = 1 + rb * wa.rows;
+        const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
+        double r1 = 0.0, r2 = 0.0;
+        w2_consume<GUARD, RESID, CW, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
+                                             (wa.parity0 + k) & 1, r1, r2);
+        if (RESID && wa.resid) {
+            r1 = warp_max(r1);
+            r2 = warp_max(r2);
+            if (lane == 0) {
+                red[0][warp] = r1;
+                red[1][warp] = r2;
+            }
+        }
+        if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
+        if (tid == 0) {
+            if (RESID && wa.resid) {
+                double m1 = red[0][0], m2 = red[1][0];
+#pragma unroll
+                for (int w = 1; w < CW; ++w) {
+                    m1 = fmax(m1, red[0][w]);
+                    m2 = fmax(m2, red[1][w]);
+                }
+                resid_max(wa.resid + 2 * k, m1);
+                resid_max(wa.resid + 2 * k + 1, m2);
+            }
+            if (!HRT_WAVE_NOFENCE) __threadfence();
+            st_release_gpu_u32(wa.done + tile, wa.base + 2u * (unsigned)k + 2u);
         }
     }
 }
@@ -1779,6 +2139,18 @@ struct Plan {
     // threads); HRT_NARROW=0 forces the 4-warp ones (experiments)
     bool narrow_ok = true;
     bool narrow_chunk() const { return narrow_ok && L.ext[1] <= 256; }
+    // two steps per pass (slab_wave2_kernel): one GPU, no faces to other
+    // processes; HRT_FUSE2=0 turns it off
+    bool fuse2 = true;
+    int* d_nb9 = nullptr;          // [nchunks][9] 3 x 3 chunk neighbourhood
+    double* d_ones = nullptr;      // BOUNDARY row (rows outside the domain)
+    int pgrid2 = 0;                // resident CTA slots of slab_wave2_kernel
+    int64_t pkey2 = -1;
+    bool fuse2_on() const {
+        return fuse2 && persist_on() && L.ndim == 2 && !wave_ipc && remote.empty() && !ipc &&
+               L.ext[0] >= 2 && L.ext[1] >= 2 && L.ext[1] % 2 == 0 && rows >= 2 &&
+               L.ext[0] % rows != 1 && (int64_t)nbr.size() == 4 * (int64_t)nchunks;
+    }
     bool persist_on() const {
         return persist && any_push() && !nbr.empty() && (wave_ipc || (remote.empty() && !ipc));
     }
@@ -1933,6 +2305,14 @@ static void set_carveouts() {
     carveout(slab_wave_kernel<true, false, 2>);
     carveout(slab_wave_kernel<false, true, 2>);
     carveout(slab_wave_kernel<false, false, 2>);
+    carveout(slab_wave2_kernel<true, true, 4>);
+    carveout(slab_wave2_kernel<true, false, 4>);
+    carveout(slab_wave2_kernel<false, true, 4>);
+    carveout(slab_wave2_kernel<false, false, 4>);
+    carveout(slab_wave2_kernel<true, true, 2>);
+    carveout(slab_wave2_kernel<true, false, 2>);
+    carveout(slab_wave2_kernel<false, true, 2>);
+    carveout(slab_wave2_kernel<false, false, 2>);
     carveout(slab_update_tma_kernel);
     carveout(volume_update_tma_kernel<true>);
     carveout(volume_wave_kernel<true>);
@@ -2198,9 +2578,141 @@ static int launch_persist3(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     return HRT_OK;
 }
 
-// steps [first, first+n) in one persistent wavefront launch
+static int launch_persist1(Plan* p, cudaStream_t s, int64_t first, int64_t n,
+                           unsigned long long* resid_base);
+
+template <int CW>
+static int wave2_occupancy(bool guard) {
+    int dev = 0, sms = 0, a = 0, b = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (guard) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW>,
+                                                      32 * (CW + 1), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW>,
+                                                      32 * (CW + 1), 0);
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW>,
+                                                      32 * (CW + 1), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW>,
+                                                      32 * (CW + 1), 0);
+    }
+    return std::min(a, b) * sms;
+}
+
+// nf passes (2 steps each) from step `first` in one slab_wave2_kernel launch
+static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
+                        unsigned long long* resid_base) {
+    if (nf <= 0) return HRT_OK;
+    const bool narrow = p->narrow_chunk();
+    int64_t tc = 0;
+    const int64_t T = wave_tiles(p, &tc);
+    if (T == 0) return HRT_OK;
+    int rc;
+    if (p->pgrid == 0 || p->ptiles != T || p->pkey != T * 4 + (p->nonneg ? 1 : 0)) {
+        HRT_CUDA(cudaStreamSynchronize(s));  // counters reset: nothing may be in flight
+        rc = build_wave(p, T);
+        if (rc) return rc;
+    }
+    if (!p->d_nb9) {
+        std::vector<int> nb9(9 * (size_t)p->nchunks, -1);
+        auto at = [&](int c, int f) { return c < 0 ? -1 : p->nbr[4 * (size_t)c + f]; };
+        for (int c = 0; c < p->nchunks; ++c) {
+            int* o = nb9.data() + 9 * (size_t)c;
+            const int n = at(c, 0), so = at(c, 1);
+            o[4] = c;
+            o[1] = n;
+            o[7] = so;
+            o[3] = at(c, 2);
+            o[5] = at(c, 3);
+            o[0] = at(n, 2);
+            o[2] = at(n, 3);
+            o[6] = at(so, 2);
+            o[8] = at(so, 3);
+        }
+        HRT_CUDA(cudaMalloc(&p->d_nb9, sizeof(int) * nb9.size()));
+        HRT_CUDA(cudaMemcpy(p->d_nb9, nb9.data(), sizeof(int) * nb9.size(),
+                            cudaMemcpyHostToDevice));
+    }
+    if (!p->d_ones) {
+        std::vector<double> ones(T4_COLS + 8, HRT_BOUNDARY);
+        HRT_CUDA(cudaMalloc(&p->d_ones, sizeof(double) * ones.size()));
+        HRT_CUDA(cudaMemcpy(p->d_ones, ones.data(), sizeof(double) * ones.size(),
+                            cudaMemcpyHostToDevice));
+    }
+    const int64_t key2 = T * 4 + (p->nonneg ? 1 : 0);
+    if (p->pgrid2 == 0 || p->pkey2 != key2) {
+        p->pgrid2 = narrow ? wave2_occupancy<2>(!p->nonneg) : wave2_occupancy<4>(!p->nonneg);
+        HRT_CUDA(cudaGetLastError());
+        if (p->pgrid2 <= 0) {
+            set_error("two-step kernel: no resident CTA slots");
+            return HRT_E_CUDA;
+        }
+        p->pkey2 = key2;
+    }
+    HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
+    const hrt_chunk_layout_t& L = p->L;
+    Wave2Args wa{};
+    wa.chunks = p->d_chunks;
+    wa.nb9 = p->d_nb9;
+    wa.done = p->d_pdone;
+    wa.ticket = p->d_pticket;
+    wa.base = p->pbase;
+    wa.nfused = (int)nf;
+    wa.parity0 = (int)(first & 1);
+    wa.ntiles = T;
+    wa.ex = L.ext[0];
+    wa.ey = L.ext[1];
+    wa.sx = L.stride[0];
+    wa.origin = L.origin;
+    wa.rows = p->rows;
+    wa.tiles_r = (L.ext[0] + p->rows - 1) / p->rows;
+    wa.tiles_c = tc;
+    wa.resid = resid_base ? resid_base + first : nullptr;
+    wa.ones = p->d_ones;
+    wa.timeout_ns = p->persist_timeout_ns;
+    wa.err = p->d_err;
+    wa.zghost = HRT_BOUNDARY;
+    const bool guard = !p->nonneg, res = resid_base != nullptr;
+    void* fn;
+    int threads;
+#define WK2(G, R, CW) (void*)slab_wave2_kernel<G, R, CW>
+    if (narrow) {
+        fn = guard ? (res ? WK2(true, true, 2) : WK2(true, false, 2))
+                   : (res ? WK2(false, true, 2) : WK2(false, false, 2));
+        threads = 96;
+    } else {
+        fn = guard ? (res ? WK2(true, true, 4) : WK2(true, false, 4))
+                   : (res ? WK2(false, true, 4) : WK2(false, false, 4));
+        threads = 160;
+    }
+#undef WK2
+    const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid2, T);
+    void* args[] = {&wa};
+    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3((unsigned)threads), args, 0, s));
+    p->pbase += 2u * (unsigned)nf;
+    p->ghosts_ready = false;  // passes read neighbours in place; ghost planes went stale
+    return HRT_OK;
+}
+
+// steps [first, first+n): on a single-GPU slab plan, passes of two steps
+// (after n mod 4 single steps, so the result lands in the buffer of parity
+// (first+n) mod 2 like single steps); otherwise one wavefront launch
 static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                           unsigned long long* resid_base) {
+    if (n <= 0) return HRT_OK;
+    if (p->fuse2_on() && n >= 4) {
+        const int64_t nf = (n / 4) * 2, nr = n - 2 * nf;
+        int rc = nr ? launch_persist1(p, s, first, nr, resid_base) : HRT_OK;
+        if (rc) return rc;
+        return launch_fused(p, s, first + nr, nf, resid_base);
+    }
+    return launch_persist1(p, s, first, n, resid_base);
+}
+
+// steps [first, first+n) in one persistent wavefront launch
+static int launch_persist1(Plan* p, cudaStream_t s, int64_t first, int64_t n,
+                           unsigned long long* resid_base) {
     if (n <= 0) return HRT_OK;
     const int parity0 = (int)(first & 1);
     int rc = prime_ghosts(p, s, parity0);
@@ -2367,6 +2879,7 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     // GLUPS; 128 planes leaves too few tiles (319)
     p->rows = 64;
     if (const char* e = getenv("HRT_NARROW")) p->narrow_ok = e[0] != '0';
+    if (const char* e = getenv("HRT_FUSE2")) p->fuse2 = e[0] != '0';
     *plan = p;
     return HRT_OK;
 }
@@ -2615,6 +3128,8 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     p->nbr.assign(nbr4, nbr4 + nf * p->nchunks);
     cudaFree(p->d_pnbr);
     p->d_pnbr = nullptr;
+    cudaFree(p->d_nb9);
+    p->d_nb9 = nullptr;
     p->persist = true;
     p->pgrid = 0;  // rebuilt at the next launch
     if (timeout_ns) p->persist_timeout_ns = timeout_ns;
@@ -2897,6 +3412,8 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_rnbr);
     cudaFree(p->d_rpeer);
     cudaFree(p->d_peer_done);
+    cudaFree(p->d_nb9);
+    cudaFree(p->d_ones);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
