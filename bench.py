@@ -254,27 +254,40 @@ def run_ours(args):
     # roofline of the dominant kernel: per-launch algorithmic bytes / average
     # launch duration (CUDA events around every launch on the solver stream).
     # Persistent mode runs all iterations of a job in one wavefront launch.
+    # Two-step passes (slab_wave2_kernel) read u and write u'' once per TWO
+    # updates: their algorithmic bytes are 8 per lattice update; the naive
+    # one-step algorithm's 16 B/update is reported beside it.
     persistent = bool(getattr(solver, "persistent", False))
+    two_step = persistent and iters >= 4 and solver.two_step
     launches_per_job = 1 if persistent else iters
     steps_per_launch = iters // launches_per_job
     avg_upd_ms = upd / (args.steps * launches_per_job)
-    bytes_per_launch = BYTES_PER_UPDATE * my_cells * steps_per_launch
+    bytes_per_update = BYTES_PER_UPDATE // 2 if two_step else BYTES_PER_UPDATE
+    bytes_per_launch = bytes_per_update * my_cells * steps_per_launch
     achieved = bytes_per_launch / (avg_upd_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     cw = 2 if grid.ext[1] <= 256 else 4
-    kname = (f"slab_wave_kernel<false,true,{cw}>" if persistent else
+    kname = (f"slab_wave2_kernel<false,true,{cw}>" if two_step else
+             f"slab_wave_kernel<false,true,{cw}>" if persistent else
              {None: f"slab_update_tma4_kernel<false,true,{cw},push>",
               2: f"slab_update_tma4_kernel<false,true,{cw},push>",
               1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant])
     if grid.slab is False:
         kname = "volume_update_tma_kernel<true>"
-    traffic = args.traffic if args.traffic is not None else _recorded_traffic(wl["name"], world)
+    traffic = (args.traffic if args.traffic is not None else
+               _recorded_traffic(wl["name"] + ("_two_step" if two_step else ""), world))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
                 "traffic": traffic * steps_per_launch if traffic else None,
                 "kernel": kname, "steps_per_launch": steps_per_launch,
                 "bytes_per_launch": bytes_per_launch,
                 "avg_launch_ms": round(avg_upd_ms, 5), "peak_source": peak_src,
+                "bytes_per_update": bytes_per_update,
+                "one_step_equivalent": {"bytes_per_update": BYTES_PER_UPDATE,
+                                        "achieved": round(achieved * BYTES_PER_UPDATE
+                                                          / bytes_per_update, 1),
+                                        "frac": round(achieved * BYTES_PER_UPDATE
+                                                      / bytes_per_update / peak, 4)},
                 "update_share_of_step": round(upd / tot, 4) if tot else None,
                 "halo_share_of_step": round(halo / tot, 4) if tot else None}
 

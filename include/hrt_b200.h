@@ -231,6 +231,15 @@ int hrt_jacobi_plan_wave_counters(void *plan, uint64_t *ptr, int64_t *ntiles);
  * peer's plan; peer_done = each peer's counters mapped here. */
 int hrt_jacobi_plan_set_wave_ipc(void *plan, const int32_t *rpeer4, const int32_t *rnbr4,
                                  const uint64_t *peer_done, int n_peers, uint64_t timeout_ns);
+/* Two steps per pass across processes (slab_wave2_kernel reads a 2-cell rim
+ * straight from the neighbour's chunk): per chunk and face N,S,W,E the
+ * neighbour chunk's two buffers (bufs8, mapped here), the base of its
+ * rank's tile counters (cnt4, mapped; 0 = not another process) and its
+ * index in that rank's plan.  Only row faces qualify; otherwise a no-op. */
+int hrt_jacobi_plan_set_wave2_remote(void *plan, const uint64_t *bufs8, const uint64_t *cnt4,
+                                     const int32_t *idx4);
+/* *on = 1 when persistent runs of >= 4 steps use two-step passes. */
+int hrt_jacobi_plan_two_step(void *plan, int *on);
 /* Synchronises; *err = 0 ok, 1 IPC edge wait timed out, 2 persistent
  * dependency wait timed out (results void). */
 int hrt_jacobi_plan_error(void *plan, int *err);

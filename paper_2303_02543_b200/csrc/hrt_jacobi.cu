@@ -1023,9 +1023,18 @@ slab_wave_kernel(WaveArgs wa) {
 // (RAW on u(t), and WAR on the buffer it overwrites, which those tiles read
 // as rim); counters count steps (2 per pass).
 
+// The 3 x 3 chunk neighbourhood of a chunk, (di+1)*3+(dj+1): the buffers
+// (this process's, or another process's mapped over CUDA IPC) and the base
+// of that chunk's tile counters; null outside the domain.
+struct Nbr9 {
+    double* b[9][2];
+    unsigned int* cnt[9];
+    unsigned int sysmask;        // bit d: counters in another process (system scope)
+    unsigned int pad_;
+};
+
 struct Wave2Args {
-    const ChunkBufs* chunks;
-    const int* nb9;              // [nchunks][9] chunk at (di, dj), (di+1)*3+(dj+1); -1 outside
+    const Nbr9* n9;              // [nchunks]
     unsigned int* done;          // [T] steps completed per tile (absolute)
     unsigned long long* ticket;
     unsigned int base;           // every done[] at launch
@@ -1050,7 +1059,7 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[12
     constexpr int W = 128 * CW;
     const int64_t j0 = 1 + cb * W;
     const int64_t last = min(j0 + W - 1, a.ey);
-    const int* nb = a.nb9 + 9 * c;
+    const Nbr9& n9 = a.n9[c];
     const bool wedge = cb == 0, eedge = last == a.ey;
     const int64_t lo = wedge ? 1 : j0 - 2;
     const int64_t hi = eedge ? a.ey : last + 2;
@@ -1062,16 +1071,16 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[12
         const int64_t r = i0 - 2 + q;
         const int di = r < 1 ? -1 : (r > a.ex ? 1 : 0);
         const int64_t rr = r - di * a.ex;
-        const int cr = nb[(di + 1) * 3 + 1];
+        const double* br = n9.b[(di + 1) * 3 + 1][parity];
         mbar_wait_sleep(&empty[s], ph ^ 1);
         uint32_t bytes = mbytes;
-        const double* msrc = cr >= 0 ? a.chunks[cr].b[parity] + a.origin + rr * a.sx + lo : a.ones;
+        const double* msrc = br ? br + a.origin + rr * a.sx + lo : a.ones;
         const double* wsrc = nullptr;
         const double* esrc = nullptr;
         if (wedge) {
-            const int cw = cr >= 0 ? nb[(di + 1) * 3 + 0] : -1;
-            if (cw >= 0) {
-                wsrc = a.chunks[cw].b[parity] + a.origin + rr * a.sx + (a.ey - 1);
+            const double* bw = br ? n9.b[(di + 1) * 3 + 0][parity] : nullptr;
+            if (bw) {
+                wsrc = bw + a.origin + rr * a.sx + (a.ey - 1);
                 bytes += 16;
             } else {
                 ring[s][0] = HRT_BOUNDARY;
@@ -1079,9 +1088,9 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[12
             }
         }
         if (eedge) {
-            const int ce = cr >= 0 ? nb[(di + 1) * 3 + 2] : -1;
-            if (ce >= 0) {
-                esrc = a.chunks[ce].b[parity] + a.origin + rr * a.sx + 1;
+            const double* be = br ? n9.b[(di + 1) * 3 + 2][parity] : nullptr;
+            if (be) {
+                esrc = be + a.origin + rr * a.sx + 1;
                 bytes += 16;
             } else {
                 ring[s][epos] = HRT_BOUNDARY;
@@ -1119,19 +1128,20 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[12
     const int nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);
     const int p = 4 * tid;  // ring position of column j-2
     const int nrows = (int)(i1 - i0 + 5);
-    const int* nb = a.nb9 + 9 * c;
-    const bool out_n = nb[1] < 0, out_s = nb[7] < 0;
+    const Nbr9& n9 = a.n9[c];
+    const bool out_n = !n9.b[1][0], out_s = !n9.b[7][0];
+    const bool out_w = !n9.b[3][0], out_e = !n9.b[5][0];
     // u(t+1) columns j-1+m (m = 0..5) outside the domain keep BOUNDARY
     unsigned cghost = 0;
 #pragma unroll
     for (int m = 0; m < 6; ++m) {
         const int64_t cc = j - 1 + m;
-        if ((cc < 1 && nb[3] < 0) || (cc > a.ey && nb[5] < 0)) cghost |= 1u << m;
+        if ((cc < 1 && out_w) || (cc > a.ey && out_e)) cghost |= 1u << m;
     }
     // does any u(t+1) value of this tile fall outside the domain?
     const bool mask = __any_sync(0xffffffffu, cghost != 0) || (out_n && i0 <= 1) ||
                       (out_s && i1 >= a.ex);
-    double* __restrict__ wr = a.chunks[c].b[parity ^ 1] + a.origin + i0 * a.sx + j;
+    double* __restrict__ wr = n9.b[4][parity ^ 1] + a.origin + i0 * a.sx + j;
     const double zg = a.zghost;
 
     auto take = [&](double (&v)[8]) {
@@ -1270,7 +1280,7 @@ slab_wave2_kernel(Wave2Args wa) {
             if (!dead) {
                 // the 3 x 3 tile neighbourhood must be done with step base+2k
                 const unsigned need = wa.base + 2u * (unsigned)k;
-                const int* nb = wa.nb9 + 9 * c;
+                const Nbr9& n9 = wa.n9[c];
                 const unsigned int* q[9];
                 bool sys[9];
 #pragma unroll
@@ -1278,11 +1288,10 @@ slab_wave2_kernel(Wave2Args wa) {
                     const int64_t r2 = rb + d / 3 - 1, c2 = cb + d % 3 - 1;
                     const int ci = r2 < 0 ? -1 : (r2 >= tr ? 1 : 0);
                     const int cj = c2 < 0 ? -1 : (c2 >= tc ? 1 : 0);
-                    const int ch = nb[(ci + 1) * 3 + (cj + 1)];
-                    q[d] = ch < 0 ? nullptr
-                                  : wa.done + (int64_t)ch * per_chunk + (r2 - ci * tr) * tc +
-                                        (c2 - cj * tc);
-                    sys[d] = false;
+                    const int e = (ci + 1) * 3 + (cj + 1);
+                    const unsigned int* base = n9.cnt[e];
+                    q[d] = base ? base + (r2 - ci * tr) * tc + (c2 - cj * tc) : nullptr;
+                    sys[d] = (n9.sysmask >> e) & 1u;
                 }
                 dead = !wait_counters<9>(q, sys, need, wa.timeout_ns, wa.err);
                 asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1325,7 +1334,13 @@ slab_wave2_kernel(Wave2Args wa) {
                 red[1][warp] = r2;
             }
         }
+        // a tile another process reads as rim (chunk edge facing it): its
+        // stores must be visible system-wide before the counter says so
+        const unsigned sm = wa.n9[c].sysmask;
+        const bool xedge = sm && ((rb == 0 && (sm & 0x7u)) || (rb == tr - 1 && (sm & 0x1C0u)) ||
+                                  (cb == 0 && (sm & 0x49u)) || (cb == tc - 1 && (sm & 0x124u)));
         if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (xedge) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
         if (tid == 0) {
             if (RESID && wa.resid) {
@@ -1338,8 +1353,15 @@ slab_wave2_kernel(Wave2Args wa) {
                 resid_max(wa.resid + 2 * k, m1);
                 resid_max(wa.resid + 2 * k + 1, m2);
             }
-            if (!HRT_WAVE_NOFENCE) __threadfence();
-            st_release_gpu_u32(wa.done + tile, wa.base + 2u * (unsigned)k + 2u);
+            const unsigned v = wa.base + 2u * (unsigned)k + 2u;
+            if (xedge) {
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
+                             : "memory");
+            } else {
+                if (!HRT_WAVE_NOFENCE) __threadfence();
+                st_release_gpu_u32(wa.done + tile, v);
+            }
         }
     }
 }
@@ -2142,12 +2164,18 @@ struct Plan {
     // two steps per pass (slab_wave2_kernel): one GPU, no faces to other
     // processes; HRT_FUSE2=0 turns it off
     bool fuse2 = true;
-    int* d_nb9 = nullptr;          // [nchunks][9] 3 x 3 chunk neighbourhood
+    Nbr9* d_n9 = nullptr;          // [nchunks] 3 x 3 chunk neighbourhood
+    int64_t n9_key = -1;           // tiles per chunk the table was built for
+    // faces to other processes (hrt_jacobi_plan_set_wave2_remote): per chunk
+    // and face N,S,W,E the mapped buffers and tile-counter base, or null
+    std::vector<uint64_t> r2buf, r2cnt;
+    std::vector<int64_t> r2idx;
     double* d_ones = nullptr;      // BOUNDARY row (rows outside the domain)
     int pgrid2 = 0;                // resident CTA slots of slab_wave2_kernel
     int64_t pkey2 = -1;
     bool fuse2_on() const {
-        return fuse2 && persist_on() && L.ndim == 2 && !wave_ipc && remote.empty() && !ipc &&
+        const bool local = !wave_ipc && remote.empty() && !ipc;
+        return fuse2 && persist_on() && L.ndim == 2 && (local || !r2buf.empty()) &&
                L.ext[0] >= 2 && L.ext[1] >= 2 && L.ext[1] % 2 == 0 && rows >= 2 &&
                L.ext[0] % rows != 1 && (int64_t)nbr.size() == 4 * (int64_t)nchunks;
     }
@@ -2614,25 +2642,40 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
         rc = build_wave(p, T);
         if (rc) return rc;
     }
-    if (!p->d_nb9) {
-        std::vector<int> nb9(9 * (size_t)p->nchunks, -1);
+    const int64_t per_chunk = T / std::max(1, p->nchunks);
+    if (!p->d_n9 || p->n9_key != per_chunk) {
+        std::vector<Nbr9> n9((size_t)p->nchunks);
         auto at = [&](int c, int f) { return c < 0 ? -1 : p->nbr[4 * (size_t)c + f]; };
         for (int c = 0; c < p->nchunks; ++c) {
-            int* o = nb9.data() + 9 * (size_t)c;
+            Nbr9& o = n9[c];
+            memset(&o, 0, sizeof(o));
             const int n = at(c, 0), so = at(c, 1);
-            o[4] = c;
-            o[1] = n;
-            o[7] = so;
-            o[3] = at(c, 2);
-            o[5] = at(c, 3);
-            o[0] = at(n, 2);
-            o[2] = at(n, 3);
-            o[6] = at(so, 2);
-            o[8] = at(so, 3);
+            const int idx[9] = {at(n, 2), n, at(n, 3), at(c, 2), c, at(c, 3),
+                                at(so, 2), so, at(so, 3)};
+            for (int e = 0; e < 9; ++e) {
+                if (idx[e] < 0) continue;
+                o.b[e][0] = p->h_chunks[idx[e]].b[0];
+                o.b[e][1] = p->h_chunks[idx[e]].b[1];
+                o.cnt[e] = p->d_pdone + (int64_t)idx[e] * per_chunk;
+            }
+            if (!p->r2buf.empty()) {  // faces to other processes (N, S, W, E)
+                const int pos[4] = {1, 7, 3, 5};
+                for (int f = 0; f < 4; ++f) {
+                    const size_t k = 4 * (size_t)c + f;
+                    if (!p->r2cnt[k]) continue;
+                    o.b[pos[f]][0] = reinterpret_cast<double*>(p->r2buf[2 * k]);
+                    o.b[pos[f]][1] = reinterpret_cast<double*>(p->r2buf[2 * k + 1]);
+                    o.cnt[pos[f]] = reinterpret_cast<unsigned int*>(p->r2cnt[k]) +
+                                    p->r2idx[k] * per_chunk;
+                    o.sysmask |= 1u << pos[f];
+                }
+            }
         }
-        HRT_CUDA(cudaMalloc(&p->d_nb9, sizeof(int) * nb9.size()));
-        HRT_CUDA(cudaMemcpy(p->d_nb9, nb9.data(), sizeof(int) * nb9.size(),
-                            cudaMemcpyHostToDevice));
+        cudaFree(p->d_n9);
+        p->d_n9 = nullptr;
+        HRT_CUDA(cudaMalloc(&p->d_n9, sizeof(Nbr9) * n9.size()));
+        HRT_CUDA(cudaMemcpy(p->d_n9, n9.data(), sizeof(Nbr9) * n9.size(), cudaMemcpyHostToDevice));
+        p->n9_key = per_chunk;
     }
     if (!p->d_ones) {
         std::vector<double> ones(T4_COLS + 8, HRT_BOUNDARY);
@@ -2653,8 +2696,7 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
     const hrt_chunk_layout_t& L = p->L;
     Wave2Args wa{};
-    wa.chunks = p->d_chunks;
-    wa.nb9 = p->d_nb9;
+    wa.n9 = p->d_n9;
     wa.done = p->d_pdone;
     wa.ticket = p->d_pticket;
     wa.base = p->pbase;
@@ -3106,6 +3148,35 @@ int hrt_jacobi_plan_set_nonneg(void* plan, int nonneg) {
 // faces): nbr4 = per chunk (plan order) the plan-local index of its north,
 // south, west, east neighbour or -1.  Runs of steps then execute as one
 // cooperative launch of slab_wave_kernel.  NULL disables.
+// Two-step passes across processes: per chunk and face (N, S, W, E) the
+// neighbour chunk's two buffers and the base of its rank's tile counters as
+// mapped here (CUDA IPC; 0 = not another process's) and its index in that
+// rank's plan.  Only row faces qualify (a chunk facing another process
+// north/south must have no west/east neighbours, so no diagonal chunk lives
+// in a third place); otherwise the plan keeps one step per pass.
+int hrt_jacobi_plan_set_wave2_remote(void* plan, const uint64_t* bufs8, const uint64_t* cnt4,
+                                     const int32_t* idx4) {
+    HRT_CHECK_ARG(plan && bufs8 && cnt4 && idx4, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG((int64_t)p->nbr.size() == 4 * (int64_t)p->nchunks && p->L.ndim == 2,
+                  "set the slab plan persistent first");
+    p->r2buf.clear();
+    p->r2cnt.clear();
+    p->r2idx.clear();
+    cudaFree(p->d_n9);
+    p->d_n9 = nullptr;
+    for (int c = 0; c < p->nchunks; ++c) {
+        const uint64_t* k = cnt4 + 4 * (size_t)c;
+        if (k[2] || k[3]) return HRT_OK;  // column faces to another process
+        if ((k[0] || k[1]) && (p->nbr[4 * (size_t)c + 2] >= 0 || p->nbr[4 * (size_t)c + 3] >= 0))
+            return HRT_OK;  // diagonal chunks would live in another process
+    }
+    p->r2buf.assign(bufs8, bufs8 + 8 * (size_t)p->nchunks);
+    p->r2cnt.assign(cnt4, cnt4 + 4 * (size_t)p->nchunks);
+    p->r2idx.assign(idx4, idx4 + 4 * (size_t)p->nchunks);
+    return HRT_OK;
+}
+
 int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t timeout_ns) {
     HRT_CHECK_ARG(plan, "null plan");
     Plan* p = reinterpret_cast<Plan*>(plan);
@@ -3128,8 +3199,8 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     p->nbr.assign(nbr4, nbr4 + nf * p->nchunks);
     cudaFree(p->d_pnbr);
     p->d_pnbr = nullptr;
-    cudaFree(p->d_nb9);
-    p->d_nb9 = nullptr;
+    cudaFree(p->d_n9);
+    p->d_n9 = nullptr;
     p->persist = true;
     p->pgrid = 0;  // rebuilt at the next launch
     if (timeout_ns) p->persist_timeout_ns = timeout_ns;
@@ -3151,6 +3222,14 @@ int hrt_jacobi_plan_error(void* plan, int* err) {
 
 // The plan's wavefront tile counters (allocated now if needed) for export to
 // neighbour ranks over CUDA IPC; *ntiles = their count.
+// *on = 1 when persistent runs of >= 4 steps use two-step passes
+// (slab_wave2_kernel) on this plan.
+int hrt_jacobi_plan_two_step(void* plan, int* on) {
+    HRT_CHECK_ARG(plan && on, "null argument");
+    *on = reinterpret_cast<Plan*>(plan)->fuse2_on() ? 1 : 0;
+    return HRT_OK;
+}
+
 int hrt_jacobi_plan_wave_counters(void* plan, uint64_t* ptr, int64_t* ntiles) {
     HRT_CHECK_ARG(plan && ptr && ntiles, "null argument");
     Plan* p = reinterpret_cast<Plan*>(plan);
@@ -3412,7 +3491,7 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_rnbr);
     cudaFree(p->d_rpeer);
     cudaFree(p->d_peer_done);
-    cudaFree(p->d_nb9);
+    cudaFree(p->d_n9);
     cudaFree(p->d_ones);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);

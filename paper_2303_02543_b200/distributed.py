@@ -173,7 +173,7 @@ class DistributedJacobi(JacobiSolver):
                ctypes.c_uint64(30_000_000_000))
         self.ipc = True
         if os.environ.get("HRT_PERSIST", "1") != "0":
-            self._setup_wave_ipc(g, mine, nbr_ranks)
+            self._setup_wave_ipc(g, mine, nbr_ranks, remote_buf)
         dist.barrier()
 
     def _setup_ipc3(self, gpu: int) -> None:
@@ -213,7 +213,7 @@ class DistributedJacobi(JacobiSolver):
         self._setup_wave_ipc(g, mine, nbr_ranks)
         dist.barrier()
 
-    def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list) -> None:
+    def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list, remote_buf=None) -> None:
         """Persistent wavefront across processes: every rank exports its
         per-tile step counters over CUDA IPC; an edge tile waits on the
         neighbour rank's adjacent tile counter (system scope) instead of a
@@ -257,6 +257,23 @@ class DistributedJacobi(JacobiSolver):
         N.call("hrt_jacobi_plan_set_wave_ipc", plan, _arr(ctypes.c_int32, rpeer),
                _arr(ctypes.c_int32, rnbr), _arr(ctypes.c_uint64, peer_ptrs), len(peer_ptrs),
                ctypes.c_uint64(30_000_000_000))
+        if remote_buf is not None and nf == 4:
+            # two steps per pass read the neighbour rank's rim rows in place
+            bufs, cnts, idxs = [], [], []
+            for k, lin in enumerate(mine):
+                for f in range(4):
+                    p = rpeer[4 * k + f]
+                    nb = self.grid.chunks[lin].neighbors.get(f)
+                    if p < 0:
+                        bufs += [0, 0]
+                        cnts.append(0)
+                        idxs.append(-1)
+                    else:
+                        bufs += [remote_buf(nb, 0), remote_buf(nb, 1)]
+                        cnts.append(peer_ptrs[p])
+                        idxs.append(rnbr[4 * k + f])
+            N.call("hrt_jacobi_plan_set_wave2_remote", plan, _arr(ctypes.c_uint64, bufs),
+                   _arr(ctypes.c_uint64, cnts), _arr(ctypes.c_int32, idxs))
         self.persistent = True
 
     def check_ipc(self) -> None:

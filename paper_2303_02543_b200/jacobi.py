@@ -902,6 +902,17 @@ class JacobiSolver:
         hpin.close()
         return out
 
+    @property
+    def two_step(self) -> bool:
+        """Runs of >= 4 steps execute as two-step passes (slab_wave2_kernel:
+        u read once per two steps) on every GPU of this solver."""
+        on = ctypes.c_int()
+        for g in self.used_gpus:
+            N.call("hrt_jacobi_plan_two_step", self.plans[g], ctypes.byref(on))
+            if not on.value:
+                return False
+        return bool(self.used_gpus)
+
     def residual_bits(self) -> dict[int, int]:
         """device address of each GPU's residual history (uint64 bit patterns)."""
         return dict(self.resid)
