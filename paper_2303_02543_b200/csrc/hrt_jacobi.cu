@@ -1108,6 +1108,87 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[12
     }
 }
 
+// Per-thread state of the two-step consumer (one tile).
+struct W2Ctx {
+    const Wave2Args* a;
+    double* ringp;          // ring base (double*), stage stride RS doubles
+    uint64_t* full;
+    uint64_t* empty;
+    int s;
+    uint32_t ph;
+    int p, lane, nv;
+    unsigned cghost;
+    bool mask, out_n, out_s;
+    int64_t i0, i1;
+    double* wr;
+    double zg, r1, r2;
+};
+
+template <int RS, int STAGES>
+__device__ __forceinline__ void w2_take(W2Ctx& x, double (&v)[8]) {
+    mbar_wait(&x.full[x.s], x.ph);
+    const double* row = x.ringp + (size_t)x.s * RS + x.p;
+    const double2 v01 = *reinterpret_cast<const double2*>(row);
+    const double2 v23 = *reinterpret_cast<const double2*>(row + 2);
+    const double2 v45 = *reinterpret_cast<const double2*>(row + 4);
+    const double2 v67 = *reinterpret_cast<const double2*>(row + 6);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
+    __syncwarp();
+    if (x.lane == 0) mbar_arrive(&x.empty[x.s]);
+    if (++x.s == STAGES) {
+        x.s = 0;
+        x.ph ^= 1;
+    }
+    v[0] = v01.x; v[1] = v01.y; v[2] = v23.x; v[3] = v23.y;
+    v[4] = v45.x; v[5] = v45.y; v[6] = v67.x; v[7] = v67.y;
+}
+
+// one ring row q: u(t) row r+1 arrives in `dn`; u(t+1) row r (r = i0-3+q)
+// goes into `u1n` (the slot of row r-3); u(t+2) row r-1 from u(t+1) rows
+// r-2 (`u1a`), r-1 (`u1b`), r (`u1n`)
+template <bool GUARD, bool RESID, int RS, int STAGES>
+__device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[8], const double (&mid)[8],
+                                       double (&dn)[8], const double (&u1a)[6],
+                                       const double (&u1b)[6], double (&u1n)[6], int q) {
+    w2_take<RS, STAGES>(x, dn);
+    const int64_t r = x.i0 - 3 + q;
+    const double zg = x.zg;
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+        u1n[m] = div6_t<GUARD>(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], zg, zg));
+    if (x.mask) {
+        const bool rghost = (r < 1 && x.out_n) || (r > x.a->ex && x.out_s);
+#pragma unroll
+        for (int m = 0; m < 6; ++m)
+            if (rghost || ((x.cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
+    }
+    if (RESID && r >= x.i0 && r <= x.i1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < x.nv) x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], mid[k + 2])));
+    }
+    if (q >= 4) {
+        double o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            o[k] = div6_t<GUARD>(sum6(u1a[k + 1], u1n[k + 1], u1b[k], u1b[k + 2], zg, zg));
+        if (x.nv == 4) {
+            *reinterpret_cast<double2*>(x.wr) = make_double2(o[0], o[1]);
+            *reinterpret_cast<double2*>(x.wr + 2) = make_double2(o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < x.nv) x.wr[k] = o[k];
+        }
+        if (RESID) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < x.nv) x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+        }
+        x.wr += x.a->sx;
+    }
+}
+
 // u(t+1) on rows i0-1 .. i1+1, columns j-1 .. j+4 of this thread (j = its
 // first column), then u(t+2) on rows i0 .. i1, columns j .. j+3 -> buffer
 // parity^1.  r1 / r2: max |u(t+1)-u(t)| / |u(t+2)-u(t+1)| over own cells.
@@ -1120,16 +1201,25 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[12
                                            uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
                                            int64_t i1, int parity, double& r1, double& r2) {
     constexpr int W = 128 * CW;
+    constexpr int RS = W + 4;
     const int tid = threadIdx.x;
-    const int lane = tid & 31;
+    W2Ctx x;
+    x.a = &a;
+    x.ringp = &ring[0][0];
+    x.full = full;
+    x.empty = empty;
+    x.s = s;
+    x.ph = ph;
+    x.lane = tid & 31;
     const int64_t j0 = 1 + cb * W;
     const int64_t j = j0 + 4 * tid;
     const int64_t nv64 = a.ey - j + 1;
-    const int nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);
-    const int p = 4 * tid;  // ring position of column j-2
+    x.nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);
+    x.p = 4 * tid;  // ring position of column j-2
     const int nrows = (int)(i1 - i0 + 5);
     const Nbr9& n9 = a.n9[c];
-    const bool out_n = !n9.b[1][0], out_s = !n9.b[7][0];
+    x.out_n = !n9.b[1][0];
+    x.out_s = !n9.b[7][0];
     const bool out_w = !n9.b[3][0], out_e = !n9.b[5][0];
     // u(t+1) columns j-1+m (m = 0..5) outside the domain keep BOUNDARY
     unsigned cghost = 0;
@@ -1138,84 +1228,33 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[12
         const int64_t cc = j - 1 + m;
         if ((cc < 1 && out_w) || (cc > a.ey && out_e)) cghost |= 1u << m;
     }
+    x.cghost = cghost;
     // does any u(t+1) value of this tile fall outside the domain?
-    const bool mask = __any_sync(0xffffffffu, cghost != 0) || (out_n && i0 <= 1) ||
-                      (out_s && i1 >= a.ex);
-    double* __restrict__ wr = n9.b[4][parity ^ 1] + a.origin + i0 * a.sx + j;
-    const double zg = a.zghost;
-
-    auto take = [&](double (&v)[8]) {
-        mbar_wait(&full[s], ph);
-        const double2 v01 = *reinterpret_cast<const double2*>(&ring[s][p]);
-        const double2 v23 = *reinterpret_cast<const double2*>(&ring[s][p + 2]);
-        const double2 v45 = *reinterpret_cast<const double2*>(&ring[s][p + 4]);
-        const double2 v67 = *reinterpret_cast<const double2*>(&ring[s][p + 6]);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-        }
-        v[0] = v01.x; v[1] = v01.y; v[2] = v23.x; v[3] = v23.y;
-        v[4] = v45.x; v[5] = v45.y; v[6] = v67.x; v[7] = v67.y;
-    };
-
-    // one ring row q: u(t) row r+1 arrives in `dn`; u(t+1) row r (r = i0-3+q)
-    // goes into `u1n` (the slot of row r-3); u(t+2) row r-1 from u1 rows
-    // r-2 (`u1a`), r-1 (`u1b`), r (`u1n`)
-    auto row = [&](const double (&up)[8], const double (&mid)[8], double (&dn)[8],
-                   const double (&u1a)[6], const double (&u1b)[6], double (&u1n)[6], int q) {
-        take(dn);
-        const int64_t r = i0 - 3 + q;
-#pragma unroll
-        for (int m = 0; m < 6; ++m)
-            u1n[m] = div6_t<GUARD>(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], zg, zg));
-        if (mask) {
-            const bool rghost = (r < 1 && out_n) || (r > a.ex && out_s);
-#pragma unroll
-            for (int m = 0; m < 6; ++m)
-                if (rghost || ((cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
-        }
-        if (RESID && r >= i0 && r <= i1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (k < nv) r1 = fmax(r1, fabs(__dsub_rn(u1n[k + 1], mid[k + 2])));
-        }
-        if (q >= 4) {
-            double o[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                o[k] = div6_t<GUARD>(sum6(u1a[k + 1], u1n[k + 1], u1b[k], u1b[k + 2], zg, zg));
-            if (nv == 4) {
-                *reinterpret_cast<double2*>(wr) = make_double2(o[0], o[1]);
-                *reinterpret_cast<double2*>(wr + 2) = make_double2(o[2], o[3]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (k < nv) wr[k] = o[k];
-            }
-            if (RESID) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (k < nv) r2 = fmax(r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
-            }
-            wr += a.sx;
-        }
-    };
+    x.mask = __any_sync(0xffffffffu, cghost != 0) || (x.out_n && i0 <= 1) ||
+             (x.out_s && i1 >= a.ex);
+    x.i0 = i0;
+    x.i1 = i1;
+    x.wr = n9.b[4][parity ^ 1] + a.origin + i0 * a.sx + j;
+    x.zg = a.zghost;
+    x.r1 = r1;
+    x.r2 = r2;
 
     double x0[8], x1[8], x2[8];  // u(t) rows, rotating
     double y0[6], y1[6], y2[6];  // u(t+1) rows, rotating
-    take(x0);                    // row i0-2
-    take(x1);                    // row i0-1
+    w2_take<RS, STAGES>(x, x0);  // row i0-2
+    w2_take<RS, STAGES>(x, x1);  // row i0-1
     int q = 2;
     for (; q + 2 < nrows; q += 3) {
-        row(x0, x1, x2, y1, y2, y0, q);
-        row(x1, x2, x0, y2, y0, y1, q + 1);
-        row(x2, x0, x1, y0, y1, y2, q + 2);
+        w2_row<GUARD, RESID, RS, STAGES>(x, x0, x1, x2, y1, y2, y0, q);
+        w2_row<GUARD, RESID, RS, STAGES>(x, x1, x2, x0, y2, y0, y1, q + 1);
+        w2_row<GUARD, RESID, RS, STAGES>(x, x2, x0, x1, y0, y1, y2, q + 2);
     }
-    if (q < nrows) row(x0, x1, x2, y1, y2, y0, q);
-    if (q + 1 < nrows) row(x1, x2, x0, y2, y0, y1, q + 1);
+    if (q < nrows) w2_row<GUARD, RESID, RS, STAGES>(x, x0, x1, x2, y1, y2, y0, q);
+    if (q + 1 < nrows) w2_row<GUARD, RESID, RS, STAGES>(x, x1, x2, x0, y2, y0, y1, q + 1);
+    s = x.s;
+    ph = x.ph;
+    r1 = x.r1;
+    r2 = x.r2;
 }
 
 #ifndef HRT_W2_MINB4
