@@ -624,6 +624,25 @@ class JacobiSolver:
             N.call("hrt_jacobi_plan_set_wave_ipc", self.plans[g], _arr(ctypes.c_int32, rpeer),
                    _arr(ctypes.c_int32, rnbr), _arr(ctypes.c_uint64, [counters[h] for h in peers]),
                    len(peers), ctypes.c_uint64(30_000_000_000))
+            if nf == 4:
+                # two-step passes read the other GPU's rim rows in place (peer)
+                bufs, cnts, idxs = [], [], []
+                for k, lin in enumerate(mine[g]):
+                    for f in range(4):
+                        nb = self.grid.chunks[lin].neighbors.get(f)
+                        h = self.placement.get(nb) if nb is not None else None
+                        if h is None or h == g:
+                            bufs += [0, 0]
+                            cnts.append(0)
+                            idxs.append(-1)
+                        else:
+                            N.call("hrt_enable_peer_access", g, h)
+                            bufs += list(self.bufs[nb])
+                            cnts.append(counters[h])
+                            idxs.append(index[h][nb])
+                N.call("hrt_jacobi_plan_set_wave2_remote", self.plans[g],
+                       _arr(ctypes.c_uint64, bufs), _arr(ctypes.c_uint64, cnts),
+                       _arr(ctypes.c_int32, idxs))
 
     def _setup_persistent(self) -> None:
         g = self.used_gpus[0]
