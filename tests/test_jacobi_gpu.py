@@ -331,3 +331,34 @@ def test_full_size_cfg3_and_cfg5_properties(hrt):
     d, cd, rd = solve((65536, 65536, 1), (8, 8, 1), 12)
     assert np.array_equal(c, d) and cc == cd and np.array_equal(rc, rd)
     assert np.array_equal(c, c[::-1])
+
+
+@pytest.mark.parametrize("dom,grid", [
+    ((130, 1030, 1), (2, 2, 1)),     # ragged row tiles (65 = 64 + 1 is excluded: 130/2 = 65)
+    ((132, 1032, 1), (2, 2, 1)),     # 66-row chunks (tiles 64 + 2), 516-wide (tiles 512 + 4)
+    ((96, 512, 1), (3, 2, 1)),       # 256-wide chunks: the 2-warp instance
+    ((8, 12, 1), (4, 3, 1)),         # 2 x 4 chunks: rims span whole neighbour chunks
+    ((200, 64, 1), (1, 1, 1)),       # one chunk: every rim is the domain boundary
+])
+@pytest.mark.parametrize("steps", [4, 6, 7, 13])
+def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps):
+    """slab_wave2_kernel (two Jacobi steps per pass, 2-cell rims read from the
+    3 x 3 chunk neighbourhood, u(t+1) only in registers) against the numpy
+    oracle on random signed data: field and every step's residual bitwise,
+    with n mod 4 single steps before the passes."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    rng = np.random.default_rng(steps * 7 + dom[0])
+    init = rng.random(dom) * 4.0 - 1.0
+    s = JacobiSolver(ChunkGrid(dom, grid=grid))
+    if dom[0] // grid[0] % 64 != 1:
+        assert s.two_step, "two-step passes should apply here"
+    s.upload(init)
+    s.run(steps, residual=True)
+    got = s.download()
+    res = s.residual_history()
+    s.close()
+    resid = []
+    ref = oracle.jacobi_reference(dom, steps, initial=init, residuals=resid)
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
+    assert np.array_equal(res, np.array(resid)), (res, resid)
