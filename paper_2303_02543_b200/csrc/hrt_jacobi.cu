@@ -1051,12 +1051,11 @@ struct Wave2Args {
 // rows i0-2 .. i1+2 of u(t) into the ring: the span j0-2 .. j0+W+1 (or the
 // owning chunk's part of it at a chunk's west/east edge, plus 16 bytes from
 // the west/east neighbour chunk's same row), BOUNDARY where outside.
-template <int CW, int STAGES>
-__device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[128 * CW + 4],
+template <int W, int STAGES>
+__device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[W + 4],
                                            uint64_t* full, uint64_t* empty, int& s,
                                            uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
                                            int64_t i1, int parity) {
-    constexpr int W = 128 * CW;
     const int64_t j0 = 1 + cb * W;
     const int64_t last = min(j0 + W - 1, a.ey);
     const Nbr9& n9 = a.n9[c];
@@ -1124,14 +1123,13 @@ struct W2Ctx {
     double zg, r1, r2;
 };
 
-template <int RS, int STAGES>
-__device__ __forceinline__ void w2_take(W2Ctx& x, double (&v)[8]) {
+template <int RS, int STAGES, int NV>
+__device__ __forceinline__ void w2_take(W2Ctx& x, double (&v)[NV]) {
     mbar_wait(&x.full[x.s], x.ph);
     const double* row = x.ringp + (size_t)x.s * RS + x.p;
-    const double2 v01 = *reinterpret_cast<const double2*>(row);
-    const double2 v23 = *reinterpret_cast<const double2*>(row + 2);
-    const double2 v45 = *reinterpret_cast<const double2*>(row + 4);
-    const double2 v67 = *reinterpret_cast<const double2*>(row + 6);
+    double2 t[NV / 2];
+#pragma unroll
+    for (int k = 0; k < NV / 2; ++k) t[k] = *reinterpret_cast<const double2*>(row + 2 * k);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
     __syncwarp();
     if (x.lane == 0) mbar_arrive(&x.empty[x.s]);
@@ -1139,50 +1137,56 @@ __device__ __forceinline__ void w2_take(W2Ctx& x, double (&v)[8]) {
         x.s = 0;
         x.ph ^= 1;
     }
-    v[0] = v01.x; v[1] = v01.y; v[2] = v23.x; v[3] = v23.y;
-    v[4] = v45.x; v[5] = v45.y; v[6] = v67.x; v[7] = v67.y;
+#pragma unroll
+    for (int k = 0; k < NV / 2; ++k) {
+        v[2 * k] = t[k].x;
+        v[2 * k + 1] = t[k].y;
+    }
 }
 
 // one ring row q: u(t) row r+1 arrives in `dn`; u(t+1) row r (r = i0-3+q)
 // goes into `u1n` (the slot of row r-3); u(t+2) row r-1 from u(t+1) rows
 // r-2 (`u1a`), r-1 (`u1b`), r (`u1n`)
-template <bool GUARD, bool RESID, int RS, int STAGES>
-__device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[8], const double (&mid)[8],
-                                       double (&dn)[8], const double (&u1a)[6],
-                                       const double (&u1b)[6], double (&u1n)[6], int q) {
-    w2_take<RS, STAGES>(x, dn);
+template <bool GUARD, bool RESID, int RS, int STAGES, int CPT>
+__device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[CPT + 4],
+                                       const double (&mid)[CPT + 4], double (&dn)[CPT + 4],
+                                       const double (&u1a)[CPT + 2],
+                                       const double (&u1b)[CPT + 2], double (&u1n)[CPT + 2],
+                                       int q) {
+    w2_take<RS, STAGES, CPT + 4>(x, dn);
     const int64_t r = x.i0 - 3 + q;
     const double zg = x.zg;
 #pragma unroll
-    for (int m = 0; m < 6; ++m)
+    for (int m = 0; m < CPT + 2; ++m)
         u1n[m] = div6_t<GUARD>(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], zg, zg));
     if (x.mask) {
         const bool rghost = (r < 1 && x.out_n) || (r > x.a->ex && x.out_s);
 #pragma unroll
-        for (int m = 0; m < 6; ++m)
+        for (int m = 0; m < CPT + 2; ++m)
             if (rghost || ((x.cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
     }
     if (RESID && r >= x.i0 && r <= x.i1) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < CPT; ++k)
             if (k < x.nv) x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], mid[k + 2])));
     }
     if (q >= 4) {
-        double o[4];
+        double o[CPT];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < CPT; ++k)
             o[k] = div6_t<GUARD>(sum6(u1a[k + 1], u1n[k + 1], u1b[k], u1b[k + 2], zg, zg));
-        if (x.nv == 4) {
-            *reinterpret_cast<double2*>(x.wr) = make_double2(o[0], o[1]);
-            *reinterpret_cast<double2*>(x.wr + 2) = make_double2(o[2], o[3]);
+        if (x.nv == CPT) {
+#pragma unroll
+            for (int k = 0; k < CPT; k += 2)
+                *reinterpret_cast<double2*>(x.wr + k) = make_double2(o[k], o[k + 1]);
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < CPT; ++k)
                 if (k < x.nv) x.wr[k] = o[k];
         }
         if (RESID) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < CPT; ++k)
                 if (k < x.nv) x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
         }
         x.wr += x.a->sx;
@@ -1195,12 +1199,13 @@ __device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[8], const do
 // The row loop is unrolled by three with the u(t) and u(t+1) row windows
 // rotating through three register arrays each (no moves); cells outside the
 // domain are masked only in tiles that touch it (a uniform branch).
-template <bool GUARD, bool RESID, int CW, int STAGES>
-__device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[128 * CW + 4],
-                                           uint64_t* full, uint64_t* empty, int& s,
-                                           uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
-                                           int64_t i1, int parity, double& r1, double& r2) {
-    constexpr int W = 128 * CW;
+template <bool GUARD, bool RESID, int CW, int CPT, int STAGES>
+__device__ __forceinline__ void w2_consume(const Wave2Args& a,
+                                           double (*ring)[32 * CPT * CW + 4], uint64_t* full,
+                                           uint64_t* empty, int& s, uint32_t& ph, int64_t c,
+                                           int64_t cb, int64_t i0, int64_t i1, int parity,
+                                           double& r1, double& r2) {
+    constexpr int W = 32 * CPT * CW;
     constexpr int RS = W + 4;
     const int tid = threadIdx.x;
     W2Ctx x;
@@ -1212,19 +1217,19 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[12
     x.ph = ph;
     x.lane = tid & 31;
     const int64_t j0 = 1 + cb * W;
-    const int64_t j = j0 + 4 * tid;
+    const int64_t j = j0 + CPT * tid;
     const int64_t nv64 = a.ey - j + 1;
-    x.nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);
-    x.p = 4 * tid;  // ring position of column j-2
+    x.nv = nv64 <= 0 ? 0 : (nv64 >= CPT ? CPT : (int)nv64);
+    x.p = CPT * tid;  // ring position of column j-2
     const int nrows = (int)(i1 - i0 + 5);
     const Nbr9& n9 = a.n9[c];
     x.out_n = !n9.b[1][0];
     x.out_s = !n9.b[7][0];
     const bool out_w = !n9.b[3][0], out_e = !n9.b[5][0];
-    // u(t+1) columns j-1+m (m = 0..5) outside the domain keep BOUNDARY
+    // u(t+1) columns j-1+m (m = 0..CPT+1) outside the domain keep BOUNDARY
     unsigned cghost = 0;
 #pragma unroll
-    for (int m = 0; m < 6; ++m) {
+    for (int m = 0; m < CPT + 2; ++m) {
         const int64_t cc = j - 1 + m;
         if ((cc < 1 && out_w) || (cc > a.ey && out_e)) cghost |= 1u << m;
     }
@@ -1239,18 +1244,18 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[12
     x.r1 = r1;
     x.r2 = r2;
 
-    double x0[8], x1[8], x2[8];  // u(t) rows, rotating
-    double y0[6], y1[6], y2[6];  // u(t+1) rows, rotating
-    w2_take<RS, STAGES>(x, x0);  // row i0-2
-    w2_take<RS, STAGES>(x, x1);  // row i0-1
+    double x0[CPT + 4], x1[CPT + 4], x2[CPT + 4];  // u(t) rows, rotating
+    double y0[CPT + 2], y1[CPT + 2], y2[CPT + 2];  // u(t+1) rows, rotating
+    w2_take<RS, STAGES, CPT + 4>(x, x0);             // row i0-2
+    w2_take<RS, STAGES, CPT + 4>(x, x1);             // row i0-1
     int q = 2;
     for (; q + 2 < nrows; q += 3) {
-        w2_row<GUARD, RESID, RS, STAGES>(x, x0, x1, x2, y1, y2, y0, q);
-        w2_row<GUARD, RESID, RS, STAGES>(x, x1, x2, x0, y2, y0, y1, q + 1);
-        w2_row<GUARD, RESID, RS, STAGES>(x, x2, x0, x1, y0, y1, y2, q + 2);
+        w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
+        w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x1, x2, x0, y2, y0, y1, q + 1);
+        w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x2, x0, x1, y0, y1, y2, q + 2);
     }
-    if (q < nrows) w2_row<GUARD, RESID, RS, STAGES>(x, x0, x1, x2, y1, y2, y0, q);
-    if (q + 1 < nrows) w2_row<GUARD, RESID, RS, STAGES>(x, x1, x2, x0, y2, y0, y1, q + 1);
+    if (q < nrows) w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
+    if (q + 1 < nrows) w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x1, x2, x0, y2, y0, y1, q + 1);
     s = x.s;
     ph = x.ph;
     r1 = x.r1;
@@ -1258,15 +1263,25 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a, double (*ring)[12
 }
 
 #ifndef HRT_W2_MINB4
-#define HRT_W2_MINB4 3   // resident CTAs/SM the 4-warp two-step kernel's registers target
+#define HRT_W2_MINB4 3   // resident CTAs/SM the registers target: 4 cols/thread, 512 wide
 #endif
 #ifndef HRT_W2_MINB2
-#define HRT_W2_MINB2 5   // same for the 2-warp (256-column) instance
+#define HRT_W2_MINB2 5   // 4 cols/thread, 256 wide
 #endif
-template <bool GUARD, bool RESID, int CW, int STAGES = T4_STAGES>
-__global__ void __launch_bounds__(32 * (CW + 1), CW == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
+#ifndef HRT_W2_MINB8
+#define HRT_W2_MINB8 2   // 2 cols/thread, 512 wide (8 consumer warps)
+#endif
+#ifndef HRT_W2_MINB4N
+#define HRT_W2_MINB4N 3  // 2 cols/thread, 256 wide
+#endif
+constexpr int w2_minb(int cw, int cpt) {
+    return cpt == 4 ? (cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
+                    : (cw == 8 ? HRT_W2_MINB8 : HRT_W2_MINB4N);
+}
+template <bool GUARD, bool RESID, int CW, int CPT = 4, int STAGES = T4_STAGES>
+__global__ void __launch_bounds__(32 * (CW + 1), w2_minb(CW, CPT))
 slab_wave2_kernel(Wave2Args wa) {
-    __shared__ alignas(128) double ring[STAGES][(128 * CW + 4)];
+    __shared__ alignas(128) double ring[STAGES][(32 * CPT * CW + 4)];
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
         tq_empty[WAVE_TQ];
     __shared__ long long tq[WAVE_TQ];
@@ -1337,7 +1352,7 @@ slab_wave2_kernel(Wave2Args wa) {
             }
             const int64_t i0 = 1 + rb * wa.rows;
             const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
-            w2_produce<CW, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
+            w2_produce<32 * CPT * CW, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
                                    (wa.parity0 + k) & 1);
         }
         return;
@@ -1363,7 +1378,7 @@ slab_wave2_kernel(Wave2Args wa) {
         const int64_t i0 = 1 + rb * wa.rows;
         const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
         double r1 = 0.0, r2 = 0.0;
-        w2_consume<GUARD, RESID, CW, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
+        w2_consume<GUARD, RESID, CW, CPT, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
                                              (wa.parity0 + k) & 1, r1, r2);
         if (RESID && wa.resid) {
             r1 = warp_max(r1);
@@ -2372,14 +2387,13 @@ static void set_carveouts() {
     carveout(slab_wave_kernel<true, false, 2>);
     carveout(slab_wave_kernel<false, true, 2>);
     carveout(slab_wave_kernel<false, false, 2>);
-    carveout(slab_wave2_kernel<true, true, 4>);
-    carveout(slab_wave2_kernel<true, false, 4>);
-    carveout(slab_wave2_kernel<false, true, 4>);
-    carveout(slab_wave2_kernel<false, false, 4>);
-    carveout(slab_wave2_kernel<true, true, 2>);
-    carveout(slab_wave2_kernel<true, false, 2>);
-    carveout(slab_wave2_kernel<false, true, 2>);
-    carveout(slab_wave2_kernel<false, false, 2>);
+#define C2(CW, CPT)                                   \
+    carveout(slab_wave2_kernel<true, true, CW, CPT>);   \
+    carveout(slab_wave2_kernel<true, false, CW, CPT>);  \
+    carveout(slab_wave2_kernel<false, true, CW, CPT>);  \
+    carveout(slab_wave2_kernel<false, false, CW, CPT>)
+    C2(4, 4); C2(2, 4); C2(8, 2); C2(4, 2);
+#undef C2
     carveout(slab_update_tma_kernel);
     carveout(volume_update_tma_kernel<true>);
     carveout(volume_wave_kernel<true>);
@@ -2648,23 +2662,32 @@ static int launch_persist3(Plan* p, cudaStream_t s, int64_t first, int64_t n,
 static int launch_persist1(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                            unsigned long long* resid_base);
 
-template <int CW>
+template <int CW, int CPT>
 static int wave2_occupancy(bool guard) {
     int dev = 0, sms = 0, a = 0, b = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (guard) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW, CPT>,
                                                       32 * (CW + 1), 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW, CPT>,
                                                       32 * (CW + 1), 0);
     } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW, CPT>,
                                                       32 * (CW + 1), 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW, CPT>,
                                                       32 * (CW + 1), 0);
     }
     return std::min(a, b) * sms;
+}
+
+// columns per consumer thread of the two-step kernel (HRT_W2_CPT: 4 or 2)
+static int w2_cpt() {
+    static const int v = [] {
+        const char* e = getenv("HRT_W2_CPT");
+        return (e && e[0] == '2') ? 2 : 4;
+    }();
+    return v;
 }
 
 // nf passes (2 steps each) from step `first` in one slab_wave2_kernel launch
@@ -2724,7 +2747,11 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     }
     const int64_t key2 = T * 4 + (p->nonneg ? 1 : 0);
     if (p->pgrid2 == 0 || p->pkey2 != key2) {
-        p->pgrid2 = narrow ? wave2_occupancy<2>(!p->nonneg) : wave2_occupancy<4>(!p->nonneg);
+        const bool c2 = w2_cpt() == 2;
+        p->pgrid2 = narrow ? (c2 ? wave2_occupancy<4, 2>(!p->nonneg)
+                                 : wave2_occupancy<2, 4>(!p->nonneg))
+                           : (c2 ? wave2_occupancy<8, 2>(!p->nonneg)
+                                 : wave2_occupancy<4, 4>(!p->nonneg));
         HRT_CUDA(cudaGetLastError());
         if (p->pgrid2 <= 0) {
             set_error("two-step kernel: no resident CTA slots");
@@ -2757,16 +2784,19 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     const bool guard = !p->nonneg, res = resid_base != nullptr;
     void* fn;
     int threads;
-#define WK2(G, R, CW) (void*)slab_wave2_kernel<G, R, CW>
+#define WK2(G, R, CW, CPT) (void*)slab_wave2_kernel<G, R, CW, CPT>
+#define PICK(CW, CPT)                                                        \
+    (guard ? (res ? WK2(true, true, CW, CPT) : WK2(true, false, CW, CPT))    \
+           : (res ? WK2(false, true, CW, CPT) : WK2(false, false, CW, CPT)))
+    const bool c2 = w2_cpt() == 2;
     if (narrow) {
-        fn = guard ? (res ? WK2(true, true, 2) : WK2(true, false, 2))
-                   : (res ? WK2(false, true, 2) : WK2(false, false, 2));
-        threads = 96;
+        fn = c2 ? PICK(4, 2) : PICK(2, 4);
+        threads = c2 ? 160 : 96;
     } else {
-        fn = guard ? (res ? WK2(true, true, 4) : WK2(true, false, 4))
-                   : (res ? WK2(false, true, 4) : WK2(false, false, 4));
-        threads = 160;
+        fn = c2 ? PICK(8, 2) : PICK(4, 4);
+        threads = c2 ? 288 : 160;
     }
+#undef PICK
 #undef WK2
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid2, T);
     void* args[] = {&wa};
