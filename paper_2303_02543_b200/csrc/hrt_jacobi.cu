@@ -2188,6 +2188,7 @@ struct Plan {
     std::vector<hrt_remote_seg_t> remote;
     void* comm = nullptr;
     int64_t rows = 64;
+    bool rows_explicit = false;   // set by hrt_jacobi_plan_set_rows
     int variant = 2;  // slab kernel: 0 LDG register march, 1 TMA ring, 2 TMA ring x4 cols
     bool nonneg = false;  // caller guarantees a finite field >= 0 (unguarded division)
     // graph of two steps (parity 0 then 1) per residual base pointer
@@ -3181,6 +3182,7 @@ int hrt_jacobi_plan_set_rows(void* plan, int64_t rows) {
     HRT_CHECK_ARG(plan && rows > 0, "bad rows");
     Plan* p = reinterpret_cast<Plan*>(plan);
     p->rows = rows;
+    p->rows_explicit = true;
     if (p->graph) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
@@ -3268,6 +3270,17 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     p->nbr.assign(nbr4, nbr4 + nf * p->nchunks);
     cudaFree(p->d_pnbr);
     p->d_pnbr = nullptr;
+    // two-step passes run best with 256-row tiles (rim rows 4/256 of the
+    // reads, fewer tile hand-offs: cfg2 591 -> 620 GLUPS); every rank of a
+    // decomposition derives the same tiling from the same layout
+    if (!p->rows_explicit && p->L.ndim == 2 && p->fuse2) {
+        const int64_t ex = p->L.ext[0];
+        p->rows = (ex % 256 == 1) ? 64 : 256;
+        if (p->graph) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+    }
     cudaFree(p->d_n9);
     p->d_n9 = nullptr;
     p->persist = true;

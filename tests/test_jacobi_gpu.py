@@ -334,14 +334,16 @@ def test_full_size_cfg3_and_cfg5_properties(hrt):
 
 
 @pytest.mark.parametrize("dom,grid", [
-    ((130, 1030, 1), (2, 2, 1)),     # ragged row tiles (65 = 64 + 1 is excluded: 130/2 = 65)
-    ((132, 1032, 1), (2, 2, 1)),     # 66-row chunks (tiles 64 + 2), 516-wide (tiles 512 + 4)
+    ((130, 1030, 1), (2, 2, 1)),     # odd chunk width: one step per pass (fallback)
+    ((132, 1032, 1), (2, 2, 1)),     # 66-row chunks (rows=64: tiles 64 + 2), 516-wide (512 + 4)
+    ((600, 1024, 1), (2, 2, 1)),     # 300-row chunks: 256 + 44 (default rows) / 4 x 64 + 44
     ((96, 512, 1), (3, 2, 1)),       # 256-wide chunks: the 2-warp instance
     ((8, 12, 1), (4, 3, 1)),         # 2 x 4 chunks: rims span whole neighbour chunks
     ((200, 64, 1), (1, 1, 1)),       # one chunk: every rim is the domain boundary
 ])
 @pytest.mark.parametrize("steps", [4, 6, 7, 13])
-def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps):
+@pytest.mark.parametrize("rows", [None, 64])
+def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows):
     """slab_wave2_kernel (two Jacobi steps per pass, 2-cell rims read from the
     3 x 3 chunk neighbourhood, u(t+1) only in registers) against the numpy
     oracle on random signed data: field and every step's residual bitwise,
@@ -350,8 +352,8 @@ def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps):
 
     rng = np.random.default_rng(steps * 7 + dom[0])
     init = rng.random(dom) * 4.0 - 1.0
-    s = JacobiSolver(ChunkGrid(dom, grid=grid))
-    if dom[0] // grid[0] % 64 != 1:
+    s = JacobiSolver(ChunkGrid(dom, grid=grid), rows=rows)
+    if dom[0] // grid[0] % 64 != 1 and dom[1] // grid[1] % 2 == 0:
         assert s.two_step, "two-step passes should apply here"
     s.upload(init)
     s.run(steps, residual=True)
