@@ -1,7 +1,8 @@
 cp paper_2303_02543_b200/libhrt_b200.so /tmp/base.so
-for v in w2e; do
+for v in pipe pipe2; do
   cp exp/$v/libhrt_b200.so paper_2303_02543_b200/libhrt_b200.so
   echo "== $v"
-  for w in cfg2 cfg5; do timeout 300 python bench.py --workload $w --no-cpu-baseline --no-scaling-baseline --e2e-steps 0 2>/dev/null | python tools/jline.py value roofline.avg_launch_ms; done
+  timeout 300 python -m pytest -x -q tests/test_jacobi_gpu.py -k "two_step or ladder" 2>&1 | tail -1
+  for w in cfg2 cfg5; do timeout 300 python bench.py --workload $w --no-cpu-baseline --no-scaling-baseline --e2e-steps 0 2>/dev/null | python tools/jline.py value; done
 done
 cp /tmp/base.so paper_2303_02543_b200/libhrt_b200.so
