@@ -1123,13 +1123,14 @@ struct W2Ctx {
     double zg, r1, r2;
 };
 
-template <int RS, int STAGES, int NV>
-__device__ __forceinline__ void w2_take(W2Ctx& x, double (&v)[NV]) {
+// u(t) rows live in double2 register pairs so each LDS.128 lands in place
+// (a plain double array made ptxas stage the loads and move them)
+template <int RS, int STAGES, int NP>
+__device__ __forceinline__ void w2_take(W2Ctx& x, double2 (&v)[NP]) {
     mbar_wait(&x.full[x.s], x.ph);
     const double* row = x.ringp + (size_t)x.s * RS + x.p;
-    double2 t[NV / 2];
 #pragma unroll
-    for (int k = 0; k < NV / 2; ++k) t[k] = *reinterpret_cast<const double2*>(row + 2 * k);
+    for (int k = 0; k < NP; ++k) v[k] = *reinterpret_cast<const double2*>(row + 2 * k);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
     __syncwarp();
     if (x.lane == 0) mbar_arrive(&x.empty[x.s]);
@@ -1137,28 +1138,29 @@ __device__ __forceinline__ void w2_take(W2Ctx& x, double (&v)[NV]) {
         x.s = 0;
         x.ph ^= 1;
     }
-#pragma unroll
-    for (int k = 0; k < NV / 2; ++k) {
-        v[2 * k] = t[k].x;
-        v[2 * k + 1] = t[k].y;
-    }
+}
+
+template <int NP>
+__device__ __forceinline__ double w2_e(const double2 (&v)[NP], int m) {
+    return (m & 1) ? v[m >> 1].y : v[m >> 1].x;
 }
 
 // one ring row q: u(t) row r+1 arrives in `dn`; u(t+1) row r (r = i0-3+q)
 // goes into `u1n` (the slot of row r-3); u(t+2) row r-1 from u(t+1) rows
 // r-2 (`u1a`), r-1 (`u1b`), r (`u1n`)
 template <bool GUARD, bool RESID, int RS, int STAGES, int CPT>
-__device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[CPT + 4],
-                                       const double (&mid)[CPT + 4], double (&dn)[CPT + 4],
-                                       const double (&u1a)[CPT + 2],
+__device__ __forceinline__ void w2_row(W2Ctx& x, const double2 (&up)[CPT / 2 + 2],
+                                       const double2 (&mid)[CPT / 2 + 2],
+                                       double2 (&dn)[CPT / 2 + 2], const double (&u1a)[CPT + 2],
                                        const double (&u1b)[CPT + 2], double (&u1n)[CPT + 2],
                                        int q) {
-    w2_take<RS, STAGES, CPT + 4>(x, dn);
+    w2_take<RS, STAGES, CPT / 2 + 2>(x, dn);
     const int64_t r = x.i0 - 3 + q;
     const double zg = x.zg;
 #pragma unroll
     for (int m = 0; m < CPT + 2; ++m)
-        u1n[m] = div6_t<GUARD>(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], zg, zg));
+        u1n[m] = div6_t<GUARD>(sum6(w2_e(up, m + 1), w2_e(dn, m + 1), w2_e(mid, m),
+                                    w2_e(mid, m + 2), zg, zg));
     if (x.mask) {
         const bool rghost = (r < 1 && x.out_n) || (r > x.a->ex && x.out_s);
 #pragma unroll
@@ -1166,9 +1168,15 @@ __device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[CPT + 4],
             if (rghost || ((x.cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
     }
     if (RESID && r >= x.i0 && r <= x.i1) {
+        if (x.nv == CPT) {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k)
-            if (k < x.nv) x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], mid[k + 2])));
+            for (int k = 0; k < CPT; ++k)
+                x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
+        } else {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+                if (k < x.nv) x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
+        }
     }
     if (q >= 4) {
         double o[CPT];
@@ -1179,15 +1187,18 @@ __device__ __forceinline__ void w2_row(W2Ctx& x, const double (&up)[CPT + 4],
 #pragma unroll
             for (int k = 0; k < CPT; k += 2)
                 *reinterpret_cast<double2*>(x.wr + k) = make_double2(o[k], o[k + 1]);
+            if (RESID) {
+#pragma unroll
+                for (int k = 0; k < CPT; ++k)
+                    x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+            }
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
-                if (k < x.nv) x.wr[k] = o[k];
-        }
-        if (RESID) {
-#pragma unroll
-            for (int k = 0; k < CPT; ++k)
-                if (k < x.nv) x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+                if (k < x.nv) {
+                    x.wr[k] = o[k];
+                    if (RESID) x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+                }
         }
         x.wr += x.a->sx;
     }
@@ -1244,10 +1255,10 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a,
     x.r1 = r1;
     x.r2 = r2;
 
-    double x0[CPT + 4], x1[CPT + 4], x2[CPT + 4];  // u(t) rows, rotating
-    double y0[CPT + 2], y1[CPT + 2], y2[CPT + 2];  // u(t+1) rows, rotating
-    w2_take<RS, STAGES, CPT + 4>(x, x0);             // row i0-2
-    w2_take<RS, STAGES, CPT + 4>(x, x1);             // row i0-1
+    double2 x0[CPT / 2 + 2], x1[CPT / 2 + 2], x2[CPT / 2 + 2];  // u(t) rows, rotating
+    double y0[CPT + 2], y1[CPT + 2], y2[CPT + 2];              // u(t+1) rows, rotating
+    w2_take<RS, STAGES, CPT / 2 + 2>(x, x0);                     // row i0-2
+    w2_take<RS, STAGES, CPT / 2 + 2>(x, x1);                     // row i0-1
     int q = 2;
     for (; q + 2 < nrows; q += 3) {
         w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
