@@ -69,6 +69,10 @@ __device__ __forceinline__ double sum6(double xm, double xp, double ym, double y
     return __dadd_rn(acc, zp);
 }
 
+// running max of |differences| (never NaN for finite fields): one compare
+// and a select, where fmax's NaN/signed-zero handling costs ~8 instructions
+__device__ __forceinline__ double rmax_acc(double r, double a) { return a > r ? a : r; }
+
 // non-negative doubles order like their bit patterns
 __device__ __forceinline__ void resid_max(unsigned long long* slot, double v) {
     atomicMax(slot, (unsigned long long)__double_as_longlong(v));
@@ -1171,11 +1175,11 @@ __device__ __forceinline__ void w2_row(W2Ctx& x, const double2 (&up)[CPT / 2 + 2
         if (x.nv == CPT) {
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
-                x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
+                x.r1 = rmax_acc(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
-                if (k < x.nv) x.r1 = fmax(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
+                if (k < x.nv) x.r1 = rmax_acc(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
         }
     }
     if (q >= 4) {
@@ -1190,14 +1194,14 @@ __device__ __forceinline__ void w2_row(W2Ctx& x, const double2 (&up)[CPT / 2 + 2
             if (RESID) {
 #pragma unroll
                 for (int k = 0; k < CPT; ++k)
-                    x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+                    x.r2 = rmax_acc(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
             }
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
                 if (k < x.nv) {
                     x.wr[k] = o[k];
-                    if (RESID) x.r2 = fmax(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
+                    if (RESID) x.r2 = rmax_acc(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
                 }
         }
         x.wr += x.a->sx;
