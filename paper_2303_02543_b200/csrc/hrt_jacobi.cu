@@ -216,10 +216,10 @@ slab_update_kernel(SlabArgs a) {
                 double* dst = w + r * a.sx + j;
                 if (both) {
                     *reinterpret_cast<double2*>(dst) = o;
-                    rmax = fmax(rmax, fmax(fabs(__dsub_rn(o.x, mid.x)), fabs(__dsub_rn(o.y, mid.y))));
+                    rmax = rmax_acc(rmax_acc(rmax, fabs(__dsub_rn(o.x, mid.x))), fabs(__dsub_rn(o.y, mid.y)));
                 } else {
                     dst[0] = o.x;
-                    rmax = fmax(rmax, fabs(__dsub_rn(o.x, mid.x)));
+                    rmax = rmax_acc(rmax, fabs(__dsub_rn(o.x, mid.x)));
                 }
             }
             double nlx, nry;
@@ -417,10 +417,10 @@ slab_update_tma_kernel(SlabArgs a) {
             double* dst = w + r * a.sx + j;
             if (both) {
                 *reinterpret_cast<double2*>(dst) = o;
-                rmax = fmax(rmax, fmax(fabs(__dsub_rn(o.x, mid.x)), fabs(__dsub_rn(o.y, mid.y))));
+                rmax = rmax_acc(rmax_acc(rmax, fabs(__dsub_rn(o.x, mid.x))), fabs(__dsub_rn(o.y, mid.y)));
             } else {
                 dst[0] = o.x;
-                rmax = fmax(rmax, fabs(__dsub_rn(o.x, mid.x)));
+                rmax = rmax_acc(rmax, fabs(__dsub_rn(o.x, mid.x)));
             }
         }
         up = mid;
@@ -663,14 +663,14 @@ __device__ __forceinline__ void t4_consume(const SlabArgs& a, double (*ring)[128
             *reinterpret_cast<double2*>(wr + 2) = make_double2(o[2], o[3]);
             if (RESID) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) rmax = fmax(rmax, fabs(__dsub_rn(o[k], mid[k])));
+                for (int k = 0; k < 4; ++k) rmax = rmax_acc(rmax, fabs(__dsub_rn(o[k], mid[k])));
             }
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (k < nv) {
                     wr[k] = o[k];
-                    if (RESID) rmax = fmax(rmax, fabs(__dsub_rn(o[k], mid[k])));
+                    if (RESID) rmax = rmax_acc(rmax, fabs(__dsub_rn(o[k], mid[k])));
                 }
         }
         if (PUSH) {
@@ -1584,10 +1584,10 @@ __device__ __forceinline__ void v_consume(const VolArgs& a, double (*ring)[V_ROW
                 oy = div6_t<GUARD>(sum6(up.y, dn.y, ym.y, yp.y, mid.x, zp));
                 *reinterpret_cast<double2*>(wr) = make_double2(ox, oy);
                 if (RESID)
-                    rmax = fmax(rmax, fmax(fabs(__dsub_rn(ox, mid.x)), fabs(__dsub_rn(oy, mid.y))));
+                    rmax = rmax_acc(rmax_acc(rmax, fabs(__dsub_rn(ox, mid.x))), fabs(__dsub_rn(oy, mid.y)));
             } else {
                 wr[0] = ox;
-                if (RESID) rmax = fmax(rmax, fabs(__dsub_rn(ox, mid.x)));
+                if (RESID) rmax = rmax_acc(rmax, fabs(__dsub_rn(ox, mid.x)));
             }
             if (PUSH && pm) {
                 // the reference's pack -> mp_send -> unpack of all six faces
@@ -1890,7 +1890,7 @@ volume_update_kernel(VolArgs a) {
             const double nv = div6(sum6(up, dn, __ldg(p - a.sy), __ldg(p + a.sy), __ldg(p - 1),
                                         __ldg(p + 1)));
             w[i * a.sx + col] = nv;
-            rmax = fmax(rmax, fabs(__dsub_rn(nv, mid)));
+            rmax = rmax_acc(rmax, fabs(__dsub_rn(nv, mid)));
             up = mid;
             mid = dn;
         }
