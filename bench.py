@@ -258,8 +258,8 @@ def run_ours(args):
     # updates: their algorithmic bytes are 8 per lattice update; the naive
     # one-step algorithm's 16 B/update is reported beside it.
     persistent = bool(getattr(solver, "persistent", False))
-    two_step = persistent and iters >= 4 and solver.two_step
-    launches_per_job = 1 if persistent else iters
+    two_step = iters >= 4 and solver.two_step
+    launches_per_job = 1 if persistent else (iters // 2 if two_step else iters)
     steps_per_launch = iters // launches_per_job
     avg_upd_ms = upd / (args.steps * launches_per_job)
     bytes_per_update = BYTES_PER_UPDATE // 2 if two_step else BYTES_PER_UPDATE
@@ -273,7 +273,7 @@ def run_ours(args):
               2: f"slab_update_tma4_kernel<false,true,{cw},push>",
               1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant])
     if grid.slab is False:
-        kname = "volume_update_tma_kernel<true>"
+        kname = "volume2_kernel<true>" if two_step else "volume_update_tma_kernel<true>"
     traffic = (args.traffic if args.traffic is not None else
                _recorded_traffic(wl["name"] + ("_two_step" if two_step else ""), world))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

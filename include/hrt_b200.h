@@ -238,8 +238,13 @@ int hrt_jacobi_plan_set_wave_ipc(void *plan, const int32_t *rpeer4, const int32_
  * index in that rank's plan.  Only row faces qualify; otherwise a no-op. */
 int hrt_jacobi_plan_set_wave2_remote(void *plan, const uint64_t *bufs8, const uint64_t *cnt4,
                                      const int32_t *idx4);
-/* *on = 1 when persistent runs of >= 4 steps use two-step passes. */
+/* *on = 1 when runs of >= 4 steps use two-step passes (slabs) or
+ * two-step launches (x-band volumes). */
 int hrt_jacobi_plan_two_step(void *plan, int *on);
+/* x-band volumes on one GPU: per chunk its -x/+x neighbour (plan-local
+ * index, -1 = domain face; y/z faces must be domain faces) — enables two
+ * steps per launch (volume2_kernel).  Null clears. */
+int hrt_jacobi_plan_set_xnbr(void *plan, const int32_t *xnb2);
 /* Synchronises; *err = 0 ok, 1 IPC edge wait timed out, 2 persistent
  * dependency wait timed out (results void). */
 int hrt_jacobi_plan_error(void *plan, int *err);
