@@ -2447,7 +2447,7 @@ struct Plan {
     bool narrow_chunk() const { return narrow_ok && L.ext[1] <= 256; }
     // two steps per pass (slab_wave2_kernel): one GPU, no faces to other
     // processes; HRT_FUSE2=0 turns it off
-    bool fuse2 = true;
+    int fuse2 = 1;  // 0 off, 1 when the problem has enough tiles, 2 always (tests)
     // two steps per launch for x-band volumes (volume2_kernel): opt-in
     // (HRT_FUSE3=1) — bit-exact but measured slower than one step per launch
     // on B200 (322 vs 350 GLUPS at 1024x1024x768: instruction-bound)
@@ -2908,6 +2908,24 @@ static int launch_persist3(Plan* p, cudaStream_t s, int64_t first, int64_t n,
 static int launch_persist1(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                            unsigned long long* resid_base);
 
+// resident CTAs of the two-step kernel on this GPU (3 per SM for 512-wide
+// tiles, 5 for 256-wide; from the occupancy API once known)
+static int64_t fuse2_slots(const Plan* p) {
+    if (p->pgrid2 > 0) return p->pgrid2;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    return (int64_t)sms * (p->narrow_chunk() ? HRT_W2_MINB2 : HRT_W2_MINB4);
+}
+
+// two-step passes pay off only with at least one tile per resident CTA
+// (smaller problems: a two-step tile pass is twice as long and too few run
+// at once — 2048^2 in 8x8 chunks: 64 vs 129 GLUPS one step per pass)
+static bool fuse2_use(const Plan* p) {
+    return p->fuse2_on() && (p->fuse2 == 2 || wave_tiles(p) >= fuse2_slots(p));
+}
+
 template <int CW, int CPT>
 static int wave2_occupancy(bool guard) {
     int dev = 0, sms = 0, a = 0, b = 0;
@@ -3058,7 +3076,7 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
 static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                           unsigned long long* resid_base) {
     if (n <= 0) return HRT_OK;
-    if (p->fuse2_on() && n >= 4) {
+    if (fuse2_use(p) && n >= 4) {
         const int64_t nf = (n / 4) * 2, nr = n - 2 * nf;
         int rc = nr ? launch_persist1(p, s, first, nr, resid_base) : HRT_OK;
         if (rc) return rc;
@@ -3274,7 +3292,7 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     // GLUPS; 128 planes leaves too few tiles (319)
     p->rows = 64;
     if (const char* e = getenv("HRT_NARROW")) p->narrow_ok = e[0] != '0';
-    if (const char* e = getenv("HRT_FUSE2")) p->fuse2 = e[0] != '0';
+    if (const char* e = getenv("HRT_FUSE2")) p->fuse2 = e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
     if (const char* e = getenv("HRT_FUSE3")) p->fuse3 = e[0] != '0';
     *plan = p;
     return HRT_OK;
@@ -3576,8 +3594,13 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     // reads, fewer tile hand-offs: cfg2 591 -> 620 GLUPS); every rank of a
     // decomposition derives the same tiling from the same layout
     if (!p->rows_explicit && p->L.ndim == 2 && p->fuse2) {
+        // 256-row tiles when that still leaves at least one tile per
+        // resident CTA of the two-step kernel; otherwise 64-row tiles
         const int64_t ex = p->L.ext[0];
-        p->rows = (ex % 256 == 1) ? 64 : 256;
+        const int64_t w = p->narrow_chunk() ? 256 : T4_COLS;
+        const int64_t tc = (p->L.ext[1] + w - 1) / w;
+        const int64_t t256 = (int64_t)p->nchunks * ((ex + 255) / 256) * tc;
+        p->rows = (ex % 256 != 1 && t256 >= fuse2_slots(p)) ? 256 : 64;
         if (p->graph) {
             cudaGraphExecDestroy(p->graph);
             p->graph = nullptr;
@@ -3611,7 +3634,7 @@ int hrt_jacobi_plan_error(void* plan, int* err) {
 int hrt_jacobi_plan_two_step(void* plan, int* on) {
     HRT_CHECK_ARG(plan && on, "null argument");
     const Plan* p = reinterpret_cast<Plan*>(plan);
-    *on = (p->fuse2_on() || p->fuse3_on()) ? 1 : 0;
+    *on = (fuse2_use(p) || p->fuse3_on()) ? 1 : 0;
     return HRT_OK;
 }
 

@@ -64,6 +64,7 @@ for dom, grid, steps in cases:
 # rim rows read over NVLink from the neighbour rank's IPC-mapped chunks):
 # every rank uploads its band of one seeded field; the gathered field and
 # the residual history vs the numpy oracle
+os.environ["HRT_FUSE2"] = "2"  # small domains: force two-step passes
 for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
                          ((96, 64, 1), (4 * world, 1, 1), 9)]:
     cg = ChunkGrid(dom, ranks=world, grid=grid)
@@ -92,6 +93,7 @@ for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
         ok_all &= ok
         print(f"dist_check world={world} random {dom} grid={grid} steps={steps} two-step="
               f"{[p[2] for p in parts]}: {'OK' if ok else 'DIFF'}", flush=True)
+del os.environ["HRT_FUSE2"]
 # full cfg3 size: the N-rank x-band run (IPC wavefront) against one GPU,
 # field bands and residual history bitwise (rank 0 solves the whole domain
 # on its own GPU after the distributed run)

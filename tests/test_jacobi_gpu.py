@@ -51,8 +51,10 @@ LADDER_NATIVE = [
 ]
 
 
+@pytest.mark.parametrize("fuse2", ["1", "2"])  # auto policy, and two-step passes forced
 @pytest.mark.parametrize("name", LADDER_NATIVE)
-def test_ladder_bitwise(hrt, ladder, small_arrays, name):
+def test_ladder_bitwise(hrt, ladder, small_arrays, name, fuse2, monkeypatch):
+    monkeypatch.setenv("HRT_FUSE2", fuse2)
     e = ladder[name]
     rep, cs, arr = hrt.run_jacobi3d(tuple(e["domain"]), steps=e["steps"], **kwargs_of(e))
     if name in small_arrays:
@@ -268,7 +270,8 @@ def test_persistent_guarded_division(hrt, oracle):
     ((512, 512, 1), (2, 2, 1), 70, 2, 1.0),     # 256-wide chunks, several row tiles
     ((1024, 2048, 1), (4, 4, 1), 40, 3, 1.0),   # 512-wide chunks, multiple column tiles
 ])
-def test_run_jobs_pipeline_matches_serial(hrt, oracle, dom, grid, steps, njobs, sign):
+def test_run_jobs_pipeline_matches_serial(hrt, oracle, dom, grid, steps, njobs, sign,
+                                          monkeypatch):
     """run_jobs (H2D/D2H of neighbouring jobs overlapped with compute on copy
     streams, double-buffered staging) gives, per job, exactly the field and
     residual history of a serial upload/run/download, on random data (side
@@ -277,6 +280,7 @@ def test_run_jobs_pipeline_matches_serial(hrt, oracle, dom, grid, steps, njobs, 
     from paper_2303_02543_b200.devices import PinnedBuffer
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
+    monkeypatch.setenv("HRT_FUSE2", "2")  # two-step passes even on these small domains
     rng = np.random.default_rng(5)
     inits = [sign * rng.random(dom) * (1 + k) for k in range(njobs)]
     nbytes = dom[0] * dom[1] * 8
@@ -343,13 +347,14 @@ def test_full_size_cfg3_and_cfg5_properties(hrt):
 ])
 @pytest.mark.parametrize("steps", [4, 6, 7, 13])
 @pytest.mark.parametrize("rows", [None, 64])
-def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows):
+def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, monkeypatch):
     """slab_wave2_kernel (two Jacobi steps per pass, 2-cell rims read from the
     3 x 3 chunk neighbourhood, u(t+1) only in registers) against the numpy
     oracle on random signed data: field and every step's residual bitwise,
     with n mod 4 single steps before the passes."""
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
+    monkeypatch.setenv("HRT_FUSE2", "2")  # these domains are too small for the auto policy
     rng = np.random.default_rng(steps * 7 + dom[0])
     init = rng.random(dom) * 4.0 - 1.0
     s = JacobiSolver(ChunkGrid(dom, grid=grid), rows=rows)
