@@ -89,7 +89,8 @@ for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
         rr = []
         ref = O.jacobi_reference(dom, steps, initial=full_init, residuals=rr)
         ok = np.array_equal(full, ref) and np.array_equal(res, np.array(rr))
-        ok &= all(p[2] for p in parts)  # two-step passes were in use on every rank
+        if os.environ.get("HRT_PERSIST", "1") != "0":  # (tile launches have no passes)
+            ok &= all(p[2] for p in parts)  # two-step passes were in use on every rank
         ok_all &= ok
         print(f"dist_check world={world} random {dom} grid={grid} steps={steps} two-step="
               f"{[p[2] for p in parts]}: {'OK' if ok else 'DIFF'}", flush=True)
