@@ -1289,12 +1289,27 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a,
 #ifndef HRT_W2_MINB4N
 #define HRT_W2_MINB4N 3  // 2 cols/thread, 256 wide
 #endif
+#ifndef HRT_W2_MAXNREG
+#define HRT_W2_MAXNREG 0  // >0: 4x4 two-step consumers grow to this many registers
+#endif
+#ifndef HRT_W2_PREG
+#define HRT_W2_PREG 32    // producer warp registers after setmaxnreg.dec
+#endif
+#ifndef HRT_W2_MREG_MINB
+#define HRT_W2_MREG_MINB 4
+#endif
+                   // (setmaxnreg), the producer warp shrinks to 24
+__host__ __device__ constexpr bool w2_mreg(int cw, int cpt) { return HRT_W2_MAXNREG > 0 && cw == 4 && cpt == 4; }
+// with setmaxnreg the producer is a whole warpgroup (4 warps; 3 leave at once)
+__host__ __device__ constexpr int w2_threads(int cw, int cpt) {
+    return 32 * (cw + (w2_mreg(cw, cpt) ? 4 : 1));
+}
 constexpr int w2_minb(int cw, int cpt) {
-    return cpt == 4 ? (cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
+    return w2_mreg(cw, cpt) ? HRT_W2_MREG_MINB : cpt == 4 ? (cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
                     : (cw == 8 ? HRT_W2_MINB8 : HRT_W2_MINB4N);
 }
 template <bool GUARD, bool RESID, int CW, int CPT = 4, int STAGES = T4_STAGES>
-__global__ void __launch_bounds__(32 * (CW + 1), w2_minb(CW, CPT))
+__global__ void __launch_bounds__(w2_threads(CW, CPT), w2_minb(CW, CPT))
 slab_wave2_kernel(Wave2Args wa) {
     __shared__ alignas(128) double ring[STAGES][(32 * CPT * CW + 4)];
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
@@ -1325,8 +1340,10 @@ slab_wave2_kernel(Wave2Args wa) {
 
     int s = 0;
     uint32_t ph = 0;
-    if (warp == CW) {
-        if (lane != 0) return;
+    if (warp >= CW) {
+        if constexpr (w2_mreg(CW, CPT))
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(HRT_W2_PREG));
+        if (warp != CW || lane != 0) return;
         bool dead = false;
         int slot = 0;
         uint32_t tph = 0;
@@ -1346,7 +1363,29 @@ slab_wave2_kernel(Wave2Args wa) {
             const int64_t rem = tile - c * per_chunk;
             const int64_t rb = rem / tc;
             const int64_t cb = rem - rb * tc;
-            if (!dead) {
+            if (w2_mreg(CW, CPT) && !dead) {
+                // lean producer (24-64 registers after setmaxnreg.dec): the
+                // neighbourhood one tile row at a time, three counters in flight
+                const unsigned need = wa.base + 2u * (unsigned)k;
+                const Nbr9& n9 = wa.n9[c];
+#pragma unroll 1
+                for (int dr = 0; dr < 3 && !dead; ++dr) {
+                    const unsigned int* q[3];
+                    bool sys[3];
+#pragma unroll
+                    for (int dc = 0; dc < 3; ++dc) {
+                        const int64_t r2 = rb + dr - 1, c2 = cb + dc - 1;
+                        const int ci = r2 < 0 ? -1 : (r2 >= tr ? 1 : 0);
+                        const int cj = c2 < 0 ? -1 : (c2 >= tc ? 1 : 0);
+                        const int e = (ci + 1) * 3 + (cj + 1);
+                        const unsigned int* base = n9.cnt[e];
+                        q[dc] = base ? base + (r2 - ci * tr) * tc + (c2 - cj * tc) : nullptr;
+                        sys[dc] = (n9.sysmask >> e) & 1u;
+                    }
+                    dead = !wait_counters<3>(q, sys, need, wa.timeout_ns, wa.err);
+                }
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            } else if (!dead) {
                 // the 3 x 3 tile neighbourhood must be done with step base+2k
                 const unsigned need = wa.base + 2u * (unsigned)k;
                 const Nbr9& n9 = wa.n9[c];
@@ -1372,6 +1411,8 @@ slab_wave2_kernel(Wave2Args wa) {
         }
         return;
     }
+    if constexpr (w2_mreg(CW, CPT))
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(HRT_W2_MAXNREG));
     int slot = 0;
     uint32_t tph = 0;
     for (;;) {
@@ -2933,14 +2974,14 @@ static int wave2_occupancy(bool guard) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (guard) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW, CPT>,
-                                                      32 * (CW + 1), 0);
+                                                      w2_threads(CW, CPT), 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW, CPT>,
-                                                      32 * (CW + 1), 0);
+                                                      w2_threads(CW, CPT), 0);
     } else {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW, CPT>,
-                                                      32 * (CW + 1), 0);
+                                                      w2_threads(CW, CPT), 0);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW, CPT>,
-                                                      32 * (CW + 1), 0);
+                                                      w2_threads(CW, CPT), 0);
     }
     return std::min(a, b) * sms;
 }
@@ -3055,10 +3096,10 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     const bool c2 = w2_cpt() == 2;
     if (narrow) {
         fn = c2 ? PICK(4, 2) : PICK(2, 4);
-        threads = c2 ? 160 : 96;
+        threads = c2 ? w2_threads(4, 2) : w2_threads(2, 4);
     } else {
         fn = c2 ? PICK(8, 2) : PICK(4, 4);
-        threads = c2 ? 288 : 160;
+        threads = c2 ? w2_threads(8, 2) : w2_threads(4, 4);
     }
 #undef PICK
 #undef WK2
