@@ -183,6 +183,27 @@ def reduce_max(x: float, world: int) -> float:
     return float(t.item())
 
 
+_JSON_FD = None  # the real stdout while library chatter is routed to stderr
+
+
+def quiet_stdout():
+    """Route fd 1 to stderr so library banners printed during communicator
+    setup (e.g. NCCL's version line) do not share stdout with the JSON line."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line: dict):
+    text = json.dumps(line) + "\n"
+    if _JSON_FD is None:
+        print(text, end="", flush=True)
+    else:
+        os.write(_JSON_FD, text.encode())
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -196,6 +217,8 @@ def run_ours(args):
     from paper_2303_02543_b200.distributed import DistributedJacobi, init_process
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
+    if args.gpus > 1:
+        quiet_stdout()
     rank, world, local = init_process("nccl") if args.gpus > 1 else (0, 1, 0)
     N.require_gpu(local)
     wl = workload(args.workload, world)
@@ -377,7 +400,7 @@ def run_ours(args):
         # N=1 so per-N efficiency can be read on one configuration
         line["scaling_baseline"] = scaling_baseline(args, local)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         import torch.distributed as dist
 
