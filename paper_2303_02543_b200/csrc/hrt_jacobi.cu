@@ -1308,10 +1308,23 @@ constexpr int w2_minb(int cw, int cpt) {
     return w2_mreg(cw, cpt) ? HRT_W2_MREG_MINB : cpt == 4 ? (cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
                     : (cw == 8 ? HRT_W2_MINB8 : HRT_W2_MINB4N);
 }
-template <bool GUARD, bool RESID, int CW, int CPT = 4, int STAGES = T4_STAGES>
+#ifndef HRT_W2_DSTAGES
+#define HRT_W2_DSTAGES 0  // >0: ring of this many stages in dynamic shared memory
+#endif
+constexpr int W2_STAGES = HRT_W2_DSTAGES > 0 ? HRT_W2_DSTAGES : T4_STAGES;
+// dynamic shared memory bytes of slab_wave2_kernel<*, *, CW, CPT>
+constexpr size_t w2_smem(int cw, int cpt) {
+    return HRT_W2_DSTAGES > 0 ? (size_t)HRT_W2_DSTAGES * (32 * cpt * cw + 4) * sizeof(double) : 0;
+}
+template <bool GUARD, bool RESID, int CW, int CPT = 4, int STAGES = W2_STAGES>
 __global__ void __launch_bounds__(w2_threads(CW, CPT), w2_minb(CW, CPT))
 slab_wave2_kernel(Wave2Args wa) {
+#if HRT_W2_DSTAGES > 0
+    extern __shared__ __align__(128) unsigned char w2_dyn_smem[];
+    auto ring = reinterpret_cast<double(*)[32 * CPT * CW + 4]>(w2_dyn_smem);
+#else
     __shared__ alignas(128) double ring[STAGES][(32 * CPT * CW + 4)];
+#endif
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
         tq_empty[WAVE_TQ];
     __shared__ long long tq[WAVE_TQ];
@@ -2672,7 +2685,15 @@ static void set_carveouts() {
     carveout(slab_wave2_kernel<true, true, CW, CPT>);   \
     carveout(slab_wave2_kernel<true, false, CW, CPT>);  \
     carveout(slab_wave2_kernel<false, true, CW, CPT>);  \
-    carveout(slab_wave2_kernel<false, false, CW, CPT>)
+    carveout(slab_wave2_kernel<false, false, CW, CPT>);                                          \
+    cudaFuncSetAttribute(slab_wave2_kernel<true, true, CW, CPT>,                                  \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT));     \
+    cudaFuncSetAttribute(slab_wave2_kernel<true, false, CW, CPT>,                                 \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT));     \
+    cudaFuncSetAttribute(slab_wave2_kernel<false, true, CW, CPT>,                                 \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT));     \
+    cudaFuncSetAttribute(slab_wave2_kernel<false, false, CW, CPT>,                                \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT))
     C2(4, 4); C2(2, 4); C2(8, 2); C2(4, 2);
 #undef C2
     carveout(slab_update_tma_kernel);
@@ -2974,14 +2995,14 @@ static int wave2_occupancy(bool guard) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (guard) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW, CPT>,
-                                                      w2_threads(CW, CPT), 0);
+                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW, CPT>,
-                                                      w2_threads(CW, CPT), 0);
+                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
     } else {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW, CPT>,
-                                                      w2_threads(CW, CPT), 0);
+                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW, CPT>,
-                                                      w2_threads(CW, CPT), 0);
+                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
     }
     return std::min(a, b) * sms;
 }
@@ -3094,18 +3115,21 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     (guard ? (res ? WK2(true, true, CW, CPT) : WK2(true, false, CW, CPT))    \
            : (res ? WK2(false, true, CW, CPT) : WK2(false, false, CW, CPT)))
     const bool c2 = w2_cpt() == 2;
+    size_t smem;
     if (narrow) {
         fn = c2 ? PICK(4, 2) : PICK(2, 4);
         threads = c2 ? w2_threads(4, 2) : w2_threads(2, 4);
+        smem = c2 ? w2_smem(4, 2) : w2_smem(2, 4);
     } else {
         fn = c2 ? PICK(8, 2) : PICK(4, 4);
         threads = c2 ? w2_threads(8, 2) : w2_threads(4, 4);
+        smem = c2 ? w2_smem(8, 2) : w2_smem(4, 4);
     }
 #undef PICK
 #undef WK2
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid2, T);
     void* args[] = {&wa};
-    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3((unsigned)threads), args, 0, s));
+    HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3((unsigned)threads), args, smem, s));
     p->pbase += 2u * (unsigned)nf;
     p->ghosts_ready = false;  // passes read neighbours in place; ghost planes went stale
     return HRT_OK;
