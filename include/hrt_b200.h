@@ -241,6 +241,19 @@ int hrt_jacobi_plan_set_wave2_remote(void *plan, const uint64_t *bufs8, const ui
 /* *on = 1 when runs of >= 4 steps use two-step passes (slabs) or
  * two-step launches (x-band volumes). */
 int hrt_jacobi_plan_two_step(void *plan, int *on);
+/* Chunk count the tiling decisions (tile rows, two-step passes or not) are
+ * made for: pass the largest chunk count per GPU of the whole
+ * decomposition (every GPU and rank of a run), before persistent mode, so
+ * neighbouring GPUs agree on the tiling whose counters they index.
+ * 0 = the plan's own chunk count. */
+int hrt_jacobi_plan_set_tiling_chunks(void *plan, int64_t n);
+/* Two-step passes: 0 off, 1 when the decomposition has at least one tile
+ * per resident CTA (default; HRT_FUSE2 overrides at plan creation), 2
+ * always.  Multi-GPU runs turn them off on every GPU when not every GPU
+ * can run them (a one-step neighbour would read ghosts nobody pushed). */
+int hrt_jacobi_plan_set_fuse2(void *plan, int mode);
+/* The plan's tiling: rows per tile, tiles per chunk, two-step passes on. */
+int hrt_jacobi_plan_tiling(void *plan, int64_t *rows, int64_t *tiles_per_chunk, int *two_step);
 /* x-band volumes on one GPU: per chunk its -x/+x neighbour (plan-local
  * index, -1 = domain face; y/z faces must be domain faces) — enables two
  * steps per launch (volume2_kernel).  Null clears. */
@@ -253,9 +266,9 @@ int hrt_jacobi_plan_field_copy(void *plan, void *stream, double *field, int64_t 
 /* slab update kernel: 0 = LDG register march, 1 = TMA bulk-copy ring,
  * 2 = TMA ring with four columns per thread (default) */
 int hrt_jacobi_plan_set_variant(void *plan, int variant);
-/* caller guarantees a finite, non-negative field (the reference's problem):
- * the slab kernel's six-term sum is then >= 2 and the division needs no
- * subnormal/special-value guard */
+/* caller guarantees a finite, non-negative field bounded by 2^997 (the
+ * reference's problem): the slab kernel's six-term sum is then in
+ * [2, 2^1000] and the division needs no subnormal/overflow guard */
 int hrt_jacobi_plan_set_nonneg(void *plan, int nonneg);
 /* one step: halo faces, then the 7-point update of every chunk (_update_body
  * jacobi.py:70-79); resid (nullable, device, uint64 bit patterns of float64)

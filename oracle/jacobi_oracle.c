@@ -35,6 +35,11 @@
 
 #define BOUNDARY 1.0
 
+int oracle_jacobi3d_init(int64_t X, int64_t Y, int64_t Z, int64_t steps,
+                         const double *initial, double *out_interior, double *resid);
+int oracle_jacobi2d_init(int64_t X, int64_t Y, int64_t steps, const double *initial,
+                         double *out_interior, double *resid);
+
 static inline size_t gidx(int64_t i, int64_t j, int64_t k, int64_t Y2, int64_t Z2) {
     return (size_t)((i * Y2 + j) * Z2 + k);
 }
@@ -44,6 +49,15 @@ static inline size_t gidx(int64_t i, int64_t j, int64_t k, int64_t Y2, int64_t Z
  * Returns 0, or -1 on allocation failure. */
 int oracle_jacobi3d(int64_t X, int64_t Y, int64_t Z, int64_t steps,
                     double *out_interior, double *resid) {
+    return oracle_jacobi3d_init(X, Y, Z, steps, NULL, out_interior, resid);
+}
+
+/* As oracle_jacobi3d, starting from `initial` (X*Y*Z C-order interior;
+ * NULL = the reference's 0.0).  The initial field is a test extension: the
+ * reference always starts from 0.0 (jacobi.py:52), but a random field is
+ * what makes full-size parity non-degenerate. */
+int oracle_jacobi3d_init(int64_t X, int64_t Y, int64_t Z, int64_t steps,
+                         const double *initial, double *out_interior, double *resid) {
     const int64_t X2 = X + 2, Y2 = Y + 2, Z2 = Z + 2;
     const size_t n = (size_t)X2 * Y2 * Z2;
     double *u = (double *)malloc(n * sizeof(double));
@@ -56,7 +70,9 @@ int oracle_jacobi3d(int64_t X, int64_t Y, int64_t Z, int64_t steps,
             for (int64_t k = 0; k < Z2; ++k) {
                 int ghost = (i == 0 || i == X2 - 1 || j == 0 || j == Y2 - 1 ||
                              k == 0 || k == Z2 - 1);
-                u[gidx(i, j, k, Y2, Z2)] = ghost ? BOUNDARY : 0.0;
+                u[gidx(i, j, k, Y2, Z2)] =
+                    ghost ? BOUNDARY
+                          : (initial ? initial[((i - 1) * Y + (j - 1)) * Z + (k - 1)] : 0.0);
             }
     memcpy(v, u, n * sizeof(double)); /* nxt = u.copy() keeps the ghosts */
     for (int64_t s = 0; s < steps; ++s) {
@@ -105,6 +121,12 @@ int oracle_jacobi3d(int64_t X, int64_t Y, int64_t Z, int64_t steps,
  * the bounded CPU baseline can reach the large configs. */
 int oracle_jacobi2d(int64_t X, int64_t Y, int64_t steps, double *out_interior,
                     double *resid) {
+    return oracle_jacobi2d_init(X, Y, steps, NULL, out_interior, resid);
+}
+
+/* As oracle_jacobi2d, starting from `initial` (X*Y interior, NULL = 0.0). */
+int oracle_jacobi2d_init(int64_t X, int64_t Y, int64_t steps, const double *initial,
+                         double *out_interior, double *resid) {
     const int64_t X2 = X + 2, Y2 = Y + 2;
     const size_t n = (size_t)X2 * Y2;
     double *u = (double *)malloc(n * sizeof(double));
@@ -114,7 +136,8 @@ int oracle_jacobi2d(int64_t X, int64_t Y, int64_t steps, double *out_interior,
     for (int64_t i = 0; i < X2; ++i)
         for (int64_t j = 0; j < Y2; ++j) {
             int ghost = (i == 0 || i == X2 - 1 || j == 0 || j == Y2 - 1);
-            u[i * Y2 + j] = ghost ? BOUNDARY : 0.0;
+            u[i * Y2 + j] = ghost ? BOUNDARY
+                                  : (initial ? initial[(i - 1) * Y + (j - 1)] : 0.0);
         }
     memcpy(v, u, n * sizeof(double));
     for (int64_t s = 0; s < steps; ++s) {

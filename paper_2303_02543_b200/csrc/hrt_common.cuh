@@ -22,6 +22,24 @@ inline Stream* as_stream(void* h) { return reinterpret_cast<Stream*>(h); }
 // Make `gpu` current for the calling thread (cheap when already current).
 int use_device(int gpu);
 
+// Streaming multiprocessors of `gpu` (queried once per device, cached);
+// gpu < 0 means the calling thread's current device.  Grid sizes derive
+// from it instead of a hard-coded 148 (other SKUs, MIG slices).
+inline int sm_count(int gpu = -1) {
+    static int cache[64] = {0};
+    if (gpu < 0 && cudaGetDevice(&gpu) != cudaSuccess) gpu = 0;
+    if (gpu >= 64) gpu = 63;
+    if (cache[gpu] <= 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, gpu) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;  // B200
+        }
+        cache[gpu] = n;
+    }
+    return cache[gpu];
+}
+
 }  // namespace hrt
 
 #define HRT_CUDA(call)                                              \

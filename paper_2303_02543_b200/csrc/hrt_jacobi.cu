@@ -2502,6 +2502,14 @@ struct Plan {
     // two steps per pass (slab_wave2_kernel): one GPU, no faces to other
     // processes; HRT_FUSE2=0 turns it off
     int fuse2 = 1;  // 0 off, 1 when the problem has enough tiles, 2 always (tests)
+    // Chunk count the tiling decisions (tile rows, two-step or not) are made
+    // for: the largest chunk count per GPU over the whole decomposition, so
+    // every GPU and rank of a run picks the same tiling — neighbours index
+    // each other's tile counters with their own tiling and read each
+    // other's buffers by pass parity (hrt_jacobi_plan_set_tiling_chunks;
+    // 0 = this plan's own count)
+    int64_t tiling_chunks = 0;
+    int64_t tn() const { return tiling_chunks > 0 ? tiling_chunks : (int64_t)nchunks; }
     // two steps per launch for x-band volumes (volume2_kernel): opt-in
     // (HRT_FUSE3=1) — bit-exact but measured slower than one step per launch
     // on B200 (322 vs 350 GLUPS at 1024x1024x768: instruction-bound)
@@ -2972,20 +2980,21 @@ static int launch_persist1(Plan* p, cudaStream_t s, int64_t first, int64_t n,
 
 // resident CTAs of the two-step kernel on this GPU (3 per SM for 512-wide
 // tiles, 5 for 256-wide; from the occupancy API once known)
+// (a function of the layout and the SM count only — not of launch history —
+// so the decision is the same before and after the first launch)
 static int64_t fuse2_slots(const Plan* p) {
-    if (p->pgrid2 > 0) return p->pgrid2;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaGetLastError();
-    return (int64_t)sms * (p->narrow_chunk() ? HRT_W2_MINB2 : HRT_W2_MINB4);
+    return (int64_t)sm_count(p->gpu) * (p->narrow_chunk() ? HRT_W2_MINB2 : HRT_W2_MINB4);
 }
 
 // two-step passes pay off only with at least one tile per resident CTA
 // (smaller problems: a two-step tile pass is twice as long and too few run
-// at once — 2048^2 in 8x8 chunks: 64 vs 129 GLUPS one step per pass)
+// at once — 2048^2 in 8x8 chunks: 64 vs 129 GLUPS one step per pass);
+// counted for tn() chunks so every GPU of a decomposition decides alike
 static bool fuse2_use(const Plan* p) {
-    return p->fuse2_on() && (p->fuse2 == 2 || wave_tiles(p) >= fuse2_slots(p));
+    if (!p->fuse2_on()) return false;
+    if (p->fuse2 == 2) return true;
+    const int64_t per_chunk = wave_tiles(p) / std::max(1, p->nchunks);
+    return per_chunk * p->tn() >= fuse2_slots(p);
 }
 
 template <int CW, int CPT>
@@ -3664,7 +3673,7 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
         const int64_t ex = p->L.ext[0];
         const int64_t w = p->narrow_chunk() ? 256 : T4_COLS;
         const int64_t tc = (p->L.ext[1] + w - 1) / w;
-        const int64_t t256 = (int64_t)p->nchunks * ((ex + 255) / 256) * tc;
+        const int64_t t256 = p->tn() * ((ex + 255) / 256) * tc;
         p->rows = (ex % 256 != 1 && t256 >= fuse2_slots(p)) ? 256 : 64;
         if (p->graph) {
             cudaGraphExecDestroy(p->graph);
@@ -3700,6 +3709,29 @@ int hrt_jacobi_plan_two_step(void* plan, int* on) {
     HRT_CHECK_ARG(plan && on, "null argument");
     const Plan* p = reinterpret_cast<Plan*>(plan);
     *on = (fuse2_use(p) || p->fuse3_on()) ? 1 : 0;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_tiling_chunks(void* plan, int64_t n) {
+    HRT_CHECK_ARG(plan && n >= 0, "bad argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG(!p->persist, "set the tiling chunk count before persistent mode");
+    p->tiling_chunks = n;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_fuse2(void* plan, int mode) {
+    HRT_CHECK_ARG(plan && mode >= 0 && mode <= 2, "bad argument");
+    reinterpret_cast<Plan*>(plan)->fuse2 = mode;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_tiling(void* plan, int64_t* rows, int64_t* tiles_per_chunk, int* two_step) {
+    HRT_CHECK_ARG(plan && rows && tiles_per_chunk && two_step, "null argument");
+    const Plan* p = reinterpret_cast<Plan*>(plan);
+    *rows = p->rows;
+    *tiles_per_chunk = wave_tiles(p) / std::max(1, p->nchunks);
+    *two_step = (fuse2_use(p) || p->fuse3_on()) ? 1 : 0;
     return HRT_OK;
 }
 
@@ -4027,7 +4059,7 @@ int hrt_plane_copy(void* stream, const hrt_halo_seg_t* seg) {
     Stream* st = as_stream(stream);
     int rc = use_device(st->gpu);
     if (rc) return rc;
-    const int64_t blocks = std::min<int64_t>((n + HALO_THREADS - 1) / HALO_THREADS, 148 * 8);
+    const int64_t blocks = std::min<int64_t>((n + HALO_THREADS - 1) / HALO_THREADS, (int64_t)sm_count() * 8);
     plane_copy_kernel<<<(unsigned)blocks, HALO_THREADS, 0, st->s>>>(*seg);
     HRT_CUDA(cudaGetLastError());
     return HRT_OK;
@@ -4064,7 +4096,7 @@ int hrt_jacobi_chunk_update(void* stream, const double* u, double* nxt, int64_t 
     volume_update_kernel<<<(unsigned)grid, dim3(VOL_TX, VOL_TY), 0, st->s>>>(a);
     HRT_CUDA(cudaGetLastError());
     const int64_t n = (ex + 2) * (ey + 2) * (ez + 2);
-    ghost_shell_copy_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0,
+    ghost_shell_copy_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8), 256, 0,
                               st->s>>>(u, nxt, ex, ey, ez, a.sx, a.sy);
     HRT_CUDA(cudaGetLastError());
     return HRT_OK;
@@ -4077,7 +4109,7 @@ int hrt_jacobi_ghost_fill(void* stream, double* base, const hrt_chunk_layout_t* 
     int rc = use_device(st->gpu);
     if (rc) return rc;
     const int64_t n = (L->ext[0] + 2) * (L->ext[1] + 2) * (L->ndim == 3 ? L->ext[2] + 2 : 1);
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
     ghost_fill_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st->s>>>(
         base, L->origin, L->ext[0], L->ext[1], L->ext[2], L->stride[0], L->stride[1], L->ndim,
         mask, value);
@@ -4163,7 +4195,7 @@ int hrt_mix_u8(void* stream, uint8_t* dst, const uint8_t* src, int64_t n, int sa
     Stream* st = as_stream(stream);
     int rc = use_device(st->gpu);
     if (rc) return rc;
-    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 8);
     mix_u8_kernel<<<(unsigned)blocks, 256, 0, st->s>>>(dst, src, n, salt);
     HRT_CUDA(cudaGetLastError());
     return HRT_OK;
@@ -4181,7 +4213,7 @@ int hrt_div6_sweep(void* stream, uint64_t seed, int64_t n, int mode, uint64_t* m
     HRT_CUDA(cudaMallocAsync(&d_bad, sizeof(double), st->s));
     HRT_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long), st->s));
     HRT_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(double), st->s));
-    div6_sweep_kernel<<<148 * 8, 256, 0, st->s>>>(seed, n, mode, d_cnt, d_bad);
+    div6_sweep_kernel<<<sm_count() * 8, 256, 0, st->s>>>(seed, n, mode, d_cnt, d_bad);
     cudaError_t le = cudaGetLastError();
     unsigned long long cnt = 0;
     double bad = 0;

@@ -580,7 +580,7 @@ int hrt_bytes_equal(void* stream, const void* a, const void* b, uint64_t bytes, 
     HRT_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), s->s));
     HRT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s->s));
     const uint64_t n16 = bytes / 16;
-    const uint64_t nb = std::min<uint64_t>(148 * 4, (n16 + 511) / 512 + 1);
+    const uint64_t nb = std::min<uint64_t>((uint64_t)hrt::sm_count(s->gpu) * 4, (n16 + 511) / 512 + 1);
     hrt::bytes_diff_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
         reinterpret_cast<const uint8_t*>(a), reinterpret_cast<const uint8_t*>(b), n16, bytes, d);
     cudaError_t le = cudaGetLastError();
@@ -606,7 +606,7 @@ int hrt_copy_sm_async(void* stream, void* dst, const void* src, uint64_t bytes, 
     if (rc) return rc;
     const uint64_t n16 = bytes / 16;
     const uint64_t nb = blocks > 0 ? (uint64_t)blocks
-                                   : std::min<uint64_t>(148 * 4, (n16 + 511) / 512 + 1);
+                                   : std::min<uint64_t>((uint64_t)hrt::sm_count(s->gpu) * 4, (n16 + 511) / 512 + 1);
     hrt::sm_copy_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
         reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), n16, n16 * 16,
         bytes);
@@ -650,7 +650,7 @@ int hrt_copy_ordered(void* stream, void* dst, const void* src, uint64_t bytes, i
         if (sm) {
             HRT_CHECK_ARG(aligned, "sm copy needs 16-byte alignment");
             const uint64_t n16 = bytes / 16;
-            const uint64_t nb = std::min<uint64_t>(148 * 4, (n16 + 511) / 512 + 1);
+            const uint64_t nb = std::min<uint64_t>((uint64_t)hrt::sm_count(s->gpu) * 4, (n16 + 511) / 512 + 1);
             hrt::sm_copy_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
                 reinterpret_cast<uint8_t*>(dst), reinterpret_cast<const uint8_t*>(src), n16,
                 n16 * 16, bytes);

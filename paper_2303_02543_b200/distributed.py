@@ -233,9 +233,13 @@ class DistributedJacobi(JacobiSolver):
         h = ctypes.create_string_buffer(64)
         N.call("hrt_ipc_get_handle", ctypes.c_void_p(ptr.value), h)
         every = [None] * self.world
-        dist.all_gather_object(every, (h.raw, ntiles.value))
+        dist.all_gather_object(every, (h.raw, self.tiling()[g][:2]))
+        # neighbours index each other's tile counters with their own tiling:
+        # (rows, tiles per chunk) agree by construction (decided from the
+        # grid's largest per-rank chunk count); checked again after the
+        # two-step set-up below
         if len({t for _, t in every}) != 1:
-            raise HrtError(f"wavefront tilings differ across ranks: {[t for _, t in every]}")
+            raise HrtError(f"per-chunk tilings differ across ranks: {[t for _, t in every]}")
         peer_ptrs = []
         for q in nbr_ranks:
             pq = ctypes.c_void_p()
@@ -274,6 +278,11 @@ class DistributedJacobi(JacobiSolver):
                         idxs.append(rnbr[4 * k + f])
             N.call("hrt_jacobi_plan_set_wave2_remote", plan, _arr(ctypes.c_uint64, bufs),
                    _arr(ctypes.c_uint64, cnts), _arr(ctypes.c_int32, idxs))
+        # a rank with a column face to another process keeps one step per
+        # pass; then no rank may run two-step passes (see _agree_tiling)
+        tilings = [None] * self.world
+        dist.all_gather_object(tilings, self.tiling()[g])
+        self._agree_tiling(tilings)
         self.persistent = True
 
     def check_ipc(self) -> None:

@@ -241,8 +241,20 @@ def remote_ops(grid: ChunkGrid, rank: int) -> list[tuple[str, int, int, int, int
     return ops
 
 
+# Largest initial value for which the unguarded division stays exact: the
+# update never leaves [0, max(M, 1)], so every six-term sum is <= 6M + 2,
+# which for M <= 2^997 stays below div6's 2^1000 range guard
+# (csrc/hrt_jacobi.cu div6).  Above it the sum can overflow to inf, where
+# IEEE gives inf/6 = inf (the reference) but Markstein's correction NaN.
+NONNEG_MAX = 2.0 ** 997
+
+
 def _nonneg(a: np.ndarray) -> bool:
-    return bool(np.isfinite(a).all() and (a >= 0).all())
+    """True when the unguarded-division kernel instances are exact for this
+    initial field: finite, >= 0 and <= NONNEG_MAX."""
+    if a.size == 0:
+        return True
+    return bool(np.isfinite(a).all() and a.min() >= 0 and a.max() <= NONNEG_MAX)
 
 
 def _contiguous(n0, n1, s0, s1) -> bool:
@@ -385,6 +397,15 @@ class JacobiSolver:
             remote_ops.append(self._remote([st, st], total, peer, kind))
         if remote_ops and comm is None:
             raise HrtError("faces cross ranks: an NCCL communicator is required")
+        # Tiling decisions (tile rows, two-step passes) are made once for the
+        # whole decomposition — from the largest chunk count per GPU, which
+        # every rank derives from the same grid — so neighbouring GPUs and
+        # ranks agree on the tiling whose counters and buffers they share.
+        if rank is not None:
+            self.tiling_chunks = max(len(v) for v in grid.per_rank.values())
+        else:
+            self.tiling_chunks = max(sum(1 for lin in owned if placement[lin] == g)
+                                     for g in self.used_gpus)
         for g in self.used_gpus:
             mine = [lin for lin in owned if placement[lin] == g]
             plan = ctypes.c_void_p()
@@ -394,6 +415,7 @@ class JacobiSolver:
                    len(pre[g]), ctypes.byref(plan))
             if rows:
                 N.call("hrt_jacobi_plan_set_rows", plan, rows)
+            N.call("hrt_jacobi_plan_set_tiling_chunks", plan, self.tiling_chunks)
             if variant is not None:
                 N.call("hrt_jacobi_plan_set_variant", plan, variant)
             if g == g0 and remote_ops:
@@ -655,6 +677,21 @@ class JacobiSolver:
                 N.call("hrt_jacobi_plan_set_wave2_remote", self.plans[g],
                        _arr(ctypes.c_uint64, bufs), _arr(ctypes.c_uint64, cnts),
                        _arr(ctypes.c_int32, idxs))
+        self._agree_tiling(list(self.tiling().values()))
+
+    def _agree_tiling(self, every: list) -> None:
+        """Every GPU of a multi-GPU run must share (rows, tiles per chunk)
+        — neighbours index each other's tile counters with their own
+        tiling — and the two-step decision: a two-step GPU never pushes
+        ghost rows and picks buffers by pass parity, so a one-step
+        neighbour would read stale ghosts.  ``every`` holds each GPU's
+        (rows, tiles per chunk, two-step); where only the last differs,
+        two-step passes are turned off on this process' plans."""
+        if len({t[:2] for t in every}) != 1:
+            raise HrtError(f"per-chunk tilings differ across GPUs: {every}")
+        if len({t[2] for t in every}) != 1:
+            for plan in self.plans.values():
+                N.call("hrt_jacobi_plan_set_fuse2", plan, 0)
 
     def _setup_persistent(self) -> None:
         g = self.used_gpus[0]
@@ -684,7 +721,7 @@ class JacobiSolver:
         H2D of the contiguous field, then device-side strided copies.  ``None``
         is the reference's initial state (interior 0.0, jacobi.py:385).
         ``nonneg`` asserts (or, if None, checks on the host) that the data are
-        finite and >= 0, which selects the unguarded division."""
+        finite, >= 0 and <= NONNEG_MAX, which selects the unguarded division."""
         nbytes = self.field_elems * F64
         f = self._field()
         g0 = self.used_gpus[0]
@@ -866,8 +903,9 @@ class JacobiSolver:
         if steps > pp["rsteps"]:
             raise HrtError("run_jobs: steps grew since the first call; use a new solver")
         h2d, d2h = pp["h2d"], pp["d2h"]
-        if nonneg is not None:
-            self._set_nonneg(bool(nonneg))
+        if nonneg is None:  # one host check over every input (the kernel instance is per run)
+            nonneg = all(_nonneg(b.array(np.float64, self.box)) for b in host_ins)
+        self._set_nonneg(bool(nonneg))
         n = len(host_ins)
         in_free = [None, None]     # scatter of the job that last used the input field
         out_free = [None, None]    # D2H of the job that last used the output field
@@ -931,6 +969,16 @@ class JacobiSolver:
         self._check_error()
         out = [h.view(np.float64).copy() if residual else np.zeros(0) for h in hists]
         hpin.close()
+        return out
+
+    def tiling(self) -> dict[int, tuple[int, int, bool]]:
+        """Per GPU: (rows per tile, tiles per chunk, two-step passes)."""
+        out = {}
+        for g in self.used_gpus:
+            r, t, on = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+            N.call("hrt_jacobi_plan_tiling", self.plans[g], ctypes.byref(r), ctypes.byref(t),
+                   ctypes.byref(on))
+            out[g] = (r.value, t.value, bool(on.value))
         return out
 
     @property

@@ -13,6 +13,7 @@ import torch.distributed as dist  # noqa: E402
 
 from paper_2303_02543_b200.distributed import DistributedJacobi, init_process  # noqa: E402
 from paper_2303_02543_b200.jacobi import ChunkGrid  # noqa: E402
+from oracle import oracle as O  # noqa: E402
 
 rank, world, local = init_process("nccl")
 # y faces (strided: packed), x faces (contiguous rows: direct), 3D z faces
@@ -81,8 +82,6 @@ for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
     parts = [None] * world
     dist.all_gather_object(parts, (lo, band, two))
     if rank == 0:
-        from oracle import oracle as O
-
         full = np.empty(dom)
         for (l0, b, _) in parts:
             full[l0[0]:l0[0] + b.shape[0], l0[1]:l0[1] + b.shape[1], l0[2]:l0[2] + b.shape[2]] = b
@@ -94,7 +93,73 @@ for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
         ok_all &= ok
         print(f"dist_check world={world} random {dom} grid={grid} steps={steps} two-step="
               f"{[p[2] for p in parts]}: {'OK' if ok else 'DIFF'}", flush=True)
+# two-step passes across processes split over several run() calls, with a
+# re-upload between jobs: single steps -> fused passes -> the next run's
+# ghost priming after stale ghosts (what bench's job stream does)
+for dom, grid, parts in [((256, 130, 1), (2 * world, 1, 1), (5, 1, 9)),
+                         ((96, 64, 1), (4 * world, 1, 1), (4, 7, 2))]:
+    cg = ChunkGrid(dom, ranks=world, grid=grid)
+    s = DistributedJacobi(cg, rank, world, local)
+    lo, bx = s.box_lo, s.box
+    outs = []
+    for job in range(2):
+        full_init = np.random.default_rng(70 + job).random(dom) * 2.0
+        s.upload(full_init[lo[0]:lo[0] + bx[0], lo[1]:lo[1] + bx[1], lo[2]:lo[2] + bx[2]])
+        for n in parts:
+            s.run(n, residual=False)
+        outs.append((full_init, s.download()))
+    two = s.two_step
+    s.check_ipc()
+    s.close()
+    parts_all = [None] * world
+    dist.all_gather_object(parts_all, (lo, [o[1] for o in outs], two))
+    if rank == 0:
+        ok = True
+        for job, (full_init, _) in enumerate(outs):
+            full = np.empty(dom)
+            for (l0, bands, _) in parts_all:
+                b = bands[job]
+                full[l0[0]:l0[0] + b.shape[0], l0[1]:l0[1] + b.shape[1], l0[2]:l0[2] + b.shape[2]] = b
+            ref = O.jacobi_reference(dom, sum(parts), initial=full_init)
+            ok &= np.array_equal(full, ref)
+        ok_all &= ok
+        print(f"dist_check world={world} split runs {dom} grid={grid} parts={parts} two-step="
+              f"{[p[2] for p in parts_all]}: {'OK' if ok else 'DIFF'}", flush=True)
 del os.environ["HRT_FUSE2"]
+# uneven chunk counts per rank ((2*world-1) x-bands: one rank holds one chunk
+# fewer): every rank must pick the same tiling (rows, two-step) from the
+# grid's largest per-rank chunk count, or neighbours index each other's
+# tile counters wrongly (4096 x 8192 chunks sit at the 256-row / two-step
+# thresholds for 2 vs 1 chunks per GPU)
+for fuse in ("1", "2"):
+    os.environ["HRT_FUSE2"] = fuse
+    nb = 2 * world - 1
+    dom, steps = (nb * 4096, 8192, 1), 21
+    cg = ChunkGrid(dom, ranks=world, grid=(nb, 1, 1))
+    s = DistributedJacobi(cg, rank, world, local)
+    s.upload()
+    s.run(steps, residual=True)
+    res = s.global_residual_history()
+    band, lo = s.download(), s.box_lo
+    til = s.tiling()[local]
+    s.check_ipc()
+    s.close()
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, band, til, len(cg.per_rank[rank])))
+    if rank == 0:
+        from oracle import oracle as O
+
+        full = np.empty(dom)
+        for (l0, b, _, _) in parts:
+            full[l0[0]:l0[0] + b.shape[0]] = b
+        ref, rres = O.jacobi_c(dom, steps, residual=True)
+        ok = np.array_equal(full, ref) and np.array_equal(res, rres)
+        ok &= len({p[2] for p in parts}) == 1
+        ok_all &= ok
+        print(f"dist_check world={world} uneven {dom} chunks/rank={[p[3] for p in parts]} "
+              f"HRT_FUSE2={fuse} tilings={[p[2] for p in parts]}: {'OK' if ok else 'DIFF'}",
+              flush=True)
+    del os.environ["HRT_FUSE2"]
 # full cfg3 size: the N-rank x-band run (IPC wavefront) against one GPU,
 # field bands and residual history bitwise (rank 0 solves the whole domain
 # on its own GPU after the distributed run)

@@ -138,3 +138,21 @@ def test_error_codes_map_to_reference_exceptions():
         with pytest.raises(cls):
             E.raise_for(rc, "x")
     assert issubclass(E.OutOfDeviceMemory, E.HrtError)
+
+
+def test_nonneg_bound_selects_guarded_division():
+    """The unguarded division (Markstein without range checks) is exact only
+    while every six-term sum stays <= 2^1000: fields above 2^997, negative
+    or non-finite keep the guarded instance (reference: inf/6 = inf)."""
+    import numpy as np
+
+    from paper_2303_02543_b200.jacobi import NONNEG_MAX, _nonneg
+
+    assert _nonneg(np.zeros((4, 4, 1)))
+    assert _nonneg(np.full((3, 3, 1), NONNEG_MAX))
+    assert not _nonneg(np.full((3, 3, 1), np.nextafter(NONNEG_MAX, np.inf)))
+    assert not _nonneg(np.array([[[1e308]]]))
+    assert not _nonneg(np.array([[[-0.5]]]))
+    assert not _nonneg(np.array([[[np.inf]]]))
+    assert not _nonneg(np.array([[[np.nan]]]))
+    assert 6 * NONNEG_MAX + 2 <= 2.0 ** 1000

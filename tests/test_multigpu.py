@@ -88,3 +88,36 @@ def test_two_process_pingpong_over_tcp():
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith('{"mode"')]
     assert sorted({(r["mode"], r["size"]) for r in rows}) == sorted(
         (m, s) for m in ("direct", "staged") for s in (8, 448, 449, 65536, 4194304))
+
+
+@pytest.mark.parametrize("fuse", ["1", "2"])
+@pytest.mark.parametrize("dom,grid,ngpus", [((3 * 4096, 8192, 1), (3, 1, 1), 2),
+                                            ((10240, 20480, 1), (8, 1, 1), 3),
+                                            ((2048, 3 * 512, 1), (1, 3, 1), 2)])
+def test_uneven_chunks_per_gpu(oracle, dom, grid, ngpus, fuse, monkeypatch):
+    """Uneven chunk counts per GPU in one process (the reference's device
+    assignment pos*dpr//len gives 2/1, 3/3/2, ...): every GPU must pick the
+    same tile rows and the same one-step/two-step decision — from the
+    largest per-GPU chunk count — since neighbours index each other's tile
+    counters with their own tiling and a two-step GPU pushes no ghosts.
+    4096x8192 chunks sit exactly at the 256-row and two-step thresholds
+    for 2 vs 1 chunks per GPU."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    if ngpu() < ngpus:
+        pytest.skip(f"needs {ngpus} GPUs")
+    monkeypatch.setenv("HRT_FUSE2", fuse)
+    steps = 19
+    s = JacobiSolver(ChunkGrid(dom, ranks=1, devices_per_rank=ngpus, grid=grid),
+                     gpus=list(range(ngpus)))
+    counts = sorted({sum(1 for lin in s.owned if s.placement[lin] == g) for g in s.used_gpus})
+    assert len(counts) > 1, "the placement must be uneven"
+    til = s.tiling()
+    assert len(set(til.values())) == 1, til
+    s.upload()
+    s.run(steps, residual=True)
+    got, res = s.download(), s.residual_history()
+    s.close()
+    ref, rres = oracle.jacobi_c(dom, steps, residual=True)
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
+    assert np.array_equal(res, rres)
