@@ -211,6 +211,63 @@ def barrier(world: int):
         dist.barrier()
 
 
+MSG_SIZES = [8, 64 << 10, 1 << 20, 8 << 20, 64 << 20, 256 << 20]
+NVLINK_GBS = 900.0  # NVLink 5, per direction (nominal)
+
+
+def messages_record():
+    """The metric's second half, "halo msg GB/s vs size" (SURVEY.md §8(d),
+    pingpong.py:126-147): one-way latency and GB/s of a device-resident
+    object through the public message path (``run_pingpong``, path
+    "direct": mp_send with device locators, the copy ordered on the GPU,
+    byte identity verified every round trip), beside the raw copy of the
+    same size timed with CUDA events.  GPU0 <-> GPU1 over NVLink when two
+    GPUs are visible, else a same-GPU D2D copy."""
+    from paper_2303_02543_b200 import _native as N
+    from paper_2303_02543_b200.pingpong import peer_copy_sweep, run_pingpong
+
+    n = N.gpu_count()
+    gpus = [0, 1] if n >= 2 else [0, 0]
+    peer = gpus[0] != gpus[1]
+    hbm, _ = peaks()
+    # a peer copy moves each byte once over the link; a D2D copy reads and
+    # writes HBM, so its size/time ceiling is half the copy peak
+    peak = NVLINK_GBS if peer else hbm / 2
+    raw = peer_copy_sweep(MSG_SIZES, gpus[0], gpus[1], iterations=20)
+    rows = []
+    for size, rr in zip(MSG_SIZES, raw.rows):
+        it = 40 if size < (64 << 20) else 10
+        rep = run_pingpong([size], iterations=it, path="direct", gpus=gpus)
+        r = rep.rows[0]
+        gbs = r["bandwidth_Bps"] / 1e9
+        raw_gbs = rr["bandwidth_Bps"] / 1e9
+        rows.append({"size_bytes": size, "iters": it,
+                     "one_way_us": round(r["mean_latency_s"] * 1e6, 2), "gbs": round(gbs, 3),
+                     "raw_copy_us": round(rr["mean_latency_s"] * 1e6, 2),
+                     "raw_copy_gbs": round(raw_gbs, 2),
+                     "share_of_raw": round(gbs / raw_gbs, 4) if raw_gbs else None,
+                     "frac_of_peak": round(gbs / peak, 4)})
+    return {"path": "mp_send direct (device locator + GPU-ordered copy), run_pingpong",
+            "gpus": gpus, "link": "NVLink 5 peer" if peer else "same-GPU D2D (one GPU visible)",
+            "peak_gbs": peak,
+            "peak_source": "NVLink 5 nominal 900 GB/s per direction" if peer else
+                           "MEASURED_PEAKS.json hbm_gbs / 2 (a D2D copy reads and writes)",
+            "raw": "cudaMemcpyAsync/cudaMemcpyPeerAsync on one stream, CUDA events",
+            "rows": rows}
+
+
+def config_for(wl: dict, world: int, iters: int) -> dict:
+    """The ``config`` object of both arms (ours and --impl reference)."""
+    X, Y, Z = wl["domain"]
+    nchunks = wl["grid"][0] * wl["grid"][1] * wl["grid"][2]
+    return {"workload": wl["desc"], "domain": list(wl["domain"]), "grid": list(wl["grid"]),
+            "iterations_per_step": iters, "chunks_per_gpu": nchunks // world,
+            "parallelism": f"domain decomposition over {world} GPU(s), one process each",
+            "l2": f"no flush needed: field {X * Y * Z * 8 / 2**30:.2f} GiB >> 126 MB L2",
+            "bitexact": "float64 bitwise == reference (Markstein /6 == IEEE, sum order kept)",
+            "residual": "L-inf per iteration, fused"}
+
+
 def run_ours(args):
     from paper_2303_02543_b200 import _native as N
     from paper_2303_02543_b200.devices import PinnedBuffer
@@ -367,12 +424,7 @@ def run_ours(args):
         "ms_per_step": round(region_ms / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the reference's initial state (interior 0.0, Dirichlet faces 1.0)",
-        "config": {"workload": wl["desc"], "domain": list(wl["domain"]), "grid": list(wl["grid"]),
-                   "iterations_per_step": iters, "chunks_per_gpu": len(solver.owned),
-                   "parallelism": f"domain decomposition over {world} GPU(s), one process each",
-                   "l2": f"no flush needed: field {cells * 8 / 2**30:.2f} GiB >> 126 MB L2",
-                   "bitexact": "float64 bitwise == reference (Markstein /6 == IEEE, sum order kept)",
-                   "residual": "L-inf per iteration, fused"},
+        "config": config_for(wl, world, iters),
         "roofline": roofline,
         "e2e": {"value": round(e2e_value, 2) if e2e_value else None, "unit": UNIT,
                 "h2d_bytes_per_step": h2d,
@@ -395,6 +447,8 @@ def run_ours(args):
     else:
         line["cpu_baseline"] = None
     solver.close()
+    if world == 1 and not args.no_messages:
+        line["messages"] = messages_record()
     if world == 1 and args.workload == "auto" and not args.no_scaling_baseline:
         # N>1 lines measure cfg3 (strong scaling); give the same workload at
         # N=1 so per-N efficiency can be read on one configuration
@@ -470,15 +524,15 @@ def run_reference(args):
     value = X * Y * per_step * args.steps / dt / 1e9
     cores = O.cpu_threads()
     sample = (f"{X}x{Y} slab, {per_step} of the {wl["iters"]} sweeps per step (field setup "
-              f"excluded), oracle/jacobi_oracle.c OpenMP port of jacobi.py:49-67")
+              f"excluded; GLUPS is a per-update rate, so the bounded sample measures the same "
+              f"quantity), oracle/jacobi_oracle.c OpenMP port of jacobi.py:49-67")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: the reference's initial state",
-        "config": {"workload": wl["desc"], "domain": list(wl["domain"]), "grid": list(wl["grid"]),
-                   "iterations_per_step": per_step},
+        "config": config_for(wl, world, args.iters or wl["iters"]),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -504,6 +558,8 @@ def main():
                     help="ncu dram bytes per update launch (from profiles/)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-scaling-baseline", action="store_true")
+    ap.add_argument("--no-messages", action="store_true",
+                    help="skip the message-bandwidth record (N=1)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-budget", type=float, default=3.0)
     args = ap.parse_args()

@@ -306,6 +306,10 @@ int hrt_np_sum(void *stream, const double *a, int64_t n, double *out);
  * read-modify-write task body for runtime ordering tests (the reference's
  * writer_body, test_acceptance.py:310-312) */
 int hrt_mix_u8(void *stream, uint8_t *dst, const uint8_t *src, int64_t n, int salt);
+/* one-thread kernel that spins `ns` ns and stores its [start, end]
+ * %globaltimer interval at slot[0..1] (device memory): the executor's
+ * overlap witness (AC-02 analogue, test_acceptance.py:67-96) */
+int hrt_spin_stamp(void *stream, uint64_t *slot, uint64_t ns);
 /* self-check of the Markstein division used by the update kernel against
  * IEEE division: n hashed samples (mode 0 uniform [0,6), 1 near 1/2/3/6,
  * 2 random finite bit patterns); synchronises */

@@ -149,6 +149,7 @@ SIGNATURES = {
     "hrt_np_sum": (c_int, [c_void_p, c_void_p, c_i64, P(c_d)]),
     "hrt_div6_sweep": (c_int, [c_void_p, c_u64, c_i64, c_int, P(c_u64), P(c_d)]),
     "hrt_mix_u8": (c_int, [c_void_p, c_void_p, c_void_p, c_i64, c_int]),
+    "hrt_spin_stamp": (c_int, [c_void_p, c_void_p, c_u64]),
     "hrt_nccl_unique_id": (c_int, [c_char_p]),
     "hrt_nccl_init": (c_int, [c_int, c_int, c_int, c_char_p, P(c_void_p)]),
     "hrt_nccl_destroy": (c_int, [c_void_p]),

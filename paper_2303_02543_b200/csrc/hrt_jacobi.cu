@@ -4201,6 +4201,28 @@ int hrt_mix_u8(void* stream, uint8_t* dst, const uint8_t* src, int64_t n, int sa
     return HRT_OK;
 }
 
+// executor witness kernel: spins `ns` nanoseconds and stores its own
+// [start, end] %globaltimer interval (one GPU's clock) into slot[0..1]
+__global__ void spin_stamp_kernel(unsigned long long* slot, unsigned long long ns) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+    slot[0] = t0;
+    slot[1] = t;
+}
+
+int hrt_spin_stamp(void* stream, uint64_t* slot, uint64_t ns) {
+    HRT_CHECK_ARG(stream && slot && ns <= 10000000000ull, "bad spin arguments");
+    Stream* st = as_stream(stream);
+    int rc = use_device(st->gpu);
+    if (rc) return rc;
+    spin_stamp_kernel<<<1, 1, 0, st->s>>>(reinterpret_cast<unsigned long long*>(slot), ns);
+    HRT_CUDA(cudaGetLastError());
+    return HRT_OK;
+}
+
 int hrt_div6_sweep(void* stream, uint64_t seed, int64_t n, int mode, uint64_t* mismatches,
                    double* first_bad) {
     HRT_CHECK_ARG(stream && mismatches, "null argument");

@@ -146,3 +146,20 @@ class Mix(NativeKernel):
 
 def dtype_of(view) -> np.dtype:
     return np.dtype(getattr(view, "dtype", np.uint8))
+
+
+class Stamp(NativeKernel):
+    """Spin ``ns`` nanoseconds on the GPU and record the kernel's own
+    [start, end] %globaltimer interval at device address ``slot`` (two
+    uint64): the witness that conflicting tasks never overlap and
+    independent ones do (AC-02, test_acceptance.py:67-96).  Touches no view."""
+
+    name = "stamp"
+
+    def __init__(self, slot: int, ns: int = 100_000):
+        self.slot = int(slot)
+        self.ns = int(ns)
+
+    def __call__(self, views, geometry, scratch, stream) -> None:
+        N.call("hrt_spin_stamp", stream.h, ctypes.c_void_p(self.slot), ctypes.c_uint64(self.ns))
+

@@ -92,6 +92,7 @@ def test_overflowing_nonneg_field_matches_reference(solver_mod, oracle, dom, gri
     init = rng.random(dom)
     hot = rng.random(dom) < 0.05
     init[hot] = 1e308 * rng.random(int(hot.sum()))
+    init[2:5, 3:6, :] = 1.5e308   # a hot block: neighbour sums overflow at step 1
     got, res, _, _, _, nonneg = _solve(solver_mod, dom, grid, steps, init)
     assert nonneg is False
     ref, rref = oracle.jacobi_c(dom, steps, residual=True, initial=init)
@@ -99,6 +100,11 @@ def test_overflowing_nonneg_field_matches_reference(solver_mod, oracle, dom, gri
     assert np.array_equal(got, ref, equal_nan=True), np.argwhere(~((got == ref) | (
         np.isnan(got) & np.isnan(ref))))[:4]
     assert np.array_equal(res, rref, equal_nan=True), (res, rref)
+    if dom[2] == 1:
+        # the hazard the bound removes: forcing the unguarded instance on
+        # this field gives NaN where the reference has inf
+        bad = _solve(solver_mod, dom, grid, steps, init, nonneg=True)[0]
+        assert np.isnan(bad).any() and not np.isnan(ref).any()
 
 
 def test_overflow_through_run_jobs_default_check(solver_mod, oracle):
