@@ -534,8 +534,7 @@ class Comm:
 
             def granted(r: Runtime, op: AccessOp) -> None:
                 tok = self._device_copy(device, alloc, loc, size, wait + op.wait_tokens)
-                ci.state = CopyState.VALID
-                ci.token = tok
+                ci.catch_up(tok)   # the wrapper's first bytes (written flips on landing)
                 r.access_launched(op, tok)
                 # ``written`` flips once the bytes have landed (comm.py:837)
                 r._watch(tok, lambda t: setattr(wrapper, "written", True))
@@ -564,8 +563,7 @@ class Comm:
                 wrapper.copies[device] = ci
                 self.stats.staging_copies += 1
                 tok = r.registry.enqueue_transfer(region, alloc, wrapper.total_size)
-                ci.state = CopyState.VALID
-                ci.token = tok
+                ci.catch_up(tok)   # the wrapper's first bytes (written flips on landing)
                 r.access_launched(op, tok)
 
             rt.register_access(wrapper, AccessMode.WRITE, granted_s, label="recv",
@@ -630,12 +628,7 @@ class Comm:
             ci = obj.copies[target]
             tok = self._device_copy(target, ci.allocation, loc, obj.total_size,
                                     list(wait) + op.wait_tokens)
-            for d, c in obj.copies.items():
-                c.state = CopyState.VALID if d == target else CopyState.STALE
-            ci.token = tok
-            if obj.host_region is not None:
-                obj.host_state = CopyState.STALE
-            obj.written = True
+            obj.publish(target, tok)
             r.access_launched(op, tok)
             loc.on_copied(tok)
             self._enqueue_handler(src, hid, None, obj)
