@@ -32,9 +32,6 @@
 
 #include "hrt_common.cuh"
 
-#ifndef HRT_WAVE_NOFENCE
-#define HRT_WAVE_NOFENCE 0
-#endif
 
 namespace hrt {
 
@@ -58,6 +55,12 @@ __device__ __forceinline__ double div6(double s) {
     if ((a < 0x1p-1019 && a != 0.0) || !(a <= 0x1p1000)) q = div6_ieee(s);
     return q;
 #endif
+}
+
+// variant 3 (the independent check path of run_jacobi3d(check=True)):
+// plain IEEE division, no Markstein correction
+__device__ __forceinline__ double div6_sel(double s, int ieee) {
+    return ieee ? __ddiv_rn(s, 6.0) : div6(s);
 }
 
 __device__ __forceinline__ double sum6(double xm, double xp, double ym, double yp, double zm,
@@ -138,6 +141,7 @@ struct SlabArgs {
     int64_t tiles_r, tiles_c;
     unsigned long long* resid;  // nullable: L-inf residual slot for this step
     double zghost;         // the two constant z ghosts (BOUNDARY)
+    int ieee;              // LDG kernel: IEEE __ddiv_rn instead of Markstein (variant 3)
 };
 
 __global__ void __launch_bounds__(SLAB_THREADS)
@@ -211,8 +215,8 @@ slab_update_kernel(SlabArgs a) {
             const double2 dn = nb[k];
             if (act) {
                 double2 o;
-                o.x = div6(sum6(up.x, dn.x, lx, mid.y, zg, zg));
-                o.y = div6(sum6(up.y, dn.y, mid.x, ry, zg, zg));
+                o.x = div6_sel(sum6(up.x, dn.x, lx, mid.y, zg, zg), a.ieee);
+                o.y = div6_sel(sum6(up.y, dn.y, mid.x, ry, zg, zg), a.ieee);
                 double* dst = w + r * a.sx + j;
                 if (both) {
                     *reinterpret_cast<double2*>(dst) = o;
@@ -995,7 +999,7 @@ slab_wave_kernel(WaveArgs wa) {
         const int* rp = wa.rpeer ? wa.rpeer + 4 * c : nullptr;
         const bool xedge = rp && ((rb == 0 && rp[0] >= 0) || (rb == a.tiles_r - 1 && rp[1] >= 0) ||
                                   (cb == 0 && rp[2] >= 0) || (cb == a.tiles_c - 1 && rp[3] >= 0));
-        if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         if (xedge) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
         if (tid == 0) {
@@ -1005,7 +1009,7 @@ slab_wave_kernel(WaveArgs wa) {
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
                              : "memory");
             } else {
-                if (!HRT_WAVE_NOFENCE) __threadfence();
+                __threadfence();
                 st_release_gpu_u32(wa.done + tile, v);
             }
         }
@@ -1278,53 +1282,19 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a,
 }
 
 #ifndef HRT_W2_MINB4
-#define HRT_W2_MINB4 3   // resident CTAs/SM the registers target: 4 cols/thread, 512 wide
+#define HRT_W2_MINB4 3   // resident CTAs/SM the registers target: 512-wide tiles
 #endif
 #ifndef HRT_W2_MINB2
-#define HRT_W2_MINB2 5   // 4 cols/thread, 256 wide
+#define HRT_W2_MINB2 5   // 256-wide tiles (chunks at most 256 wide)
 #endif
-#ifndef HRT_W2_MINB8
-#define HRT_W2_MINB8 2   // 2 cols/thread, 512 wide (8 consumer warps)
-#endif
-#ifndef HRT_W2_MINB4N
-#define HRT_W2_MINB4N 3  // 2 cols/thread, 256 wide
-#endif
-#ifndef HRT_W2_MAXNREG
-#define HRT_W2_MAXNREG 0  // >0: 4x4 two-step consumers grow to this many registers
-#endif
-#ifndef HRT_W2_PREG
-#define HRT_W2_PREG 32    // producer warp registers after setmaxnreg.dec
-#endif
-#ifndef HRT_W2_MREG_MINB
-#define HRT_W2_MREG_MINB 4
-#endif
-                   // (setmaxnreg), the producer warp shrinks to 24
-__host__ __device__ constexpr bool w2_mreg(int cw, int cpt) { return HRT_W2_MAXNREG > 0 && cw == 4 && cpt == 4; }
-// with setmaxnreg the producer is a whole warpgroup (4 warps; 3 leave at once)
-__host__ __device__ constexpr int w2_threads(int cw, int cpt) {
-    return 32 * (cw + (w2_mreg(cw, cpt) ? 4 : 1));
-}
-constexpr int w2_minb(int cw, int cpt) {
-    return w2_mreg(cw, cpt) ? HRT_W2_MREG_MINB : cpt == 4 ? (cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4)
-                    : (cw == 8 ? HRT_W2_MINB8 : HRT_W2_MINB4N);
-}
-#ifndef HRT_W2_DSTAGES
-#define HRT_W2_DSTAGES 0  // >0: ring of this many stages in dynamic shared memory
-#endif
-constexpr int W2_STAGES = HRT_W2_DSTAGES > 0 ? HRT_W2_DSTAGES : T4_STAGES;
-// dynamic shared memory bytes of slab_wave2_kernel<*, *, CW, CPT>
-constexpr size_t w2_smem(int cw, int cpt) {
-    return HRT_W2_DSTAGES > 0 ? (size_t)HRT_W2_DSTAGES * (32 * cpt * cw + 4) * sizeof(double) : 0;
-}
+// CW consumer warps (4 columns per thread) + one producer warp
+__host__ __device__ constexpr int w2_threads(int cw) { return 32 * (cw + 1); }
+constexpr int w2_minb(int cw) { return cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4; }
+constexpr int W2_STAGES = T4_STAGES;
 template <bool GUARD, bool RESID, int CW, int CPT = 4, int STAGES = W2_STAGES>
-__global__ void __launch_bounds__(w2_threads(CW, CPT), w2_minb(CW, CPT))
+__global__ void __launch_bounds__(w2_threads(CW), w2_minb(CW))
 slab_wave2_kernel(Wave2Args wa) {
-#if HRT_W2_DSTAGES > 0
-    extern __shared__ __align__(128) unsigned char w2_dyn_smem[];
-    auto ring = reinterpret_cast<double(*)[32 * CPT * CW + 4]>(w2_dyn_smem);
-#else
     __shared__ alignas(128) double ring[STAGES][(32 * CPT * CW + 4)];
-#endif
     __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
         tq_empty[WAVE_TQ];
     __shared__ long long tq[WAVE_TQ];
@@ -1354,9 +1324,7 @@ slab_wave2_kernel(Wave2Args wa) {
     int s = 0;
     uint32_t ph = 0;
     if (warp >= CW) {
-        if constexpr (w2_mreg(CW, CPT))
-            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(HRT_W2_PREG));
-        if (warp != CW || lane != 0) return;
+        if (lane != 0) return;
         bool dead = false;
         int slot = 0;
         uint32_t tph = 0;
@@ -1376,29 +1344,7 @@ slab_wave2_kernel(Wave2Args wa) {
             const int64_t rem = tile - c * per_chunk;
             const int64_t rb = rem / tc;
             const int64_t cb = rem - rb * tc;
-            if (w2_mreg(CW, CPT) && !dead) {
-                // lean producer (24-64 registers after setmaxnreg.dec): the
-                // neighbourhood one tile row at a time, three counters in flight
-                const unsigned need = wa.base + 2u * (unsigned)k;
-                const Nbr9& n9 = wa.n9[c];
-#pragma unroll 1
-                for (int dr = 0; dr < 3 && !dead; ++dr) {
-                    const unsigned int* q[3];
-                    bool sys[3];
-#pragma unroll
-                    for (int dc = 0; dc < 3; ++dc) {
-                        const int64_t r2 = rb + dr - 1, c2 = cb + dc - 1;
-                        const int ci = r2 < 0 ? -1 : (r2 >= tr ? 1 : 0);
-                        const int cj = c2 < 0 ? -1 : (c2 >= tc ? 1 : 0);
-                        const int e = (ci + 1) * 3 + (cj + 1);
-                        const unsigned int* base = n9.cnt[e];
-                        q[dc] = base ? base + (r2 - ci * tr) * tc + (c2 - cj * tc) : nullptr;
-                        sys[dc] = (n9.sysmask >> e) & 1u;
-                    }
-                    dead = !wait_counters<3>(q, sys, need, wa.timeout_ns, wa.err);
-                }
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-            } else if (!dead) {
+            if (!dead) {
                 // the 3 x 3 tile neighbourhood must be done with step base+2k
                 const unsigned need = wa.base + 2u * (unsigned)k;
                 const Nbr9& n9 = wa.n9[c];
@@ -1424,8 +1370,6 @@ slab_wave2_kernel(Wave2Args wa) {
         }
         return;
     }
-    if constexpr (w2_mreg(CW, CPT))
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(HRT_W2_MAXNREG));
     int slot = 0;
     uint32_t tph = 0;
     for (;;) {
@@ -1462,7 +1406,7 @@ slab_wave2_kernel(Wave2Args wa) {
         const unsigned sm = wa.n9[c].sysmask;
         const bool xedge = sm && ((rb == 0 && (sm & 0x7u)) || (rb == tr - 1 && (sm & 0x1C0u)) ||
                                   (cb == 0 && (sm & 0x49u)) || (cb == tc - 1 && (sm & 0x124u)));
-        if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         if (xedge) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
         if (tid == 0) {
@@ -1482,7 +1426,7 @@ slab_wave2_kernel(Wave2Args wa) {
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
                              : "memory");
             } else {
-                if (!HRT_WAVE_NOFENCE) __threadfence();
+                __threadfence();
                 st_release_gpu_u32(wa.done + tile, v);
             }
         }
@@ -1516,6 +1460,7 @@ struct VolArgs {
     int64_t rows;
     int64_t tiles_i, tiles_j, tiles_k;
     int flat;                  // ez == 1 stored with z ghosts: threads tile j only
+    int ieee;                  // LDG kernel: IEEE __ddiv_rn instead of Markstein (variant 3)
     unsigned long long* resid;
     const VolPush* vpush;      // null: no fused push
 };
@@ -2099,7 +2044,7 @@ volume_wave_kernel(VolWaveArgs wa) {
         const bool xedge = rp && ((ti == 0 && rp[0] >= 0) || (ti == a.tiles_i - 1 && rp[1] >= 0) ||
                                   (tj == 0 && rp[2] >= 0) || (tj == a.tiles_j - 1 && rp[3] >= 0) ||
                                   (tk == 0 && rp[4] >= 0) || (tk == a.tiles_k - 1 && rp[5] >= 0));
-        if (!HRT_WAVE_NOFENCE) asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         if (xedge) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * V_CW));
         if (tid == 0) {
@@ -2115,7 +2060,7 @@ volume_wave_kernel(VolWaveArgs wa) {
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
                              : "memory");
             } else {
-                if (!HRT_WAVE_NOFENCE) __threadfence();
+                __threadfence();
                 st_release_gpu_u32(wa.done + tile, v);
             }
         }
@@ -2155,8 +2100,8 @@ volume_update_kernel(VolArgs a) {
         for (int64_t i = i0; i <= i1; ++i) {
             const double* p = u + i * a.sx + col;
             const double dn = __ldg(p + a.sx);
-            const double nv = div6(sum6(up, dn, __ldg(p - a.sy), __ldg(p + a.sy), __ldg(p - 1),
-                                        __ldg(p + 1)));
+            const double nv = div6_sel(sum6(up, dn, __ldg(p - a.sy), __ldg(p + a.sy),
+                                            __ldg(p - 1), __ldg(p + 1)), a.ieee);
             w[i * a.sx + col] = nv;
             rmax = rmax_acc(rmax, fabs(__dsub_rn(nv, mid)));
             up = mid;
@@ -2439,7 +2384,7 @@ struct Plan {
     bool ghosts_ready = false;    // ghost planes of the next buffer are current
     bool push_on() const { return d_push != nullptr && L.ndim == 2 && variant == 2; }
     bool vpush_on() const {
-        return d_vpush != nullptr && L.ndim == 3 && variant != 0 && L.origin % 2 == 1 &&
+        return d_vpush != nullptr && L.ndim == 3 && variant != 0 && variant != 3 && L.origin % 2 == 1 &&
                L.stride[1] % 2 == 0;
     }
     bool any_push() const { return push_on() || vpush_on(); }
@@ -2592,6 +2537,7 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.tiles_c = (a.ey + cols - 1) / cols;
         a.resid = resid;
         a.zghost = HRT_BOUNDARY;
+        a.ieee = p->variant == 3;
         const int64_t grid = subset == 1   ? p->n_edge
                              : subset == 2 ? p->n_inner
                              : subset == 3 ? p->n_edge + p->n_inner
@@ -2639,10 +2585,12 @@ static int launch_update(Plan* p, cudaStream_t s, int parity, unsigned long long
         a.du = nullptr;
         a.dw = nullptr;
         a.flat = 0;
+        a.ieee = p->variant == 3;
         a.resid = resid;
         a.vpush = p->vpush_on() ? p->d_vpush : nullptr;
         // TMA ring variant needs 16-byte aligned z rows (origin odd, sy even)
-        const bool tma = p->variant != 0 && (L.origin % 2 == 1) && (L.stride[1] % 2 == 0);
+        const bool tma = p->variant != 0 && p->variant != 3 && (L.origin % 2 == 1) &&
+                         (L.stride[1] % 2 == 0);
         if (tma) {
             a.tiles_j = (a.ey + V_CW - 1) / V_CW;
             a.tiles_k = (a.ez + V_ZW - 1) / V_ZW;
@@ -2689,20 +2637,13 @@ static void set_carveouts() {
     carveout(slab_wave_kernel<true, false, 2>);
     carveout(slab_wave_kernel<false, true, 2>);
     carveout(slab_wave_kernel<false, false, 2>);
-#define C2(CW, CPT)                                   \
-    carveout(slab_wave2_kernel<true, true, CW, CPT>);   \
-    carveout(slab_wave2_kernel<true, false, CW, CPT>);  \
-    carveout(slab_wave2_kernel<false, true, CW, CPT>);  \
-    carveout(slab_wave2_kernel<false, false, CW, CPT>);                                          \
-    cudaFuncSetAttribute(slab_wave2_kernel<true, true, CW, CPT>,                                  \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT));     \
-    cudaFuncSetAttribute(slab_wave2_kernel<true, false, CW, CPT>,                                 \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT));     \
-    cudaFuncSetAttribute(slab_wave2_kernel<false, true, CW, CPT>,                                 \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT));     \
-    cudaFuncSetAttribute(slab_wave2_kernel<false, false, CW, CPT>,                                \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)w2_smem(CW, CPT))
-    C2(4, 4); C2(2, 4); C2(8, 2); C2(4, 2);
+#define C2(CW)                                    \
+    carveout(slab_wave2_kernel<true, true, CW>);    \
+    carveout(slab_wave2_kernel<true, false, CW>);   \
+    carveout(slab_wave2_kernel<false, true, CW>);   \
+    carveout(slab_wave2_kernel<false, false, CW>)
+    C2(4);
+    C2(2);
 #undef C2
     carveout(slab_update_tma_kernel);
     carveout(volume_update_tma_kernel<true>);
@@ -2997,32 +2938,22 @@ static bool fuse2_use(const Plan* p) {
     return per_chunk * p->tn() >= fuse2_slots(p);
 }
 
-template <int CW, int CPT>
+template <int CW>
 static int wave2_occupancy(bool guard) {
-    int dev = 0, sms = 0, a = 0, b = 0;
+    int dev = 0, a = 0, b = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (guard) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW, CPT>,
-                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW, CPT>,
-                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW>,
+                                                      w2_threads(CW), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW>,
+                                                      w2_threads(CW), 0);
     } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW, CPT>,
-                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW, CPT>,
-                                                      w2_threads(CW, CPT), w2_smem(CW, CPT));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW>,
+                                                      w2_threads(CW), 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW>,
+                                                      w2_threads(CW), 0);
     }
-    return std::min(a, b) * sms;
-}
-
-// columns per consumer thread of the two-step kernel (HRT_W2_CPT: 4 or 2)
-static int w2_cpt() {
-    static const int v = [] {
-        const char* e = getenv("HRT_W2_CPT");
-        return (e && e[0] == '2') ? 2 : 4;
-    }();
-    return v;
+    return std::min(a, b) * sm_count(dev);
 }
 
 // nf passes (2 steps each) from step `first` in one slab_wave2_kernel launch
@@ -3082,11 +3013,7 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     }
     const int64_t key2 = T * 4 + (p->nonneg ? 1 : 0);
     if (p->pgrid2 == 0 || p->pkey2 != key2) {
-        const bool c2 = w2_cpt() == 2;
-        p->pgrid2 = narrow ? (c2 ? wave2_occupancy<4, 2>(!p->nonneg)
-                                 : wave2_occupancy<2, 4>(!p->nonneg))
-                           : (c2 ? wave2_occupancy<8, 2>(!p->nonneg)
-                                 : wave2_occupancy<4, 4>(!p->nonneg));
+        p->pgrid2 = narrow ? wave2_occupancy<2>(!p->nonneg) : wave2_occupancy<4>(!p->nonneg);
         HRT_CUDA(cudaGetLastError());
         if (p->pgrid2 <= 0) {
             set_error("two-step kernel: no resident CTA slots");
@@ -3119,21 +3046,13 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     const bool guard = !p->nonneg, res = resid_base != nullptr;
     void* fn;
     int threads;
-#define WK2(G, R, CW, CPT) (void*)slab_wave2_kernel<G, R, CW, CPT>
-#define PICK(CW, CPT)                                                        \
-    (guard ? (res ? WK2(true, true, CW, CPT) : WK2(true, false, CW, CPT))    \
-           : (res ? WK2(false, true, CW, CPT) : WK2(false, false, CW, CPT)))
-    const bool c2 = w2_cpt() == 2;
-    size_t smem;
-    if (narrow) {
-        fn = c2 ? PICK(4, 2) : PICK(2, 4);
-        threads = c2 ? w2_threads(4, 2) : w2_threads(2, 4);
-        smem = c2 ? w2_smem(4, 2) : w2_smem(2, 4);
-    } else {
-        fn = c2 ? PICK(8, 2) : PICK(4, 4);
-        threads = c2 ? w2_threads(8, 2) : w2_threads(4, 4);
-        smem = c2 ? w2_smem(8, 2) : w2_smem(4, 4);
-    }
+#define WK2(G, R, CW) (void*)slab_wave2_kernel<G, R, CW>
+#define PICK(CW)                                                \
+    (guard ? (res ? WK2(true, true, CW) : WK2(true, false, CW))  \
+           : (res ? WK2(false, true, CW) : WK2(false, false, CW)))
+    const size_t smem = 0;
+    fn = narrow ? PICK(2) : PICK(4);
+    threads = w2_threads(narrow ? 2 : 4);
 #undef PICK
 #undef WK2
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid2, T);
@@ -3567,7 +3486,7 @@ int hrt_jacobi_plan_set_rows(void* plan, int64_t rows) {
 }
 
 int hrt_jacobi_plan_set_variant(void* plan, int variant) {
-    HRT_CHECK_ARG(plan && variant >= 0 && variant <= 2, "variant must be 0, 1 or 2");
+    HRT_CHECK_ARG(plan && variant >= 0 && variant <= 3, "variant must be 0, 1, 2 or 3");
     Plan* p = reinterpret_cast<Plan*>(plan);
     p->variant = variant;
     if (p->graph) {

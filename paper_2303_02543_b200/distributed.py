@@ -21,7 +21,7 @@ import numpy as np
 from . import _native as N
 from .devices import DevicePool
 from .errors import HrtError
-from .jacobi import ChunkGrid, JacobiSolver, _arr, face_plane, opposite
+from .jacobi import ChunkGrid, JacobiSolver, _arr, face_plane, opposite, persist_timeout_ns
 
 
 def env_rank() -> tuple[int, int, int]:
@@ -227,7 +227,8 @@ class DistributedJacobi(JacobiSolver):
         nbr = [index.get(self.grid.chunks[lin].neighbors.get(f), -1)
                if self.grid.chunks[lin].neighbors.get(f) is not None else -1
                for lin in mine for f in range(nf)]
-        N.call("hrt_jacobi_plan_set_persistent", plan, _arr(ctypes.c_int32, nbr), 0)
+        N.call("hrt_jacobi_plan_set_persistent", plan, _arr(ctypes.c_int32, nbr),
+               persist_timeout_ns())
         ptr, ntiles = ctypes.c_uint64(), ctypes.c_int64()
         N.call("hrt_jacobi_plan_wave_counters", plan, ctypes.byref(ptr), ctypes.byref(ntiles))
         h = ctypes.create_string_buffer(64)
