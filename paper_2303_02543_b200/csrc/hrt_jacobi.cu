@@ -1115,37 +1115,92 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[W 
     }
 }
 
+#ifndef W2_EARLY
+#define W2_EARLY 1
+#endif
+// ---- shared-memory helpers on 32-bit shared addresses (computed once per
+// tile: a generic->shared conversion per row cost an S2R of the CTA id, a
+// LEA and an IMAD on every row) ----
+__device__ __forceinline__ bool mbar_try_u32(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __noinline__ void mbar_wait_u32_slow(uint32_t bar, uint32_t parity) {
+    unsigned long long t0 = 0;
+    unsigned n = 0;
+    while (!mbar_try_u32(bar, parity)) {
+        if ((++n & 0xFFFFu) == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 20000000000ULL) __trap();
+        }
+    }
+}
+// one lane arrives (a predicated instruction: no divergent branch)
+__device__ __forceinline__ void mbar_arrive_lane0_u32(uint32_t bar, int lane) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.eq.s32 p, %1, 0;\n\t"
+        "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar),
+        "r"(lane)
+        : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+// |x| on the integer pipe (a DADD with |.| would take an FP64 issue slot)
+__device__ __forceinline__ double abs_bits(double x) {
+    return __hiloint2double(__double2hiint(x) & 0x7fffffff, __double2loint(x));
+}
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
 // Per-thread state of the two-step consumer (one tile).
 struct W2Ctx {
-    const Wave2Args* a;
-    double* ringp;          // ring base (double*), stage stride RS doubles
-    uint64_t* full;
-    uint64_t* empty;
+    uint32_t ring;          // shared address of this thread's column span in stage 0
+    uint32_t full, empty;   // shared addresses of the barrier arrays
     int s;
     uint32_t ph;
-    int p, lane, nv;
+    bool ready;             // the current stage's full barrier was seen complete
+    int lane, nv;
     unsigned cghost;
     bool mask, out_n, out_s;
-    int64_t i0, i1;
+    int qlast;              // last ring row whose u(t+1) row is inside the tile
+    int64_t i0, ex, sx;
     double* wr;
     double zg, r1, r2;
 };
 
-// u(t) rows live in double2 register pairs so each LDS.128 lands in place
-// (a plain double array made ptxas stage the loads and move them)
+// Take the next ring row: wait for its stage (unless an earlier poll saw it
+// complete), read this thread's span, hand the stage back to the producer,
+// and poll the following stage now so its barrier latency overlaps this
+// row's arithmetic instead of stalling the next take.
 template <int RS, int STAGES, int NP>
 __device__ __forceinline__ void w2_take(W2Ctx& x, double2 (&v)[NP]) {
-    mbar_wait(&x.full[x.s], x.ph);
-    const double* row = x.ringp + (size_t)x.s * RS + x.p;
+    const uint32_t fb = x.full + 8u * (uint32_t)x.s;
+    if (!x.ready && !mbar_try_u32(fb, x.ph)) mbar_wait_u32_slow(fb, x.ph);
+    const uint32_t row = x.ring + (uint32_t)(x.s * RS * 8);
 #pragma unroll
-    for (int k = 0; k < NP; ++k) v[k] = *reinterpret_cast<const double2*>(row + 2 * k);
+    for (int k = 0; k < NP; ++k) v[k] = lds_f64x2(row + 16u * k);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
     __syncwarp();
-    if (x.lane == 0) mbar_arrive(&x.empty[x.s]);
+    mbar_arrive_lane0_u32(x.empty + 8u * (uint32_t)x.s, x.lane);
     if (++x.s == STAGES) {
         x.s = 0;
         x.ph ^= 1;
     }
+#if W2_EARLY
+    x.ready = mbar_try_u32(x.full + 8u * (uint32_t)x.s, x.ph);
+#endif
 }
 
 template <int NP>
@@ -1155,61 +1210,75 @@ __device__ __forceinline__ double w2_e(const double2 (&v)[NP], int m) {
 
 // one ring row q: u(t) row r+1 arrives in `dn`; u(t+1) row r (r = i0-3+q)
 // goes into `u1n` (the slot of row r-3); u(t+2) row r-1 from u(t+1) rows
-// r-2 (`u1a`), r-1 (`u1b`), r (`u1n`)
-template <bool GUARD, bool RESID, int RS, int STAGES, int CPT>
+// r-2 (`u1a`), r-1 (`u1b`), r (`u1n`).  Per-row residual maxima are folded
+// as a tree (two independent compares, then one into the running max).
+template <bool GUARD, bool RESID, bool FULL, int RS, int STAGES, int CPT>
 __device__ __forceinline__ void w2_row(W2Ctx& x, const double2 (&up)[CPT / 2 + 2],
                                        const double2 (&mid)[CPT / 2 + 2],
                                        double2 (&dn)[CPT / 2 + 2], const double (&u1a)[CPT + 2],
                                        const double (&u1b)[CPT + 2], double (&u1n)[CPT + 2],
                                        int q) {
+    static_assert(CPT == 4, "the residual tree assumes four columns per thread");
     w2_take<RS, STAGES, CPT / 2 + 2>(x, dn);
-    const int64_t r = x.i0 - 3 + q;
     const double zg = x.zg;
 #pragma unroll
     for (int m = 0; m < CPT + 2; ++m)
         u1n[m] = div6_t<GUARD>(sum6(w2_e(up, m + 1), w2_e(dn, m + 1), w2_e(mid, m),
                                     w2_e(mid, m + 2), zg, zg));
     if (x.mask) {
-        const bool rghost = (r < 1 && x.out_n) || (r > x.a->ex && x.out_s);
+        const int64_t r = x.i0 - 3 + q;
+        const bool rghost = (r < 1 && x.out_n) || (r > x.ex && x.out_s);
 #pragma unroll
         for (int m = 0; m < CPT + 2; ++m)
             if (rghost || ((x.cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
     }
-    if (RESID && r >= x.i0 && r <= x.i1) {
-        if (x.nv == CPT) {
+    if (RESID && q >= 3 && q <= x.qlast) {  // u(t+1) row r = i0-3+q inside [i0, i1]
+        double d[CPT];
 #pragma unroll
-            for (int k = 0; k < CPT; ++k)
-                x.r1 = rmax_acc(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
-        } else {
-#pragma unroll
-            for (int k = 0; k < CPT; ++k)
-                if (k < x.nv) x.r1 = rmax_acc(x.r1, fabs(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))));
-        }
+        for (int k = 0; k < CPT; ++k)
+            d[k] = (FULL || k < x.nv) ? abs_bits(__dsub_rn(u1n[k + 1], w2_e(mid, k + 2))) : 0.0;
+        x.r1 = dmax(x.r1, dmax(dmax(d[0], d[1]), dmax(d[2], d[3])));
     }
     if (q >= 4) {
         double o[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k)
             o[k] = div6_t<GUARD>(sum6(u1a[k + 1], u1n[k + 1], u1b[k], u1b[k + 2], zg, zg));
-        if (x.nv == CPT) {
+        if (FULL) {
 #pragma unroll
             for (int k = 0; k < CPT; k += 2)
                 *reinterpret_cast<double2*>(x.wr + k) = make_double2(o[k], o[k + 1]);
-            if (RESID) {
-#pragma unroll
-                for (int k = 0; k < CPT; ++k)
-                    x.r2 = rmax_acc(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
-            }
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k)
-                if (k < x.nv) {
-                    x.wr[k] = o[k];
-                    if (RESID) x.r2 = rmax_acc(x.r2, fabs(__dsub_rn(o[k], u1b[k + 1])));
-                }
+                if (k < x.nv) x.wr[k] = o[k];
         }
-        x.wr += x.a->sx;
+        if (RESID) {
+            double d[CPT];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k)
+                d[k] = (FULL || k < x.nv) ? abs_bits(__dsub_rn(o[k], u1b[k + 1])) : 0.0;
+            x.r2 = dmax(x.r2, dmax(dmax(d[0], d[1]), dmax(d[2], d[3])));
+        }
+        x.wr += x.sx;
     }
+}
+
+template <bool GUARD, bool RESID, bool FULL, int RS, int STAGES, int CPT>
+__device__ __forceinline__ void w2_rows(W2Ctx& x, int nrows) {
+    double2 x0[CPT / 2 + 2], x1[CPT / 2 + 2], x2[CPT / 2 + 2];  // u(t) rows, rotating
+    double y0[CPT + 2], y1[CPT + 2], y2[CPT + 2];              // u(t+1) rows, rotating
+    w2_take<RS, STAGES, CPT / 2 + 2>(x, x0);                     // row i0-2
+    w2_take<RS, STAGES, CPT / 2 + 2>(x, x1);                     // row i0-1
+    int q = 2;
+    for (; q + 2 < nrows; q += 3) {
+        w2_row<GUARD, RESID, FULL, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
+        w2_row<GUARD, RESID, FULL, RS, STAGES, CPT>(x, x1, x2, x0, y2, y0, y1, q + 1);
+        w2_row<GUARD, RESID, FULL, RS, STAGES, CPT>(x, x2, x0, x1, y0, y1, y2, q + 2);
+    }
+    if (q < nrows) w2_row<GUARD, RESID, FULL, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
+    if (q + 1 < nrows)
+        w2_row<GUARD, RESID, FULL, RS, STAGES, CPT>(x, x1, x2, x0, y2, y0, y1, q + 1);
 }
 
 // u(t+1) on rows i0-1 .. i1+1, columns j-1 .. j+4 of this thread (j = its
@@ -1218,28 +1287,26 @@ __device__ __forceinline__ void w2_row(W2Ctx& x, const double2 (&up)[CPT / 2 + 2
 // The row loop is unrolled by three with the u(t) and u(t+1) row windows
 // rotating through three register arrays each (no moves); cells outside the
 // domain are masked only in tiles that touch it (a uniform branch).
-template <bool GUARD, bool RESID, int CW, int CPT, int STAGES>
-__device__ __forceinline__ void w2_consume(const Wave2Args& a,
-                                           double (*ring)[32 * CPT * CW + 4], uint64_t* full,
-                                           uint64_t* empty, int& s, uint32_t& ph, int64_t c,
-                                           int64_t cb, int64_t i0, int64_t i1, int parity,
-                                           double& r1, double& r2) {
+template <bool GUARD, bool RESID, bool FULL, int CW, int CPT, int STAGES>
+__device__ __forceinline__ void w2_consume(const Wave2Args& a, uint32_t ring_u32,
+                                           uint32_t full_u32, uint32_t empty_u32, int& s,
+                                           uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
+                                           int64_t i1, int parity, double& r1, double& r2) {
     constexpr int W = 32 * CPT * CW;
     constexpr int RS = W + 4;
     const int tid = threadIdx.x;
     W2Ctx x;
-    x.a = &a;
-    x.ringp = &ring[0][0];
-    x.full = full;
-    x.empty = empty;
+    x.full = full_u32;
+    x.empty = empty_u32;
     x.s = s;
     x.ph = ph;
+    x.ready = false;
     x.lane = tid & 31;
     const int64_t j0 = 1 + cb * W;
     const int64_t j = j0 + CPT * tid;
     const int64_t nv64 = a.ey - j + 1;
     x.nv = nv64 <= 0 ? 0 : (nv64 >= CPT ? CPT : (int)nv64);
-    x.p = CPT * tid;  // ring position of column j-2
+    x.ring = ring_u32 + 8u * (uint32_t)(CPT * tid);  // ring position of column j-2
     const int nrows = (int)(i1 - i0 + 5);
     const Nbr9& n9 = a.n9[c];
     x.out_n = !n9.b[1][0];
@@ -1257,24 +1324,15 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a,
     x.mask = __any_sync(0xffffffffu, cghost != 0) || (x.out_n && i0 <= 1) ||
              (x.out_s && i1 >= a.ex);
     x.i0 = i0;
-    x.i1 = i1;
+    x.qlast = (int)(i1 - i0) + 3;
+    x.ex = a.ex;
+    x.sx = a.sx;
     x.wr = n9.b[4][parity ^ 1] + a.origin + i0 * a.sx + j;
     x.zg = a.zghost;
     x.r1 = r1;
     x.r2 = r2;
 
-    double2 x0[CPT / 2 + 2], x1[CPT / 2 + 2], x2[CPT / 2 + 2];  // u(t) rows, rotating
-    double y0[CPT + 2], y1[CPT + 2], y2[CPT + 2];              // u(t+1) rows, rotating
-    w2_take<RS, STAGES, CPT / 2 + 2>(x, x0);                     // row i0-2
-    w2_take<RS, STAGES, CPT / 2 + 2>(x, x1);                     // row i0-1
-    int q = 2;
-    for (; q + 2 < nrows; q += 3) {
-        w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
-        w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x1, x2, x0, y2, y0, y1, q + 1);
-        w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x2, x0, x1, y0, y1, y2, q + 2);
-    }
-    if (q < nrows) w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x0, x1, x2, y1, y2, y0, q);
-    if (q + 1 < nrows) w2_row<GUARD, RESID, RS, STAGES, CPT>(x, x1, x2, x0, y2, y0, y1, q + 1);
+    w2_rows<GUARD, RESID, FULL, RS, STAGES, CPT>(x, nrows);
     s = x.s;
     ph = x.ph;
     r1 = x.r1;
@@ -1291,7 +1349,10 @@ __device__ __forceinline__ void w2_consume(const Wave2Args& a,
 __host__ __device__ constexpr int w2_threads(int cw) { return 32 * (cw + 1); }
 constexpr int w2_minb(int cw) { return cw == 2 ? HRT_W2_MINB2 : HRT_W2_MINB4; }
 constexpr int W2_STAGES = T4_STAGES;
-template <bool GUARD, bool RESID, int CW, int CPT = 4, int STAGES = W2_STAGES>
+// FULL: the chunk width is a multiple of the tile width, so every thread
+// owns CPT columns inside the chunk and the row body needs no column masks
+template <bool GUARD, bool RESID, int CW, bool FULL = false, int CPT = 4,
+          int STAGES = W2_STAGES>
 __global__ void __launch_bounds__(w2_threads(CW), w2_minb(CW))
 slab_wave2_kernel(Wave2Args wa) {
     __shared__ alignas(128) double ring[STAGES][(32 * CPT * CW + 4)];
@@ -1370,6 +1431,8 @@ slab_wave2_kernel(Wave2Args wa) {
         }
         return;
     }
+    const uint32_t ring_u32 = smem_u32(&ring[0][0]);
+    const uint32_t full_u32 = smem_u32(&full[0]), empty_u32 = smem_u32(&empty[0]);
     int slot = 0;
     uint32_t tph = 0;
     for (;;) {
@@ -1391,8 +1454,8 @@ slab_wave2_kernel(Wave2Args wa) {
         const int64_t i0 = 1 + rb * wa.rows;
         const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
         double r1 = 0.0, r2 = 0.0;
-        w2_consume<GUARD, RESID, CW, CPT, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
-                                             (wa.parity0 + k) & 1, r1, r2);
+        w2_consume<GUARD, RESID, FULL, CW, CPT, STAGES>(wa, ring_u32, full_u32, empty_u32, s, ph, c,
+                                                  cb, i0, i1, (wa.parity0 + k) & 1, r1, r2);
         if (RESID && wa.resid) {
             r1 = warp_max(r1);
             r2 = warp_max(r2);
@@ -2638,10 +2701,14 @@ static void set_carveouts() {
     carveout(slab_wave_kernel<false, true, 2>);
     carveout(slab_wave_kernel<false, false, 2>);
 #define C2(CW)                                    \
-    carveout(slab_wave2_kernel<true, true, CW>);    \
-    carveout(slab_wave2_kernel<true, false, CW>);   \
-    carveout(slab_wave2_kernel<false, true, CW>);   \
-    carveout(slab_wave2_kernel<false, false, CW>)
+    carveout(slab_wave2_kernel<true, true, CW, false>);    \
+    carveout(slab_wave2_kernel<true, false, CW, false>);   \
+    carveout(slab_wave2_kernel<false, true, CW, false>);   \
+    carveout(slab_wave2_kernel<false, false, CW, false>);  \
+    carveout(slab_wave2_kernel<true, true, CW, true>);     \
+    carveout(slab_wave2_kernel<true, false, CW, true>);    \
+    carveout(slab_wave2_kernel<false, true, CW, true>);    \
+    carveout(slab_wave2_kernel<false, false, CW, true>)
     C2(4);
     C2(2);
 #undef C2
@@ -2938,22 +3005,28 @@ static bool fuse2_use(const Plan* p) {
     return per_chunk * p->tn() >= fuse2_slots(p);
 }
 
+template <bool G, bool R, int CW, bool F>
+static int w2_blocks_per_sm() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, slab_wave2_kernel<G, R, CW, F>,
+                                                  w2_threads(CW), 0);
+    return n;
+}
+
+// co-resident CTAs of every instance a launch may pick (cooperative launch)
 template <int CW>
 static int wave2_occupancy(bool guard) {
-    int dev = 0, a = 0, b = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    if (guard) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<true, true, CW>,
-                                                      w2_threads(CW), 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<true, false, CW>,
-                                                      w2_threads(CW), 0);
-    } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, slab_wave2_kernel<false, true, CW>,
-                                                      w2_threads(CW), 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, slab_wave2_kernel<false, false, CW>,
-                                                      w2_threads(CW), 0);
-    }
-    return std::min(a, b) * sm_count(dev);
+    const int n = guard ? std::min(std::min(w2_blocks_per_sm<true, true, CW, false>(),
+                                            w2_blocks_per_sm<true, false, CW, false>()),
+                                   std::min(w2_blocks_per_sm<true, true, CW, true>(),
+                                            w2_blocks_per_sm<true, false, CW, true>()))
+                        : std::min(std::min(w2_blocks_per_sm<false, true, CW, false>(),
+                                            w2_blocks_per_sm<false, false, CW, false>()),
+                                   std::min(w2_blocks_per_sm<false, true, CW, true>(),
+                                            w2_blocks_per_sm<false, false, CW, true>()));
+    return n * sm_count(dev);
 }
 
 // nf passes (2 steps each) from step `first` in one slab_wave2_kernel launch
@@ -3046,14 +3119,18 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     const bool guard = !p->nonneg, res = resid_base != nullptr;
     void* fn;
     int threads;
-#define WK2(G, R, CW) (void*)slab_wave2_kernel<G, R, CW>
-#define PICK(CW)                                                \
-    (guard ? (res ? WK2(true, true, CW) : WK2(true, false, CW))  \
-           : (res ? WK2(false, true, CW) : WK2(false, false, CW)))
+    // every column tile full: the chunk width is a multiple of the tile's
+    const bool full = L.ext[1] % (narrow ? 256 : T4_COLS) == 0;
+#define WK2(G, R, CW, F) (void*)slab_wave2_kernel<G, R, CW, F>
+#define PICKF(CW, F)                                                    \
+    (guard ? (res ? WK2(true, true, CW, F) : WK2(true, false, CW, F))    \
+           : (res ? WK2(false, true, CW, F) : WK2(false, false, CW, F)))
+#define PICK(CW) (full ? PICKF(CW, true) : PICKF(CW, false))
     const size_t smem = 0;
     fn = narrow ? PICK(2) : PICK(4);
     threads = w2_threads(narrow ? 2 : 4);
 #undef PICK
+#undef PICKF
 #undef WK2
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid2, T);
     void* args[] = {&wa};
