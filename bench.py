@@ -338,16 +338,31 @@ def run_ours(args):
     # updates: their algorithmic bytes are 8 per lattice update; the naive
     # one-step algorithm's 16 B/update is reported beside it.
     persistent = bool(getattr(solver, "persistent", False))
-    two_step = iters >= 4 and solver.two_step
-    launches_per_job = 1 if persistent else (iters // 2 if two_step else iters)
-    steps_per_launch = iters // launches_per_job
+    # steps one fused pass covers (3: slab_wave3_kernel, 2: slab_wave2_kernel
+    # / volume2_kernel, 1: one step per pass); a run of `iters` steps is
+    # n_single one-step sweeps plus n_pass fused passes, each reading u once
+    # and writing once: 16 algorithmic bytes per cell and sweep/pass
+    k = solver.steps_per_pass if iters >= 3 else 1
+    if k == 3:
+        n_pass, n_single = iters // 3, iters % 3
+    elif k == 2 and iters >= 4:
+        n_pass = (iters // 4) * 2
+        n_single = iters - 2 * n_pass
+    else:
+        k, n_pass, n_single = 1, 0, iters
+    two_step = k > 1
+    launches_per_job = (int(n_single > 0) + int(n_pass > 0)) if persistent else \
+        (n_pass + n_single)
+    steps_per_launch = iters / launches_per_job
     avg_upd_ms = upd / (args.steps * launches_per_job)
-    bytes_per_update = BYTES_PER_UPDATE // 2 if two_step else BYTES_PER_UPDATE
-    bytes_per_launch = bytes_per_update * my_cells * steps_per_launch
+    bytes_per_job = BYTES_PER_UPDATE * my_cells * (n_single + n_pass)
+    bytes_per_update = bytes_per_job / (my_cells * iters)
+    bytes_per_launch = bytes_per_job / launches_per_job
     achieved = bytes_per_launch / (avg_upd_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     cw = 2 if grid.ext[1] <= 256 else 4
-    kname = (f"slab_wave2_kernel<false,true,{cw}>" if two_step else
+    kname = (f"slab_wave3_kernel<false,true,{cw}>" if k == 3 else
+             f"slab_wave2_kernel<false,true,{cw}>" if k == 2 else
              f"slab_wave_kernel<false,true,{cw}>" if persistent else
              {None: f"slab_update_tma4_kernel<false,true,{cw},push>",
               2: f"slab_update_tma4_kernel<false,true,{cw},push>",
@@ -355,14 +370,16 @@ def run_ours(args):
     if grid.slab is False:
         kname = "volume2_kernel<true>" if two_step else "volume_update_tma_kernel<true>"
     traffic = (args.traffic if args.traffic is not None else
-               _recorded_traffic(wl["name"] + ("_two_step" if two_step else ""), world))
+               _recorded_traffic(wl["name"] + {3: "_three_step", 2: "_two_step"}.get(k, ""),
+                                 world))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
                 "traffic": traffic * steps_per_launch if traffic else None,
-                "kernel": kname, "steps_per_launch": steps_per_launch,
-                "bytes_per_launch": bytes_per_launch,
+                "kernel": kname, "steps_per_launch": round(steps_per_launch, 3),
+                "steps_per_pass": k, "passes_per_job": n_pass, "single_steps_per_job": n_single,
+                "bytes_per_launch": round(bytes_per_launch),
                 "avg_launch_ms": round(avg_upd_ms, 5), "peak_source": peak_src,
-                "bytes_per_update": bytes_per_update,
+                "bytes_per_update": round(bytes_per_update, 4),
                 "one_step_equivalent": {"bytes_per_update": BYTES_PER_UPDATE,
                                         "achieved": round(achieved * BYTES_PER_UPDATE
                                                           / bytes_per_update, 1),

@@ -694,16 +694,22 @@ class JacobiSolver:
     def _agree_tiling(self, every: list) -> None:
         """Every GPU of a multi-GPU run must share (rows, tiles per chunk)
         — neighbours index each other's tile counters with their own
-        tiling — and the two-step decision: a two-step GPU never pushes
+        tiling — and the fused-pass decision: a fused GPU never pushes
         ghost rows and picks buffers by pass parity, so a one-step
-        neighbour would read stale ghosts.  ``every`` holds each GPU's
-        (rows, tiles per chunk, two-step); where only the last differs,
-        two-step passes are turned off on this process' plans."""
+        neighbour would read stale ghosts, and neighbours counting steps in
+        passes of 3 and of 2 would wait on each other's counters at
+        different strides.  ``every`` holds each GPU's (rows, tiles per
+        chunk, steps per pass); if only some GPUs can run three-step
+        passes, all fall back to two; if only some can fuse, none does."""
         if len({t[:2] for t in every}) != 1:
             raise HrtError(f"per-chunk tilings differ across GPUs: {every}")
-        if len({t[2] for t in every}) != 1:
+        ks = {t[2] for t in every}
+        if len(ks) != 1:
             for plan in self.plans.values():
-                N.call("hrt_jacobi_plan_set_fuse2", plan, 0)
+                if 0 in ks:
+                    N.call("hrt_jacobi_plan_set_fuse2", plan, 0)
+                else:
+                    N.call("hrt_jacobi_plan_set_pass_steps", plan, 2)
 
     def _setup_persistent(self) -> None:
         g = self.used_gpus[0]
@@ -984,15 +990,23 @@ class JacobiSolver:
         hpin.close()
         return out
 
-    def tiling(self) -> dict[int, tuple[int, int, bool]]:
-        """Per GPU: (rows per tile, tiles per chunk, two-step passes)."""
+    def tiling(self) -> dict[int, tuple[int, int, int]]:
+        """Per GPU: (rows per tile, tiles per chunk, Jacobi steps per fused
+        pass — 3, 2, or 0 for one step per pass)."""
         out = {}
         for g in self.used_gpus:
-            r, t, on = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+            r, t, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
             N.call("hrt_jacobi_plan_tiling", self.plans[g], ctypes.byref(r), ctypes.byref(t),
-                   ctypes.byref(on))
-            out[g] = (r.value, t.value, bool(on.value))
+                   ctypes.byref(k))
+            out[g] = (r.value, t.value, k.value)
         return out
+
+    @property
+    def steps_per_pass(self) -> int:
+        """Jacobi steps one pass over HBM covers in runs of several steps
+        (3: slab_wave3_kernel, 2: slab_wave2_kernel / volume2_kernel, 1)."""
+        ks = {t[2] for t in self.tiling().values()}
+        return max(1, min(ks)) if ks and 0 not in ks else 1
 
     @property
     def two_step(self) -> bool:

@@ -343,23 +343,33 @@ def test_full_size_cfg3_and_cfg5_properties(hrt):
     ((600, 1024, 1), (2, 2, 1)),     # 300-row chunks: 256 + 44 (default rows) / 4 x 64 + 44
     ((96, 512, 1), (3, 2, 1)),       # 256-wide chunks: the 2-warp instance
     ((8, 12, 1), (4, 3, 1)),         # 2 x 4 chunks: rims span whole neighbour chunks
+    ((12, 16, 1), (4, 4, 1)),        # 3 x 4 chunks: 3-cell rims span whole neighbours
+    ((134, 1032, 1), (2, 2, 1)),     # 67-row chunks: tiles 64 + 3 (the 3-row minimum)
     ((200, 64, 1), (1, 1, 1)),       # one chunk: every rim is the domain boundary
 ])
-@pytest.mark.parametrize("steps", [4, 6, 7, 13])
+@pytest.mark.parametrize("steps", [3, 4, 6, 7, 13])
 @pytest.mark.parametrize("rows", [None, 64])
-def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, monkeypatch):
-    """slab_wave2_kernel (two Jacobi steps per pass, 2-cell rims read from the
-    3 x 3 chunk neighbourhood, u(t+1) only in registers) against the numpy
-    oracle on random signed data: field and every step's residual bitwise,
-    with n mod 4 single steps before the passes."""
+@pytest.mark.parametrize("pass_steps", ["3", "2"])
+def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, pass_steps, monkeypatch):
+    """Fused passes — slab_wave3_kernel (three Jacobi steps per pass, 3-cell
+    rims, u(t+1) and u(t+2) in registers, column neighbours by shuffles and
+    warp-edge chains) and slab_wave2_kernel (two steps, 2-cell rims) —
+    reading their rims from the 3 x 3 chunk neighbourhood, against the
+    numpy oracle on random signed data: field and every step's residual
+    bitwise, with the leftover single steps (n mod 3, n mod 4) first."""
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
     monkeypatch.setenv("HRT_FUSE2", "2")  # these domains are too small for the auto policy
+    monkeypatch.setenv("HRT_PASS_STEPS", pass_steps)
     rng = np.random.default_rng(steps * 7 + dom[0])
     init = rng.random(dom) * 4.0 - 1.0
     s = JacobiSolver(ChunkGrid(dom, grid=grid), rows=rows)
-    if dom[0] // grid[0] % 64 != 1 and dom[1] // grid[1] % 2 == 0:
-        assert s.two_step, "two-step passes should apply here"
+    ex, ey = dom[0] // grid[0], dom[1] // grid[1]
+    r = rows or 64  # (these domains are below the 256-row threshold)
+    if ex % (rows or 64) != 1 and ey % 2 == 0:
+        assert s.two_step, "fused passes should apply here"
+    if pass_steps == "3" and s.two_step and ex >= 3 and ey >= 4 and ex % r not in (1, 2):
+        assert s.steps_per_pass == 3, s.tiling()
     s.upload(init)
     s.run(steps, residual=True)
     got = s.download()

@@ -1,6 +1,6 @@
 """One slab_wave2_kernel launch at cfg2 shape for ncu (steps passes / 2):
 
-    ncu --set full --import-source on -k regex:slab_wave2 -c 1 \
+    ncu --set full --import-source on -k regex:slab_wave -c 1 \
         python tools/ncu_wave2.py [steps] [grid]
 """
 import os
