@@ -338,14 +338,12 @@ def run_ours(args):
     # updates: their algorithmic bytes are 8 per lattice update; the naive
     # one-step algorithm's 16 B/update is reported beside it.
     persistent = bool(getattr(solver, "persistent", False))
-    # steps one fused pass covers (3: slab_wave3_kernel, 2: slab_wave2_kernel
-    # / volume2_kernel, 1: one step per pass); a run of `iters` steps is
-    # n_single one-step sweeps plus n_pass fused passes, each reading u once
-    # and writing once: 16 algorithmic bytes per cell and sweep/pass
-    k = solver.steps_per_pass if iters >= 3 else 1
-    if k == 3:
-        n_pass, n_single = iters // 3, iters % 3
-    elif k == 2 and iters >= 4:
+    # steps one fused pass covers (2: slab_wave2_kernel / volume2_kernel, 1:
+    # one step per pass); a run of `iters` steps is n_single one-step sweeps
+    # plus n_pass fused passes, each reading u once and writing once: 16
+    # algorithmic bytes per cell and sweep/pass
+    k = solver.steps_per_pass
+    if k == 2 and iters >= 4:
         n_pass = (iters // 4) * 2
         n_single = iters - 2 * n_pass
     else:
@@ -361,8 +359,7 @@ def run_ours(args):
     achieved = bytes_per_launch / (avg_upd_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     cw = 2 if grid.ext[1] <= 256 else 4
-    kname = (f"slab_wave3_kernel<false,true,{cw}>" if k == 3 else
-             f"slab_wave2_kernel<false,true,{cw}>" if k == 2 else
+    kname = (f"slab_wave2_kernel<false,true,{cw}>" if k == 2 else
              f"slab_wave_kernel<false,true,{cw}>" if persistent else
              {None: f"slab_update_tma4_kernel<false,true,{cw},push>",
               2: f"slab_update_tma4_kernel<false,true,{cw},push>",
@@ -370,8 +367,7 @@ def run_ours(args):
     if grid.slab is False:
         kname = "volume2_kernel<true>" if two_step else "volume_update_tma_kernel<true>"
     traffic = (args.traffic if args.traffic is not None else
-               _recorded_traffic(wl["name"] + {3: "_three_step", 2: "_two_step"}.get(k, ""),
-                                 world))
+               _recorded_traffic(wl["name"] + ("_two_step" if k == 2 else ""), world))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
                 "traffic": traffic * steps_per_launch if traffic else None,

@@ -252,10 +252,6 @@ int hrt_jacobi_plan_set_tiling_chunks(void *plan, int64_t n);
  * always.  Multi-GPU runs turn them off on every GPU when not every GPU
  * can run them (a one-step neighbour would read ghosts nobody pushed). */
 int hrt_jacobi_plan_set_fuse2(void *plan, int mode);
-/* Jacobi steps per fused pass: 3 (slab_wave3_kernel: u read once per three
- * steps, the default) or 2 (slab_wave2_kernel); HRT_PASS_STEPS overrides
- * at plan creation. */
-int hrt_jacobi_plan_set_pass_steps(void *plan, int steps);
 /* The plan's tiling: rows per tile, tiles per chunk, and the Jacobi steps
  * per fused pass runs of several steps use (0 = one step per pass). */
 int hrt_jacobi_plan_tiling(void *plan, int64_t *rows, int64_t *tiles_per_chunk, int *steps_per_pass);

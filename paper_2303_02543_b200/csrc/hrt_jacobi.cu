@@ -1498,513 +1498,6 @@ slab_wave2_kernel(Wave2Args wa) {
 
 
 // ---------------------------------------------------------------------------
-// THREE Jacobi steps per pass (slab_wave3_kernel).  A tile of pass k reads
-// u(t) once — rows i0-3 .. i1+3, columns j0-4 .. j0+W+3 (a 3-cell rim, the
-// span widened to 16-byte alignment) from the 3 x 3 chunk neighbourhood —
-// and writes only u(t+3): 5.33 algorithmic bytes per lattice update
-// instead of the two-step kernel's 8.
-//
-// Each consumer thread owns four columns.  u(t) rows stay in the ring (a
-// stage is released once the row has served as dn, mid and up — three row
-// steps); u(t+1) and u(t+2) rows live in registers, three rows each.  The
-// column neighbours a level needs come from the neighbouring lanes by
-// shuffles; only the warp's edge lanes need values no lane owns, and every
-// lane computes those "edge" chains in the same instruction stream (lane 0
-// the columns left of its block, lane 31 those right of it): level 1 six
-// chains (4 own + 2 edge), level 2 five, level 3 four — 15 chains for 12
-// lattice updates, the two-step kernel's redundancy (10 for 8) with a third
-// of its DRAM traffic per update removed.  Every cell is computed with the
-// reference's operations in the reference's order, so the field and all
-// three per-step residuals stay bitwise equal.
-
-template <int W, int STAGES>
-__device__ __forceinline__ void w3_produce(const Wave2Args& a, double (*ring)[W + 8],
-                                           uint64_t* full, uint64_t* empty, int& s,
-                                           uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
-                                           int64_t i1, int parity) {
-    const int64_t j0 = 1 + cb * W;
-    const int64_t last = min(j0 + W - 1, a.ey);
-    const Nbr9& n9 = a.n9[c];
-    const bool wedge = cb == 0, eedge = last == a.ey;
-    const int64_t lo = wedge ? 1 : j0 - 4;
-    const int64_t hi = eedge ? a.ey : last + 4;
-    const uint32_t mbytes = (uint32_t)((hi - lo + 1) * 8);  // ey even: 16-byte multiple
-    const int mpos = (int)(lo - (j0 - 4));
-    const int epos = (int)(last - j0 + 5);                   // ring index of column last+1
-    const int nrows = (int)(i1 - i0 + 7);
-    for (int q = 0; q < nrows; ++q) {
-        const int64_t r = i0 - 3 + q;
-        const int di = r < 1 ? -1 : (r > a.ex ? 1 : 0);
-        const int64_t rr = r - di * a.ex;
-        const double* br = n9.b[(di + 1) * 3 + 1][parity];
-        mbar_wait_sleep(&empty[s], ph ^ 1);
-        uint32_t bytes = mbytes;
-        const double* msrc = br ? br + a.origin + rr * a.sx + lo : a.ones;
-        const double* wsrc = nullptr;
-        const double* esrc = nullptr;
-        if (wedge) {
-            const double* bw = br ? n9.b[(di + 1) * 3 + 0][parity] : nullptr;
-            if (bw) {
-                wsrc = bw + a.origin + rr * a.sx + (a.ey - 3);
-                bytes += 32;
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) ring[s][e] = HRT_BOUNDARY;
-            }
-        }
-        if (eedge) {
-            const double* be = br ? n9.b[(di + 1) * 3 + 2][parity] : nullptr;
-            if (be) {
-                esrc = be + a.origin + rr * a.sx + 1;
-                bytes += 32;
-            } else {
-#pragma unroll
-                for (int e = 0; e < 4; ++e) ring[s][epos + e] = HRT_BOUNDARY;
-            }
-        }
-        mbar_expect_tx(&full[s], bytes);
-        tma_row_load(&ring[s][mpos], msrc, mbytes, &full[s]);
-        if (wsrc) tma_row_load(&ring[s][0], wsrc, 32, &full[s]);
-        if (esrc) tma_row_load(&ring[s][epos], esrc, 32, &full[s]);
-        if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-        }
-    }
-}
-
-__device__ __forceinline__ double lds_f64(uint32_t addr) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-__device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
-
-// one level of a row: own[0..3] of row r from rows (up, mid, dn) own values
-// and the two column neighbours of mid's block (nl = column j-1, nr = j+4)
-template <bool GUARD>
-__device__ __forceinline__ void w3_level(const double (&up)[4], const double (&mid)[4],
-                                         const double (&dn)[4], double nl, double nr, double zg,
-                                         double (&out)[4]) {
-    out[0] = div6_t<GUARD>(sum6(up[0], dn[0], nl, mid[1], zg, zg));
-    out[1] = div6_t<GUARD>(sum6(up[1], dn[1], mid[0], mid[2], zg, zg));
-    out[2] = div6_t<GUARD>(sum6(up[2], dn[2], mid[1], mid[3], zg, zg));
-    out[3] = div6_t<GUARD>(sum6(up[3], dn[3], mid[2], nr, zg, zg));
-}
-
-__device__ __forceinline__ double dmax4(double r, const double (&d)[4]) {
-    return dmax(r, dmax(dmax(d[0], d[1]), dmax(d[2], d[3])));
-}
-
-// Per-thread state of the three-step consumer (one tile).
-struct W3Ctx {
-    uint32_t ring;             // shared address: this thread's column j in stage 0
-    uint32_t eo1, eo2, eo3;    // offsets from a stage base (shared address of ring column 0)
-                               // of the edge columns 1..3 away from this lane's block
-    uint32_t stage0;           // shared address of stage 0, column 0
-    uint32_t full, empty;
-    int s, sr;                 // next stage to take / to release
-    uint32_t ph;
-    bool ready, l0, l31;
-    int nv, nrows;
-    unsigned cghost;           // bits 0-3 own columns, 4 edge col 1 away, 5 edge col 2 away
-    bool mask, out_n, out_s;
-    int qlast1;                // last ring row whose level-1 row is inside the tile
-    int64_t i0, ex, sx;
-    double* wr;
-    double zg, r1, r2, r3;
-};
-
-template <int RS>
-__device__ __forceinline__ void w3_own(uint32_t col_j, double (&v)[4]) {
-    const double2 a = lds_f64x2(col_j), b = lds_f64x2(col_j + 16u);
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = b.x;
-    v[3] = b.y;
-}
-
-// wait for the next ring row; returns its stage index
-template <int STAGES>
-__device__ __forceinline__ int w3_take(W3Ctx& x) {
-    const uint32_t fb = x.full + 8u * (uint32_t)x.s;
-    if (!x.ready && !mbar_try_u32(fb, x.ph)) mbar_wait_u32_slow(fb, x.ph);
-    const int st = x.s;
-    if (++x.s == STAGES) {
-        x.s = 0;
-        x.ph ^= 1;
-    }
-    x.ready = mbar_try_u32(x.full + 8u * (uint32_t)x.s, x.ph);
-    return st;
-}
-
-// hand the oldest held stage back to the producer
-template <int STAGES>
-__device__ __forceinline__ void w3_release(W3Ctx& x) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
-    __syncwarp();
-    mbar_arrive_lane0_u32(x.empty + 8u * (uint32_t)x.sr, x.l0 ? 0 : 1);
-    if (++x.sr == STAGES) x.sr = 0;
-}
-
-// One pipeline step q.  The three levels work on different rows so their
-// dependency chains are independent (15 chains in flight per thread):
-//   level 1: u(t+1) row R(q-1) from u(t) rows R(q-2..q) (ring stages
-//            sup, smid, sdn; R(q) is taken now)          -> u1n
-//   level 2: u(t+2) row R(q-3) from u(t+1) rows R(q-4) a, R(q-3) b, R(q-2) c -> u2n
-//   level 3: u(t+3) row R(q-5) from u(t+2) rows R(q-6) A, R(q-5) B, R(q-4) C -> HBM
-// R(q) = i0-3+q.  Steps past the last ring row (q >= nrows) only drain
-// levels 2 and 3.  All branches are warp-uniform.
-template <bool GUARD, bool RESID, bool FULL, int RS, int STAGES>
-__device__ __forceinline__ void w3_step(W3Ctx& x, int& sup, int& smid, int& sdn,
-                                        const double (&u1a)[6], const double (&u1b)[6],
-                                        const double (&u1c)[6], double (&u1n)[6],
-                                        const double (&u2a)[5], const double (&u2b)[5],
-                                        const double (&u2c)[5], double (&u2n)[5], int q) {
-    const double zg = x.zg;
-    // ---- level 1: u(t+1) row R(q-1) ----
-    if (q < x.nrows) {
-        sup = smid;
-        smid = sdn;
-        sdn = w3_take<STAGES>(x);
-        const uint32_t bu = x.stage0 + (uint32_t)(sup * RS * 8);
-        const uint32_t bm = x.stage0 + (uint32_t)(smid * RS * 8);
-        const uint32_t bd = x.stage0 + (uint32_t)(sdn * RS * 8);
-        const uint32_t own = x.ring - x.stage0;
-        double up[4], mid[4], dn[4];
-        w3_own<RS>(bu + own, up);
-        w3_own<RS>(bm + own, mid);
-        w3_own<RS>(bd + own, dn);
-        const double m1 = lds_f64(bm + x.eo1), m2 = lds_f64(bm + x.eo2), m3 = lds_f64(bm + x.eo3);
-        const double p1 = lds_f64(bu + x.eo1), p2 = lds_f64(bu + x.eo2);
-        const double d1 = lds_f64(bd + x.eo1), d2 = lds_f64(bd + x.eo2);
-        const double sl = shfl_up1(mid[3]), sr = shfl_dn1(mid[0]);
-        double o[4];
-        w3_level<GUARD>(up, mid, dn, x.l0 ? m1 : sl, x.l31 ? m1 : sr, zg, o);
-        // edge chains: the column 1 away (lane 0: j-1, lane 31: j+4), 2 away
-        const double e1 = div6_t<GUARD>(sum6(p1, d1, x.l0 ? m2 : mid[3], x.l0 ? mid[0] : m2, zg, zg));
-        const double e2 = div6_t<GUARD>(sum6(p2, d2, x.l0 ? m3 : m1, x.l0 ? m1 : m3, zg, zg));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) u1n[k] = o[k];
-        u1n[4] = e1;
-        u1n[5] = e2;
-        if (x.mask) {
-            const int64_t r = x.i0 - 4 + q;
-            const bool rghost = (r < 1 && x.out_n) || (r > x.ex && x.out_s);
-#pragma unroll
-            for (int m = 0; m < 6; ++m)
-                if (rghost || ((x.cghost >> m) & 1u)) u1n[m] = HRT_BOUNDARY;
-        }
-        if (RESID && q >= 4 && q <= x.qlast1) {
-            double d[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                d[k] = (FULL || k < x.nv) ? abs_bits(__dsub_rn(u1n[k], mid[k])) : 0.0;
-            x.r1 = dmax4(x.r1, d);
-        }
-        w3_release<STAGES>(x);  // row R(q-2) has served as up: done
-    }
-    // ---- level 2: u(t+2) row R(q-3) ----
-    if (q >= 5 && q <= x.nrows) {
-        const double sl = shfl_up1(u1b[3]), sr = shfl_dn1(u1b[0]);
-        const double (&ua)[4] = *reinterpret_cast<const double(*)[4]>(&u1a[0]);
-        const double (&ub)[4] = *reinterpret_cast<const double(*)[4]>(&u1b[0]);
-        const double (&uc)[4] = *reinterpret_cast<const double(*)[4]>(&u1c[0]);
-        double o[4];
-        w3_level<GUARD>(ua, ub, uc, x.l0 ? u1b[4] : sl, x.l31 ? u1b[4] : sr, zg, o);
-        const double e1 = div6_t<GUARD>(sum6(u1a[4], u1c[4], x.l0 ? u1b[5] : u1b[3],
-                                             x.l0 ? u1b[0] : u1b[5], zg, zg));
-#pragma unroll
-        for (int k = 0; k < 4; ++k) u2n[k] = o[k];
-        u2n[4] = e1;
-        if (x.mask) {
-            const int64_t r = x.i0 - 6 + q;
-            const bool rghost = (r < 1 && x.out_n) || (r > x.ex && x.out_s);
-#pragma unroll
-            for (int m = 0; m < 5; ++m)
-                if (rghost || ((x.cghost >> m) & 1u)) u2n[m] = HRT_BOUNDARY;
-        }
-        if (RESID && q >= 6 && q <= x.nrows - 1) {
-            double d[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                d[k] = (FULL || k < x.nv) ? abs_bits(__dsub_rn(u2n[k], u1b[k])) : 0.0;
-            x.r2 = dmax4(x.r2, d);
-        }
-    }
-    // ---- level 3: u(t+3) row R(q-5) -> buffer parity^1 ----
-    if (q >= 8 && q <= x.nrows + 1) {
-        const double sl = shfl_up1(u2b[3]), sr = shfl_dn1(u2b[0]);
-        const double (&ua)[4] = *reinterpret_cast<const double(*)[4]>(&u2a[0]);
-        const double (&ub)[4] = *reinterpret_cast<const double(*)[4]>(&u2b[0]);
-        const double (&uc)[4] = *reinterpret_cast<const double(*)[4]>(&u2c[0]);
-        double o[4];
-        w3_level<GUARD>(ua, ub, uc, x.l0 ? u2b[4] : sl, x.l31 ? u2b[4] : sr, zg, o);
-        if (FULL) {
-            *reinterpret_cast<double2*>(x.wr) = make_double2(o[0], o[1]);
-            *reinterpret_cast<double2*>(x.wr + 2) = make_double2(o[2], o[3]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (k < x.nv) x.wr[k] = o[k];
-        }
-        if (RESID) {
-            double d[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                d[k] = (FULL || k < x.nv) ? abs_bits(__dsub_rn(o[k], u2b[k])) : 0.0;
-            x.r3 = dmax4(x.r3, d);
-        }
-        x.wr += x.sx;
-    }
-}
-
-template <bool GUARD, bool RESID, bool FULL, int RS, int STAGES>
-__device__ __forceinline__ void w3_rows(W3Ctx& x) {
-    double a0[6], a1[6], a2[6], a3[6];  // u(t+1) rows: own 4 + edge 1 and 2 away (rotating)
-    double b0[5], b1[5], b2[5], b3[5];  // u(t+2) rows: own 4 + edge 1 away (rotating)
-    int sup = 0, smid = 0, sdn = w3_take<STAGES>(x);  // R(0) = i0-3
-    smid = sdn;
-    sdn = w3_take<STAGES>(x);                         // R(1)
-    // steps 2 .. nrows+1; the rotation of both windows has period 4
-    for (int q = 2; q < x.nrows + 2; q += 4) {
-        w3_step<GUARD, RESID, FULL, RS, STAGES>(x, sup, smid, sdn, a0, a1, a2, a3, b0, b1, b2, b3, q);
-        w3_step<GUARD, RESID, FULL, RS, STAGES>(x, sup, smid, sdn, a1, a2, a3, a0, b1, b2, b3, b0,
-                                                q + 1);
-        w3_step<GUARD, RESID, FULL, RS, STAGES>(x, sup, smid, sdn, a2, a3, a0, a1, b2, b3, b0, b1,
-                                                q + 2);
-        w3_step<GUARD, RESID, FULL, RS, STAGES>(x, sup, smid, sdn, a3, a0, a1, a2, b3, b0, b1, b2,
-                                                q + 3);
-    }
-    // the last two rows only ever served as mid / dn: hand them back
-    w3_release<STAGES>(x);
-    w3_release<STAGES>(x);
-}
-
-template <bool GUARD, bool RESID, bool FULL, int CW, int STAGES>
-__device__ __forceinline__ void w3_consume(const Wave2Args& a, uint32_t ring_u32,
-                                           uint32_t full_u32, uint32_t empty_u32, int& s,
-                                           uint32_t& ph, int64_t c, int64_t cb, int64_t i0,
-                                           int64_t i1, int parity, double& r1, double& r2,
-                                           double& r3) {
-    constexpr int W = 128 * CW;
-    constexpr int RS = W + 8;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    W3Ctx x;
-    x.full = full_u32;
-    x.empty = empty_u32;
-    x.s = s;
-    x.sr = s;
-    x.ph = ph;
-    x.ready = false;
-    x.l0 = lane == 0;
-    x.l31 = lane == 31;
-    const int64_t j0 = 1 + cb * W;
-    const int64_t j = j0 + 4 * tid;
-    const int64_t nv64 = a.ey - j + 1;
-    x.nv = nv64 <= 0 ? 0 : (nv64 >= 4 ? 4 : (int)nv64);
-    // ring index of column j is 4 + 4*tid (ring column 0 = j0-4)
-    x.stage0 = ring_u32;
-    x.ring = ring_u32 + 8u * (uint32_t)(4 + 4 * tid);
-    // edge columns: lane 0 reads j-1, j-2, j-3; lane 31 j+4, j+5, j+6; the
-    // other lanes all read ring column 0 (one broadcast address: no bank
-    // conflicts; the values are never used)
-    const uint32_t jb = 8u * (uint32_t)(4 + 4 * tid);
-    x.eo1 = x.l0 ? jb - 8u : (x.l31 ? jb + 32u : 0u);
-    x.eo2 = x.l0 ? jb - 16u : (x.l31 ? jb + 40u : 0u);
-    x.eo3 = x.l0 ? jb - 24u : (x.l31 ? jb + 48u : 0u);
-    x.nrows = (int)(i1 - i0 + 7);
-    const Nbr9& n9 = a.n9[c];
-    x.out_n = !n9.b[1][0];
-    x.out_s = !n9.b[7][0];
-    const bool out_w = !n9.b[3][0], out_e = !n9.b[5][0];
-    // level-1/2 columns outside the domain keep BOUNDARY: own j..j+3 (bits
-    // 0-3), the edge column 1 away (bit 4) and 2 away (bit 5)
-    unsigned cghost = 0;
-    const int64_t ecol1 = x.l0 ? j - 1 : j + 4, ecol2 = x.l0 ? j - 2 : j + 5;
-    const int64_t cols[6] = {j, j + 1, j + 2, j + 3, ecol1, ecol2};
-#pragma unroll
-    for (int m = 0; m < 6; ++m) {
-        const int64_t cc = cols[m];
-        if ((cc < 1 && out_w) || (cc > a.ey && out_e)) cghost |= 1u << m;
-    }
-    if (!x.l0 && !x.l31) cghost &= 0xFu;  // middle lanes' edge values are unused
-    x.cghost = cghost;
-    x.mask = __any_sync(0xffffffffu, cghost != 0) || (x.out_n && i0 <= 2) ||
-             (x.out_s && i1 >= a.ex - 1);
-    x.i0 = i0;
-    x.qlast1 = (int)(i1 - i0) + 4;  // level-1 row R(q-1) = i1
-    x.ex = a.ex;
-    x.sx = a.sx;
-    x.wr = n9.b[4][parity ^ 1] + a.origin + i0 * a.sx + j;
-    x.zg = a.zghost;
-    x.r1 = r1;
-    x.r2 = r2;
-    x.r3 = r3;
-    w3_rows<GUARD, RESID, FULL, RS, STAGES>(x);
-    s = x.s;
-    ph = x.ph;
-    r1 = x.r1;
-    r2 = x.r2;
-    r3 = x.r3;
-}
-
-constexpr int W3_STAGES = 11;  // 11 x 4160 B ring within the 48 KB static limit
-
-#ifndef HRT_W3_MINB4
-#define HRT_W3_MINB4 2   // resident CTAs/SM the registers target: 512-wide tiles (<= 168 regs)
-#endif
-#ifndef HRT_W3_MINB2
-#define HRT_W3_MINB2 4   // 256-wide tiles
-#endif
-constexpr int w3_minb(int cw) { return cw == 2 ? HRT_W3_MINB2 : HRT_W3_MINB4; }
-
-template <bool GUARD, bool RESID, int CW, bool FULL = false, int STAGES = W3_STAGES>
-__global__ void __launch_bounds__(w2_threads(CW), w3_minb(CW))
-slab_wave3_kernel(Wave2Args wa) {
-    __shared__ alignas(128) double ring[STAGES][128 * CW + 8];
-    __shared__ alignas(8) uint64_t full[STAGES], empty[STAGES], tq_full[WAVE_TQ],
-        tq_empty[WAVE_TQ];
-    __shared__ long long tq[WAVE_TQ];
-    __shared__ double red[3][CW];
-    const int tid = threadIdx.x;
-    const int warp = tid >> 5;
-    const int lane = tid & 31;
-    const int64_t T = wa.ntiles;
-    const int64_t tr = wa.tiles_r, tc = wa.tiles_c;
-    const int64_t per_chunk = tr * tc;
-    const long long total = (long long)T * wa.nfused;
-
-    if (tid == 0) {
-        for (int k = 0; k < STAGES; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], CW);
-        }
-        for (int k = 0; k < WAVE_TQ; ++k) {
-            mbar_init(&tq_full[k], 1);
-            mbar_init(&tq_empty[k], CW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-
-    int s = 0;
-    uint32_t ph = 0;
-    if (warp >= CW) {
-        if (lane != 0) return;
-        bool dead = false;
-        int slot = 0;
-        uint32_t tph = 0;
-        for (;;) {
-            const long long t = (long long)atomicAdd(wa.ticket, 1ull);
-            mbar_wait(&tq_empty[slot], tph ^ 1);
-            tq[slot] = t < total ? t : -1;
-            mbar_arrive(&tq_full[slot]);
-            if (++slot == WAVE_TQ) {
-                slot = 0;
-                tph ^= 1;
-            }
-            if (t >= total) break;
-            const int k = (int)(t / T);
-            const int64_t tile = t - (long long)k * T;
-            const int64_t c = tile / per_chunk;
-            const int64_t rem = tile - c * per_chunk;
-            const int64_t rb = rem / tc;
-            const int64_t cb = rem - rb * tc;
-            if (!dead) {
-                // the 3 x 3 tile neighbourhood must be done with step base+3k
-                const unsigned need = wa.base + 3u * (unsigned)k;
-                const Nbr9& n9 = wa.n9[c];
-                const unsigned int* q[9];
-                bool sys[9];
-#pragma unroll
-                for (int d = 0; d < 9; ++d) {
-                    const int64_t r2 = rb + d / 3 - 1, c2 = cb + d % 3 - 1;
-                    const int ci = r2 < 0 ? -1 : (r2 >= tr ? 1 : 0);
-                    const int cj = c2 < 0 ? -1 : (c2 >= tc ? 1 : 0);
-                    const int e = (ci + 1) * 3 + (cj + 1);
-                    const unsigned int* base = n9.cnt[e];
-                    q[d] = base ? base + (r2 - ci * tr) * tc + (c2 - cj * tc) : nullptr;
-                    sys[d] = (n9.sysmask >> e) & 1u;
-                }
-                dead = !wait_counters<9>(q, sys, need, wa.timeout_ns, wa.err);
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-            }
-            const int64_t i0 = 1 + rb * wa.rows;
-            const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
-            w3_produce<128 * CW, STAGES>(wa, ring, full, empty, s, ph, c, cb, i0, i1,
-                                         (wa.parity0 + k) & 1);
-        }
-        return;
-    }
-    const uint32_t ring_u32 = smem_u32(&ring[0][0]);
-    const uint32_t full_u32 = smem_u32(&full[0]), empty_u32 = smem_u32(&empty[0]);
-    int slot = 0;
-    uint32_t tph = 0;
-    for (;;) {
-        mbar_wait(&tq_full[slot], tph);
-        const long long t = tq[slot];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tq_empty[slot]);
-        if (++slot == WAVE_TQ) {
-            slot = 0;
-            tph ^= 1;
-        }
-        if (t < 0) break;
-        const int k = (int)(t / T);
-        const int64_t tile = t - (long long)k * T;
-        const int64_t c = tile / per_chunk;
-        const int64_t rem = tile - c * per_chunk;
-        const int64_t rb = rem / tc;
-        const int64_t cb = rem - rb * tc;
-        const int64_t i0 = 1 + rb * wa.rows;
-        const int64_t i1 = min(wa.ex, i0 + wa.rows - 1);
-        double r1 = 0.0, r2 = 0.0, r3 = 0.0;
-        w3_consume<GUARD, RESID, FULL, CW, STAGES>(wa, ring_u32, full_u32, empty_u32, s, ph, c,
-                                                   cb, i0, i1, (wa.parity0 + k) & 1, r1, r2, r3);
-        if (RESID && wa.resid) {
-            r1 = warp_max(r1);
-            r2 = warp_max(r2);
-            r3 = warp_max(r3);
-            if (lane == 0) {
-                red[0][warp] = r1;
-                red[1][warp] = r2;
-                red[2][warp] = r3;
-            }
-        }
-        const unsigned sm = wa.n9[c].sysmask;
-        const bool xedge = sm && ((rb == 0 && (sm & 0x7u)) || (rb == tr - 1 && (sm & 0x1C0u)) ||
-                                  (cb == 0 && (sm & 0x49u)) || (cb == tc - 1 && (sm & 0x124u)));
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        if (xedge) __threadfence_system();
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * CW));
-        if (tid == 0) {
-            if (RESID && wa.resid) {
-#pragma unroll
-                for (int l = 0; l < 3; ++l) {
-                    double m = red[l][0];
-#pragma unroll
-                    for (int w = 1; w < CW; ++w) m = fmax(m, red[l][w]);
-                    resid_max(wa.resid + 3 * k + l, m);
-                }
-            }
-            const unsigned v = wa.base + 3u * (unsigned)k + 3u;
-            if (xedge) {
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
-                             : "memory");
-            } else {
-                __threadfence();
-                st_release_gpu_u32(wa.done + tile, v);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // volume update, TMA variant.  Tile: V_CW consumer warps = V_CW y-rows
 // (j0 .. j0+V_CW-1) x 64 z-columns (two per lane), marching planes i along x.
 // Stage q holds plane i0-1+q of the tile plus its y/z halo: V_CW+2 row spans
@@ -3026,11 +2519,6 @@ struct Plan {
     // 0 = this plan's own count)
     int64_t tiling_chunks = 0;
     int64_t tn() const { return tiling_chunks > 0 ? tiling_chunks : (int64_t)nchunks; }
-    // Jacobi steps per fused pass: 2 (slab_wave2_kernel, default) or 3
-    // (slab_wave3_kernel, experimental: measured slower); HRT_PASS_STEPS
-    int pass_steps = 2;
-    int pgrid3 = 0;                // resident CTA slots of slab_wave3_kernel
-    int64_t pkey3 = -1;
     // two steps per launch for x-band volumes (volume2_kernel): opt-in
     // (HRT_FUSE3=1) — bit-exact but measured slower than one step per launch
     // on B200 (322 vs 350 GLUPS at 1024x1024x768: instruction-bound)
@@ -3225,18 +2713,6 @@ static void set_carveouts() {
     C2(4);
     C2(2);
 #undef C2
-#define C3(CW)                                    \
-    carveout(slab_wave3_kernel<true, true, CW, false>);    \
-    carveout(slab_wave3_kernel<true, false, CW, false>);   \
-    carveout(slab_wave3_kernel<false, true, CW, false>);   \
-    carveout(slab_wave3_kernel<false, false, CW, false>);  \
-    carveout(slab_wave3_kernel<true, true, CW, true>);     \
-    carveout(slab_wave3_kernel<true, false, CW, true>);    \
-    carveout(slab_wave3_kernel<false, true, CW, true>);    \
-    carveout(slab_wave3_kernel<false, false, CW, true>)
-    C3(4);
-    C3(2);
-#undef C3
     carveout(slab_update_tma_kernel);
     carveout(volume_update_tma_kernel<true>);
     carveout(volume_wave_kernel<true>);
@@ -3530,17 +3006,9 @@ static bool fuse2_use(const Plan* p) {
     return per_chunk * p->tn() >= fuse2_slots(p);
 }
 
-// three steps per pass: the rims are 3 cells deep, so every tile (and the
-// 16-byte pieces read from west/east neighbours) must be at least that big
-static bool pass3_use(const Plan* p) {
-    if (p->pass_steps != 3 || !fuse2_use(p)) return false;
-    const int64_t ex = p->L.ext[0], ey = p->L.ext[1], rows = p->rows;
-    return ex >= 3 && ey >= 4 && rows >= 3 && (ex % rows == 0 || ex % rows >= 3);
-}
-
 // steps per fused pass this plan runs (0: one step per pass)
 static int pass_steps_of(const Plan* p) {
-    return pass3_use(p) ? 3 : (fuse2_use(p) || p->fuse3_on()) ? 2 : 0;
+    return (fuse2_use(p) || p->fuse3_on()) ? 2 : 0;
 }
 
 template <bool G, bool R, int CW, bool F>
@@ -3567,33 +3035,9 @@ static int wave2_occupancy(bool guard) {
     return n * sm_count(dev);
 }
 
-template <bool G, bool R, int CW, bool F>
-static int w3_blocks_per_sm() {
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, slab_wave3_kernel<G, R, CW, F>,
-                                                  w2_threads(CW), 0);
-    return n;
-}
-
-template <int CW>
-static int wave3_occupancy(bool guard) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int n = guard ? std::min(std::min(w3_blocks_per_sm<true, true, CW, false>(),
-                                            w3_blocks_per_sm<true, false, CW, false>()),
-                                   std::min(w3_blocks_per_sm<true, true, CW, true>(),
-                                            w3_blocks_per_sm<true, false, CW, true>()))
-                        : std::min(std::min(w3_blocks_per_sm<false, true, CW, false>(),
-                                            w3_blocks_per_sm<false, false, CW, false>()),
-                                   std::min(w3_blocks_per_sm<false, true, CW, true>(),
-                                            w3_blocks_per_sm<false, false, CW, true>()));
-    return n * sm_count(dev);
-}
-
-// nf passes of `steps` (2 or 3) Jacobi steps each from step `first` in one
-// slab_wave2_kernel / slab_wave3_kernel launch
+// nf passes (2 steps each) from step `first` in one slab_wave2_kernel launch
 static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
-                        unsigned long long* resid_base, int steps) {
+                        unsigned long long* resid_base) {
     if (nf <= 0) return HRT_OK;
     const bool narrow = p->narrow_chunk();
     int64_t tc = 0;
@@ -3647,17 +3091,15 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
                             cudaMemcpyHostToDevice));
     }
     const int64_t key2 = T * 4 + (p->nonneg ? 1 : 0);
-    int& pg = steps == 3 ? p->pgrid3 : p->pgrid2;
-    int64_t& pk = steps == 3 ? p->pkey3 : p->pkey2;
-    if (pg == 0 || pk != key2) {
-        pg = steps == 3 ? (narrow ? wave3_occupancy<2>(!p->nonneg) : wave3_occupancy<4>(!p->nonneg))
-                        : (narrow ? wave2_occupancy<2>(!p->nonneg) : wave2_occupancy<4>(!p->nonneg));
+    int& pg = p->pgrid2;
+    if (pg == 0 || p->pkey2 != key2) {
+        pg = narrow ? wave2_occupancy<2>(!p->nonneg) : wave2_occupancy<4>(!p->nonneg);
         HRT_CUDA(cudaGetLastError());
         if (pg <= 0) {
-            set_error("fused-pass kernel: no resident CTA slots");
+            set_error("two-step kernel: no resident CTA slots");
             return HRT_E_CUDA;
         }
-        pk = key2;
+        p->pkey2 = key2;
     }
     HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
     const hrt_chunk_layout_t& L = p->L;
@@ -3686,8 +3128,7 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     int threads;
     // every column tile full: the chunk width is a multiple of the tile's
     const bool full = L.ext[1] % (narrow ? 256 : T4_COLS) == 0;
-#define WK2(G, R, CW, F) \
-    (steps == 3 ? (void*)slab_wave3_kernel<G, R, CW, F> : (void*)slab_wave2_kernel<G, R, CW, F>)
+#define WK2(G, R, CW, F) (void*)slab_wave2_kernel<G, R, CW, F>
 #define PICKF(CW, F)                                                    \
     (guard ? (res ? WK2(true, true, CW, F) : WK2(true, false, CW, F))    \
            : (res ? WK2(false, true, CW, F) : WK2(false, false, CW, F)))
@@ -3701,7 +3142,7 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     const unsigned grid = (unsigned)std::min<int64_t>(pg, T);
     void* args[] = {&wa};
     HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3((unsigned)threads), args, smem, s));
-    p->pbase += (unsigned)steps * (unsigned)nf;
+    p->pbase += 2u * (unsigned)nf;
     p->ghosts_ready = false;  // passes read neighbours in place; ghost planes went stale
     return HRT_OK;
 }
@@ -3712,19 +3153,11 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
 static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                           unsigned long long* resid_base) {
     if (n <= 0) return HRT_OK;
-    if (pass3_use(p) && n >= 3) {
-        // n mod 3 single steps, then passes of three (each pass flips the
-        // buffer parity once, like an odd number of single steps)
-        const int64_t nf = n / 3, nr = n - 3 * nf;
-        int rc = nr ? launch_persist1(p, s, first, nr, resid_base) : HRT_OK;
-        if (rc) return rc;
-        return launch_fused(p, s, first + nr, nf, resid_base, 3);
-    }
     if (fuse2_use(p) && n >= 4) {
         const int64_t nf = (n / 4) * 2, nr = n - 2 * nf;
         int rc = nr ? launch_persist1(p, s, first, nr, resid_base) : HRT_OK;
         if (rc) return rc;
-        return launch_fused(p, s, first + nr, nf, resid_base, 2);
+        return launch_fused(p, s, first + nr, nf, resid_base);
     }
     return launch_persist1(p, s, first, n, resid_base);
 }
@@ -3937,7 +3370,7 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     p->rows = 64;
     if (const char* e = getenv("HRT_NARROW")) p->narrow_ok = e[0] != '0';
     if (const char* e = getenv("HRT_FUSE2")) p->fuse2 = e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
-    if (const char* e = getenv("HRT_PASS_STEPS")) p->pass_steps = e[0] == '3' ? 3 : 2;
+
     if (const char* e = getenv("HRT_FUSE3")) p->fuse3 = e[0] != '0';
     *plan = p;
     return HRT_OK;
@@ -4288,12 +3721,6 @@ int hrt_jacobi_plan_set_tiling_chunks(void* plan, int64_t n) {
     Plan* p = reinterpret_cast<Plan*>(plan);
     HRT_CHECK_ARG(!p->persist, "set the tiling chunk count before persistent mode");
     p->tiling_chunks = n;
-    return HRT_OK;
-}
-
-int hrt_jacobi_plan_set_pass_steps(void* plan, int steps) {
-    HRT_CHECK_ARG(plan && (steps == 2 || steps == 3), "steps per pass must be 2 or 3");
-    reinterpret_cast<Plan*>(plan)->pass_steps = steps;
     return HRT_OK;
 }
 

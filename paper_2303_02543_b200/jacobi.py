@@ -699,17 +699,12 @@ class JacobiSolver:
         neighbour would read stale ghosts, and neighbours counting steps in
         passes of 3 and of 2 would wait on each other's counters at
         different strides.  ``every`` holds each GPU's (rows, tiles per
-        chunk, steps per pass); if only some GPUs can run three-step
-        passes, all fall back to two; if only some can fuse, none does."""
+        chunk, steps per pass); if only some GPUs can fuse, none does."""
         if len({t[:2] for t in every}) != 1:
             raise HrtError(f"per-chunk tilings differ across GPUs: {every}")
-        ks = {t[2] for t in every}
-        if len(ks) != 1:
+        if len({t[2] for t in every}) != 1:
             for plan in self.plans.values():
-                if 0 in ks:
-                    N.call("hrt_jacobi_plan_set_fuse2", plan, 0)
-                else:
-                    N.call("hrt_jacobi_plan_set_pass_steps", plan, 2)
+                N.call("hrt_jacobi_plan_set_fuse2", plan, 0)
 
     def _setup_persistent(self) -> None:
         g = self.used_gpus[0]
@@ -992,7 +987,7 @@ class JacobiSolver:
 
     def tiling(self) -> dict[int, tuple[int, int, int]]:
         """Per GPU: (rows per tile, tiles per chunk, Jacobi steps per fused
-        pass — 3, 2, or 0 for one step per pass)."""
+        pass — 2, or 0 for one step per pass)."""
         out = {}
         for g in self.used_gpus:
             r, t, k = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
@@ -1004,7 +999,7 @@ class JacobiSolver:
     @property
     def steps_per_pass(self) -> int:
         """Jacobi steps one pass over HBM covers in runs of several steps
-        (3: slab_wave3_kernel, 2: slab_wave2_kernel / volume2_kernel, 1)."""
+        (2: slab_wave2_kernel / volume2_kernel, else 1)."""
         ks = {t[2] for t in self.tiling().values()}
         return max(1, min(ks)) if ks and 0 not in ks else 1
 

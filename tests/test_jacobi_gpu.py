@@ -349,27 +349,20 @@ def test_full_size_cfg3_and_cfg5_properties(hrt):
 ])
 @pytest.mark.parametrize("steps", [3, 4, 6, 7, 13])
 @pytest.mark.parametrize("rows", [None, 64])
-@pytest.mark.parametrize("pass_steps", ["3", "2"])
-def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, pass_steps, monkeypatch):
-    """Fused passes — slab_wave3_kernel (three Jacobi steps per pass, 3-cell
-    rims, u(t+1) and u(t+2) in registers, column neighbours by shuffles and
-    warp-edge chains) and slab_wave2_kernel (two steps, 2-cell rims) —
-    reading their rims from the 3 x 3 chunk neighbourhood, against the
-    numpy oracle on random signed data: field and every step's residual
-    bitwise, with the leftover single steps (n mod 3, n mod 4) first."""
+def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, monkeypatch):
+    """slab_wave2_kernel (two Jacobi steps per pass, 2-cell rims read from the
+    3 x 3 chunk neighbourhood, u(t+1) only in registers) against the numpy
+    oracle on random signed data: field and every step's residual bitwise,
+    with n mod 4 single steps before the passes."""
     from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
 
     monkeypatch.setenv("HRT_FUSE2", "2")  # these domains are too small for the auto policy
-    monkeypatch.setenv("HRT_PASS_STEPS", pass_steps)
     rng = np.random.default_rng(steps * 7 + dom[0])
     init = rng.random(dom) * 4.0 - 1.0
     s = JacobiSolver(ChunkGrid(dom, grid=grid), rows=rows)
     ex, ey = dom[0] // grid[0], dom[1] // grid[1]
-    r = rows or 64  # (these domains are below the 256-row threshold)
-    if ex % (rows or 64) != 1 and ey % 2 == 0:
-        assert s.two_step, "fused passes should apply here"
-    if pass_steps == "3" and s.two_step and ex >= 3 and ey >= 4 and ex % r not in (1, 2):
-        assert s.steps_per_pass == 3, s.tiling()
+    if ex % (rows or 64) != 1 and ey % 2 == 0:   # (below the 256-row threshold: 64-row tiles)
+        assert s.two_step and s.steps_per_pass == 2, "two-step passes should apply here"
     s.upload(init)
     s.run(steps, residual=True)
     got = s.download()
