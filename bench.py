@@ -338,7 +338,7 @@ def run_ours(args):
     # updates: their algorithmic bytes are 8 per lattice update; the naive
     # one-step algorithm's 16 B/update is reported beside it.
     persistent = bool(getattr(solver, "persistent", False))
-    # steps one fused pass covers (2: slab_wave2_kernel / volume2_kernel, 1:
+    # steps one fused pass covers (2: slab_wave2_kernel, 1:
     # one step per pass); a run of `iters` steps is n_single one-step sweeps
     # plus n_pass fused passes, each reading u once and writing once: 16
     # algorithmic bytes per cell and sweep/pass
@@ -365,7 +365,7 @@ def run_ours(args):
               2: f"slab_update_tma4_kernel<false,true,{cw},push>",
               1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant])
     if grid.slab is False:
-        kname = "volume2_kernel<true>" if two_step else "volume_update_tma_kernel<true>"
+        kname = "volume_update_tma_kernel<true>"
     traffic = (args.traffic if args.traffic is not None else
                _recorded_traffic(wl["name"] + ("_two_step" if k == 2 else ""), world))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -255,10 +255,6 @@ int hrt_jacobi_plan_set_fuse2(void *plan, int mode);
 /* The plan's tiling: rows per tile, tiles per chunk, and the Jacobi steps
  * per fused pass runs of several steps use (0 = one step per pass). */
 int hrt_jacobi_plan_tiling(void *plan, int64_t *rows, int64_t *tiles_per_chunk, int *steps_per_pass);
-/* x-band volumes on one GPU: per chunk its -x/+x neighbour (plan-local
- * index, -1 = domain face; y/z faces must be domain faces) — enables two
- * steps per launch (volume2_kernel).  Null clears. */
-int hrt_jacobi_plan_set_xnbr(void *plan, const int32_t *xnb2);
 /* Synchronises; *err = 0 ok, 1 IPC edge wait timed out, 2 persistent
  * dependency wait timed out (results void). */
 int hrt_jacobi_plan_error(void *plan, int *err);

@@ -1745,220 +1745,6 @@ volume_update_tma_kernel(VolArgs a) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// Two steps per launch for volumes split only along x (x-band chunks of one
-// GPU: y/z faces are all domain faces).  A tile (8 y-rows x 64 z-columns,
-// marching x planes i0 .. i1) reads u(t) planes i0-2 .. i1+2 — from its own
-// buffer or in place from the x-neighbour chunk — with a 2-cell y/z rim
-// (12 rows x 68 z per stage), computes u(t+1) on planes i0-1 .. i1+1 over
-// the tile plus a one-cell y/z rim into a 3-plane shared ring (own cells
-// also in registers for the x window), then u(t+2) on the tile.  Cells
-// outside the domain keep BOUNDARY in u(t+1) (the reference's ghost shell);
-// every value uses the reference's operation order, so results stay
-// bitwise equal.  No halo pass: the neighbour's planes are read directly.
-
-constexpr int V2_CW = 8;                 // consumer warps = y rows
-constexpr int V2_R0 = V2_CW + 4;         // u(t) rows per stage (2-row rim)
-constexpr int V2_R1 = V2_CW + 2;         // u(t+1) rows per shared plane
-constexpr int V2_Z = V_ZROW;             // 68 z positions (k0-2 .. k0+65)
-#ifndef HRT_V2_STAGES
-#define HRT_V2_STAGES 8
-#endif
-constexpr int V2_STAGES = HRT_V2_STAGES;
-constexpr size_t V2_SMEM = sizeof(double) * ((size_t)V2_STAGES * V2_R0 * V2_Z + 3 * V2_R1 * V2_Z);
-
-struct Vol2Args {
-    const ChunkBufs* chunks;
-    const int* xnb;          // [nchunks][2] chunk at -x / +x, or -1 (domain face)
-    int parity;
-    int64_t ex, ey, ez, sx, sy, origin;
-    int64_t rows, tiles_i, tiles_j, tiles_k;
-    unsigned long long* resid;  // nullable: 2 slots (step, step + 1)
-    const double* ones;         // >= V2_Z doubles of BOUNDARY
-};
-
-template <bool RESID>
-__global__ void __launch_bounds__(32 * (V2_CW + 1), 3)
-volume2_kernel(Vol2Args a) {
-    extern __shared__ __align__(128) unsigned char v2_smem[];
-    auto ring = reinterpret_cast<double (*)[V2_R0][V2_Z]>(v2_smem);
-    auto u1s = reinterpret_cast<double (*)[V2_R1][V2_Z]>(
-        v2_smem + sizeof(double) * (size_t)V2_STAGES * V2_R0 * V2_Z);
-    __shared__ alignas(8) uint64_t full[V2_STAGES], empty[V2_STAGES];
-    __shared__ double red[2][V2_CW];
-
-    const int64_t per_chunk = a.tiles_i * a.tiles_j * a.tiles_k;
-    const int64_t t = blockIdx.x;
-    const int64_t c = t / per_chunk;
-    int64_t rem = t - c * per_chunk;
-    const int64_t ti = rem / (a.tiles_j * a.tiles_k);
-    rem -= ti * a.tiles_j * a.tiles_k;
-    const int64_t tj = rem / a.tiles_k;
-    const int64_t tk = rem - tj * a.tiles_k;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t k0 = 1 + tk * V_ZW, j0 = 1 + tj * V2_CW;
-    const int64_t i0 = 1 + ti * a.rows, i1 = min(a.ex, i0 + a.rows - 1);
-    const int np = (int)(i1 - i0 + 5);  // u(t) planes i0-2 .. i1+2
-    const int xm_c = a.xnb[2 * c], xp_c = a.xnb[2 * c + 1];
-
-    if (tid == 0) {
-        for (int k = 0; k < V2_STAGES; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], V2_CW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-
-    if (warp == V2_CW) {  // producer
-        if (lane != 0) return;
-        const int64_t klast = min(k0 + V_ZW - 1, a.ez);
-        const uint32_t bytes = (uint32_t)((((klast - k0 + 4) + 1) & ~int64_t(1)) * 8);
-        int s = 0;
-        uint32_t ph = 0;
-        for (int q = 0; q < np; ++q) {
-            const int64_t pl = i0 - 2 + q;
-            const double* base;  // plane pl's element (0, 0, 0) (origin included), or null
-            if (pl >= 1 && pl <= a.ex) base = a.chunks[c].b[a.parity] + a.origin + pl * a.sx;
-            else if (pl < 1 && xm_c >= 0) base = a.chunks[xm_c].b[a.parity] + a.origin + (a.ex + pl) * a.sx;
-            else if (pl > a.ex && xp_c >= 0) base = a.chunks[xp_c].b[a.parity] + a.origin + (pl - a.ex) * a.sx;
-            else if (pl == 0 || pl == a.ex + 1) base = a.chunks[c].b[a.parity] + a.origin + pl * a.sx;
-            else base = nullptr;  // beyond the domain's ghost plane
-            mbar_wait_sleep(&empty[s], ph ^ 1);
-            mbar_expect_tx(&full[s], bytes * (uint32_t)V2_R0);
-            for (int r = 0; r < V2_R0; ++r) {
-                const int64_t y = j0 - 2 + r;
-                const double* src = (base && y >= 0 && y <= a.ey + 1) ? base + y * a.sy + (k0 - 2)
-                                                                     : a.ones;
-                tma_row_load(&ring[s][r][0], src, bytes, &full[s]);
-            }
-            if (++s == V2_STAGES) {
-                s = 0;
-                ph ^= 1;
-            }
-        }
-        return;
-    }
-
-    // consumers: own cell (y = j0+warp, z = k0+2*lane, +1) at stage row
-    // warp+2 / u1 row warp+1, column cz = 2*lane+2
-    const int cz = 2 * lane + 2;
-    const int r0 = warp + 2, r1 = warp + 1;
-    const int64_t y = j0 + warp, z = k0 + 2 * lane;
-    const bool yok = y <= a.ey;
-    const bool act = yok && z <= a.ez, both = act && z + 1 <= a.ez;
-    // rim cells of u(t+1): rows j0-1 / j0+8 (all 66 z) and columns k0-1 /
-    // k0+64 of the 8 own rows; thread e < 148 computes rim cell e
-    int er = -1, ec = 0;
-    if (tid < 132) {
-        er = tid < 66 ? 0 : V2_R1 - 1;
-        ec = 1 + (tid < 66 ? tid : tid - 66);
-    } else if (tid < 148) {
-        er = 1 + (tid - 132) / 2;
-        ec = ((tid - 132) & 1) ? 66 : 1;
-    }
-    auto outside = [&](int64_t yy, int64_t zz) {
-        return yy < 1 || yy > a.ey || zz < 1 || zz > a.ez;
-    };
-    const bool own_out0 = outside(y, z), own_out1 = outside(y, z + 1);
-    const bool rim_out = er >= 0 && outside(j0 - 1 + er, k0 - 2 + ec);
-    double* wr = a.chunks[c].b[a.parity ^ 1] + a.origin + i0 * a.sx + y * a.sy + z;
-    const double zg = 0.0;  // (unused: volumes have real z neighbours)
-    (void)zg;
-    double rm1 = 0.0, rm2 = 0.0;
-    double2 w0 = make_double2(0.0, 0.0), w1 = w0;  // u(t+1) own cells, planes q-2, q-1
-    int s = 0;
-    uint32_t ph = 0;
-    // stages of planes q-1, q, q+1 are s-2, s-1, s (mod); start: wait planes i0-2, i0-1
-    auto slot = [&](int back) { int v = s - back; return v < 0 ? v + V2_STAGES : v; };
-    mbar_wait(&full[0], 0);
-    mbar_wait(&full[1 % V2_STAGES], V2_STAGES > 1 ? 0 : 1);
-    s = 2 % V2_STAGES;
-    ph = (2 >= V2_STAGES) ? 1 : 0;
-    for (int q = 1; q < np - 1; ++q) {  // u(t+1) on plane i0-2+q
-        const int64_t pl = i0 - 2 + q;
-        mbar_wait(&full[s], ph);        // plane pl+1
-        const int sm = slot(2), sc = slot(1), sp = s;
-        const bool pout = (pl < 1 && xm_c < 0) || (pl > a.ex && xp_c < 0);
-        // own cells
-        const double2 xm = *reinterpret_cast<const double2*>(&ring[sm][r0][cz]);
-        const double2 xp = *reinterpret_cast<const double2*>(&ring[sp][r0][cz]);
-        const double2 ym = *reinterpret_cast<const double2*>(&ring[sc][r0 - 1][cz]);
-        const double2 yp = *reinterpret_cast<const double2*>(&ring[sc][r0 + 1][cz]);
-        const double2 ce = *reinterpret_cast<const double2*>(&ring[sc][r0][cz]);
-        const double zm = ring[sc][r0][cz - 1], zp = ring[sc][r0][cz + 2];
-        double2 u;
-        u.x = div6(sum6(xm.x, xp.x, ym.x, yp.x, zm, ce.y));
-        u.y = div6(sum6(xm.y, xp.y, ym.y, yp.y, ce.x, zp));
-        if (pout || own_out0) u.x = HRT_BOUNDARY;
-        if (pout || own_out1) u.y = HRT_BOUNDARY;
-        *reinterpret_cast<double2*>(&u1s[q % 3][r1][cz]) = u;
-        if (RESID && pl >= i0 && pl <= i1) {
-            if (act) rm1 = rmax_acc(rm1, fabs(__dsub_rn(u.x, ce.x)));
-            if (both) rm1 = rmax_acc(rm1, fabs(__dsub_rn(u.y, ce.y)));
-        }
-        // rim cell
-        if (er >= 0) {
-            const int rr = er + 1;  // stage row
-            double v = div6(sum6(ring[sm][rr][ec], ring[sp][rr][ec], ring[sc][rr - 1][ec],
-                                 ring[sc][rr + 1][ec], ring[sc][rr][ec - 1], ring[sc][rr][ec + 1]));
-            if (pout || rim_out) v = HRT_BOUNDARY;
-            u1s[q % 3][er][ec] = v;
-        }
-        // plane pl-1 (stage sm) is no longer needed
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[sm]);
-        if (++s == V2_STAGES) {
-            s = 0;
-            ph ^= 1;
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * V2_CW));
-        // u(t+2) on plane pl-1 from u(t+1) planes pl-2 (w0), pl-1 (w1), pl (u)
-        if (q >= 3) {
-            const int b = (q - 1) % 3;
-            const double2 ym2 = *reinterpret_cast<const double2*>(&u1s[b][r1 - 1][cz]);
-            const double2 yp2 = *reinterpret_cast<const double2*>(&u1s[b][r1 + 1][cz]);
-            const double zm2 = u1s[b][r1][cz - 1], zp2 = u1s[b][r1][cz + 2];
-            const double ox = div6(sum6(w0.x, u.x, ym2.x, yp2.x, zm2, w1.y));
-            const double oy = div6(sum6(w0.y, u.y, ym2.y, yp2.y, w1.x, zp2));
-            if (both) {
-                *reinterpret_cast<double2*>(wr) = make_double2(ox, oy);
-                if (RESID) {
-                    rm2 = rmax_acc(rm2, fabs(__dsub_rn(ox, w1.x)));
-                    rm2 = rmax_acc(rm2, fabs(__dsub_rn(oy, w1.y)));
-                }
-            } else if (act) {
-                wr[0] = ox;
-                if (RESID) rm2 = rmax_acc(rm2, fabs(__dsub_rn(ox, w1.x)));
-            }
-            wr += a.sx;
-        }
-        w0 = w1;
-        w1 = u;
-    }
-    // release the last two stages' slots are not reused: the tile ends here
-    if (RESID && a.resid) {
-        rm1 = warp_max(rm1);
-        rm2 = warp_max(rm2);
-        if (lane == 0) {
-            red[0][warp] = rm1;
-            red[1][warp] = rm2;
-        }
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * V2_CW));
-        if (tid == 0) {
-            double m1 = red[0][0], m2 = red[1][0];
-            for (int w = 1; w < V2_CW; ++w) {
-                m1 = rmax_acc(m1, red[0][w]);
-                m2 = rmax_acc(m2, red[1][w]);
-            }
-            resid_max(a.resid, m1);
-            resid_max(a.resid + 1, m2);
-        }
-    }
-}
-
 // Persistent wavefront for volumes: the slab protocol (tickets, per-tile
 // step counters, tile-descriptor queue, timeouts) with 6-neighbour tile
 // dependencies — (i, j, k) block neighbours inside a chunk, the adjacent
@@ -2519,16 +2305,6 @@ struct Plan {
     // 0 = this plan's own count)
     int64_t tiling_chunks = 0;
     int64_t tn() const { return tiling_chunks > 0 ? tiling_chunks : (int64_t)nchunks; }
-    // two steps per launch for x-band volumes (volume2_kernel): opt-in
-    // (HRT_FUSE3=1) — bit-exact but measured slower than one step per launch
-    // on B200 (322 vs 350 GLUPS at 1024x1024x768: instruction-bound)
-    bool fuse3 = false;
-    int* d_xnb = nullptr;          // [nchunks][2] x neighbours (plan-local) or -1
-    bool fuse3_on() const {
-        return fuse3 && d_xnb && L.ndim == 3 && !vpush_on() && !persist_on() &&
-               remote.empty() && !ipc && L.origin % 2 == 1 && L.stride[1] % 2 == 0 &&
-               L.ext[0] >= 2;
-    }
     Nbr9* d_n9 = nullptr;          // [nchunks] 3 x 3 chunk neighbourhood
     int64_t n9_key = -1;           // tiles per chunk the table was built for
     // faces to other processes (hrt_jacobi_plan_set_wave2_remote): per chunk
@@ -2726,12 +2502,6 @@ static void set_carveouts() {
                          (int)V_SMEM);
     cudaFuncSetAttribute(volume_wave_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)V_SMEM);
-    carveout(volume2_kernel<true>);
-    carveout(volume2_kernel<false>);
-    cudaFuncSetAttribute(volume2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)V2_SMEM);
-    cudaFuncSetAttribute(volume2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)V2_SMEM);
     cudaGetLastError();
 }
 
@@ -3008,7 +2778,7 @@ static bool fuse2_use(const Plan* p) {
 
 // steps per fused pass this plan runs (0: one step per pass)
 static int pass_steps_of(const Plan* p) {
-    return (fuse2_use(p) || p->fuse3_on()) ? 2 : 0;
+    return fuse2_use(p) ? 2 : 0;
 }
 
 template <bool G, bool R, int CW, bool F>
@@ -3218,44 +2988,6 @@ static int launch_persist1(Plan* p, cudaStream_t s, int64_t first, int64_t n,
     return HRT_OK;
 }
 
-// steps (step, step+1) of an x-band volume plan in one volume2_kernel launch,
-// reading buffer `parity` and writing parity^1 (launches alternate buffers)
-static int launch_fused3(Plan* p, cudaStream_t s, int64_t step, int parity,
-                         unsigned long long* resid_base) {
-    const hrt_chunk_layout_t& L = p->L;
-    if (!p->d_ones) {
-        std::vector<double> ones(T4_COLS + 8, HRT_BOUNDARY);
-        HRT_CUDA(cudaMalloc(&p->d_ones, sizeof(double) * ones.size()));
-        HRT_CUDA(cudaMemcpy(p->d_ones, ones.data(), sizeof(double) * ones.size(),
-                            cudaMemcpyHostToDevice));
-    }
-    Vol2Args a{};
-    a.chunks = p->d_chunks;
-    a.xnb = p->d_xnb;
-    a.parity = parity;
-    a.ex = L.ext[0];
-    a.ey = L.ext[1];
-    a.ez = L.ext[2];
-    a.sx = L.stride[0];
-    a.sy = L.stride[1];
-    a.origin = L.origin;
-    a.rows = p->rows;
-    a.tiles_i = (a.ex + a.rows - 1) / a.rows;
-    a.tiles_j = (a.ey + V2_CW - 1) / V2_CW;
-    a.tiles_k = (a.ez + V_ZW - 1) / V_ZW;
-    a.resid = resid_base ? resid_base + step : nullptr;
-    a.ones = p->d_ones;
-    const int64_t grid = (int64_t)p->nchunks * a.tiles_i * a.tiles_j * a.tiles_k;
-    if (grid == 0) return HRT_OK;
-    if (a.resid)
-        volume2_kernel<true><<<(unsigned)grid, 32 * (V2_CW + 1), V2_SMEM, s>>>(a);
-    else
-        volume2_kernel<false><<<(unsigned)grid, 32 * (V2_CW + 1), V2_SMEM, s>>>(a);
-    HRT_CUDA(cudaGetLastError());
-    p->ghosts_ready = false;
-    return HRT_OK;
-}
-
 static int do_step(Plan* p, cudaStream_t s, int64_t step, unsigned long long* resid_base) {
     const int parity = (int)(step & 1);
     unsigned long long* slot = resid_base ? resid_base + step : nullptr;
@@ -3371,7 +3103,6 @@ int hrt_jacobi_plan_create(int gpu, const hrt_chunk_layout_t* layout, int nchunk
     if (const char* e = getenv("HRT_NARROW")) p->narrow_ok = e[0] != '0';
     if (const char* e = getenv("HRT_FUSE2")) p->fuse2 = e[0] == '0' ? 0 : (e[0] == '2' ? 2 : 1);
 
-    if (const char* e = getenv("HRT_FUSE3")) p->fuse3 = e[0] != '0';
     *plan = p;
     return HRT_OK;
 }
@@ -3628,24 +3359,6 @@ int hrt_jacobi_plan_set_wave2_remote(void* plan, const uint64_t* bufs8, const ui
     return HRT_OK;
 }
 
-// x-band volumes: per chunk its -x / +x neighbour (plan-local index, -1 at
-// a domain face; y/z faces must all be domain faces) — enables two steps
-// per launch (volume2_kernel).  Null clears.
-int hrt_jacobi_plan_set_xnbr(void* plan, const int32_t* xnb2) {
-    HRT_CHECK_ARG(plan, "null plan");
-    Plan* p = reinterpret_cast<Plan*>(plan);
-    int rc = use_device(p->gpu);
-    if (rc) return rc;
-    cudaFree(p->d_xnb);
-    p->d_xnb = nullptr;
-    if (!xnb2 || p->nchunks == 0) return HRT_OK;
-    for (int i = 0; i < 2 * p->nchunks; ++i)
-        HRT_CHECK_ARG(xnb2[i] >= -1 && xnb2[i] < p->nchunks, "x neighbour out of range");
-    HRT_CUDA(cudaMalloc(&p->d_xnb, sizeof(int) * 2 * p->nchunks));
-    HRT_CUDA(cudaMemcpy(p->d_xnb, xnb2, sizeof(int) * 2 * p->nchunks, cudaMemcpyHostToDevice));
-    return HRT_OK;
-}
-
 int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t timeout_ns) {
     HRT_CHECK_ARG(plan, "null plan");
     Plan* p = reinterpret_cast<Plan*>(plan);
@@ -3712,7 +3425,7 @@ int hrt_jacobi_plan_error(void* plan, int* err) {
 int hrt_jacobi_plan_two_step(void* plan, int* on) {
     HRT_CHECK_ARG(plan && on, "null argument");
     const Plan* p = reinterpret_cast<Plan*>(plan);
-    *on = (fuse2_use(p) || p->fuse3_on()) ? 1 : 0;
+    *on = fuse2_use(p) ? 1 : 0;
     return HRT_OK;
 }
 
@@ -3847,20 +3560,6 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
     cudaStream_t s = as_stream(stream)->s;
     unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
     if (p->persist_on()) return launch_persist(p, s, first, n, r);
-    if (p->fuse3_on() && n >= 4) {
-        // n mod 4 single steps, then pairs of two-step launches (the result
-        // lands in the buffer of parity first+n, like single steps)
-        const int64_t nf = (n / 4) * 2, nr = n - 2 * nf;
-        for (int64_t k = 0; k < nr; ++k) {
-            rc = do_step(p, s, first + k, r);
-            if (rc) return rc;
-        }
-        for (int64_t k = 0; k < nf; ++k) {
-            rc = launch_fused3(p, s, first + nr + 2 * k, (int)((first + nr + k) & 1), r);
-            if (rc) return rc;
-        }
-        return HRT_OK;
-    }
     // IPC step tags are per launch; in push mode graph replays measured 40 %
     // slower than direct launches on B200 (cause not yet identified; the
     // max-shared carveout did not change it), so push mode launches directly
@@ -3941,22 +3640,6 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
         if (total_ms) *total_ms = n ? a + b : 0.0;
         return HRT_OK;
     }
-    if (p->fuse3_on() && n >= 4) {
-        // single steps (n mod 4) + two-step launches; "update" is all of it
-        HRT_CUDA(cudaEventRecord(ev[0], s));
-        HRT_CUDA(cudaEventRecord(ev[1], s));
-        rc = hrt_jacobi_plan_run(plan, stream, first, n, resid, 0);
-        if (rc) return rc;
-        HRT_CUDA(cudaEventRecord(ev[2], s));
-        HRT_CUDA(cudaStreamSynchronize(s));
-        float a = 0, b = 0;
-        cudaEventElapsedTime(&a, ev[0], ev[1]);
-        cudaEventElapsedTime(&b, ev[1], ev[2]);
-        if (update_ms) *update_ms = b;
-        if (halo_ms) *halo_ms = a;
-        if (total_ms) *total_ms = a + b;
-        return HRT_OK;
-    }
     HRT_CUDA(cudaEventRecord(ev[0], s));
     const bool push = p->any_push();
     const bool split = p->split_on() || p->ipc_on();
@@ -4032,7 +3715,6 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_peer_done);
     cudaFree(p->d_n9);
     cudaFree(p->d_ones);
-    cudaFree(p->d_xnb);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);

@@ -470,18 +470,6 @@ class JacobiSolver:
                 self._setup_persistent()
             else:
                 self._setup_persistent_multi()
-        # x-band volumes on one GPU: two steps per launch (volume2_kernel)
-        if (L.ndim == 3 and not self.vpush and not remote_ops and len(self.used_gpus) == 1
-                and grid.grid[1] == 1 and grid.grid[2] == 1 and variant != CHECK_VARIANT):
-            g = self.used_gpus[0]
-            mine = [lin for lin in self.owned if self.placement[lin] == g]
-            index = {lin: i for i, lin in enumerate(mine)}
-            xnb = []
-            for lin in mine:
-                for f in (0, 1):
-                    nb = self.grid.chunks[lin].neighbors.get(f)
-                    xnb.append(index.get(nb, -1) if nb is not None else -1)
-            N.call("hrt_jacobi_plan_set_xnbr", self.plans[g], _arr(ctypes.c_int32, xnb))
         self._init_ghosts()
 
     def _set_nonneg(self, flag: bool) -> None:
@@ -999,7 +987,7 @@ class JacobiSolver:
     @property
     def steps_per_pass(self) -> int:
         """Jacobi steps one pass over HBM covers in runs of several steps
-        (2: slab_wave2_kernel / volume2_kernel, else 1)."""
+        (2: slab_wave2_kernel, else 1)."""
         ks = {t[2] for t in self.tiling().values()}
         return max(1, min(ks)) if ks and 0 not in ks else 1
 

@@ -372,33 +372,3 @@ def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, monkeypatc
     ref = oracle.jacobi_reference(dom, steps, initial=init, residuals=resid)
     assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
     assert np.array_equal(res, np.array(resid)), (res, resid)
-
-
-@pytest.mark.parametrize("dom,grid", [
-    ((40, 36, 70), (2, 1, 1)),       # x-bands, ragged z tile (64 + 6)
-    ((130, 17, 33), (2, 1, 1)),      # 65-plane chunks (x tiles 64 + 1), odd y and z extents
-    ((24, 8, 64), (4, 1, 1)),        # 6-plane chunks: rims reach across whole neighbours
-    ((12, 20, 10), (1, 1, 1)),       # one chunk: every rim is the domain boundary
-])
-@pytest.mark.parametrize("steps", [4, 5, 6, 9])
-def test_volume_two_step_launches_bitwise(hrt, oracle, dom, grid, steps, monkeypatch):
-    """volume2_kernel (x-band volumes: two Jacobi steps per launch, u(t)
-    planes read in place from the x-neighbour chunk, u(t+1) on a y/z rim in
-    shared memory) against the numpy oracle on random signed data: field
-    and every step's residual bitwise, with n mod 4 single steps first."""
-    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
-
-    monkeypatch.setenv("HRT_FUSE3", "1")  # opt-in (measured slower, DESIGN.md §6)
-    rng = np.random.default_rng(steps * 11 + dom[2])
-    init = rng.random(dom) * 4.0 - 1.0
-    s = JacobiSolver(ChunkGrid(dom, grid=grid))
-    assert s.two_step, "two-step launches should apply to x-band volumes"
-    s.upload(init)
-    s.run(steps, residual=True)
-    got = s.download()
-    res = s.residual_history()
-    s.close()
-    resid = []
-    ref = oracle.jacobi_reference(dom, steps, initial=init, residuals=resid)
-    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
-    assert np.array_equal(res, np.array(resid)), (res, resid)

@@ -10,7 +10,7 @@ mkdir -p "$OUT"
 export HRT_PERSIST_TIMEOUT_S=600
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in racecheck synccheck memcheck; do
-  for c in wave2 wave2_narrow wave tma4 tma volume_tma volume2; do
+  for c in wave2 wave2_narrow wave tma4 tma volume_tma; do
     timeout 900 $CS --tool $tool --print-limit 20 python tools/sanitize_cases.py $c \
       > "$OUT/${tool}_$c.log" 2>&1
     echo "$tool $c rc=$? $(grep -h 'ERROR SUMMARY\|RACECHECK SUMMARY\|case ' "$OUT/${tool}_$c.log" | tr '\n' ' ')" \

@@ -28,8 +28,6 @@ CASES = {
     "tma": ((130, 600, 1), (2, 2, 1), 3, {}, {"variant": 1}),
     # volume_update_tma_kernel (3D ring)
     "volume_tma": ((40, 36, 70), (2, 1, 1), 3, {}, {}),
-    # volume2_kernel (3D two steps per launch)
-    "volume2": ((24, 12, 40), (2, 1, 1), 4, {"HRT_FUSE3": "1"}, {}),
 }
 
 
