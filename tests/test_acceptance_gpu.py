@@ -111,7 +111,9 @@ def test_ac09_put_vs_writer_race_and_get(seed):
     rt1.release(target)
     # the writer (dst = dst*7 + salt) and a long-running kernel to hold it back
     rt1.register_kernel("writer", gpu_sim=Mix(salt))
-    scratch = DevicePool(0, 4096)
+    # the stamp slots live on rank 1's GPU (the kernels run there)
+    gpu1 = rt1.registry.gpu_of(rt1.registry.devices_of_type(DeviceType.GPU_SIM)[0])
+    scratch = DevicePool(gpu1, 4096)
     rt1.register_kernel("blocker", gpu_sim=Stamp(scratch.alloc(16)[2], ns=500_000))
     blocker_obj = rt1.create_object((8,), dtype=np.uint8)
     done = []
