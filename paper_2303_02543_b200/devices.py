@@ -27,6 +27,7 @@ bench/jacobi.py:232) target the B200; ``DeviceType.B200`` is an alias.
 from __future__ import annotations
 
 import ctypes
+from collections import deque
 import os
 import time
 from dataclasses import dataclass, field
@@ -136,7 +137,8 @@ class Stream:
     def record(self, kind: TokenKind = TokenKind.KERNEL, device_id: int = -1) -> "CompletionToken":
         t = ctypes.c_uint64()
         N.call("hrt_token_record", self.h, ctypes.byref(t))
-        return CompletionToken(t.value, kind, device_id if device_id >= 0 else self.gpu)
+        return CompletionToken(t.value, kind, device_id if device_id >= 0 else self.gpu,
+                               stream=self.h.value)
 
     def wait(self, token: "CompletionToken") -> None:
         """GPU-side edge: later work on this stream waits for ``token``."""
@@ -163,9 +165,11 @@ class CompletionToken:
     """
 
     __slots__ = ("token_id", "kind", "device_id", "_status", "error", "end_time", "_native",
-                 "__weakref__")
+                 "stream", "__weakref__")
 
-    def __init__(self, token_id: int, kind: TokenKind, device_id: int, native: bool = True):
+    def __init__(self, token_id: int, kind: TokenKind, device_id: int, native: bool = True,
+                 stream=None):
+        self.stream = stream  # the recording stream's handle (events complete in stream order)
         self.token_id = token_id
         self.kind = kind
         self.device_id = device_id
@@ -407,7 +411,7 @@ class DeviceClock:
 
     def __init__(self) -> None:
         self._t0 = time.perf_counter()
-        self._outstanding: list[CompletionToken] = []
+        self._outstanding: deque = deque()
 
     @property
     def now(self) -> float:
@@ -417,17 +421,22 @@ class DeviceClock:
         if token.status is TokenStatus.PENDING:
             self._outstanding.append(token)
 
-    def track_pending(self, token: CompletionToken) -> None:
-        """A token recorded just now (no status query: it is pending or
-        will be found complete by the next service pass)."""
-        self._outstanding.append(token)
-
     def schedule(self, token: CompletionToken, end_time: float) -> None:
         self.track(token)
 
+    def track_pending(self, token: CompletionToken) -> None:
+        """A token recorded just now (no status query: it is pending or
+        will be found complete by the next service pass).  Settled tokens at
+        the front are dropped here, so the queue stays as long as the work
+        actually in flight."""
+        q = self._outstanding
+        while q and q[0]._status is not TokenStatus.PENDING:
+            q.popleft()
+        q.append(token)
+
     def advance_one(self) -> Optional[CompletionToken]:
         while self._outstanding:
-            tok = self._outstanding.pop(0)
+            tok = self._outstanding.popleft()
             if tok.status is TokenStatus.PENDING:
                 tok.wait()
                 return tok
@@ -435,7 +444,7 @@ class DeviceClock:
 
     @property
     def pending_events(self) -> int:
-        self._outstanding = [t for t in self._outstanding if t.status is TokenStatus.PENDING]
+        self._outstanding = deque(t for t in self._outstanding if t.status is TokenStatus.PENDING)
         return len(self._outstanding)
 
 
@@ -454,6 +463,8 @@ class _Device:
         self.pool = DevicePool(gpu, descriptor.memory_capacity)
         self.compute_streams = [Stream(gpu, name=f"c{i}")
                                 for i in range(descriptor.compute_stream_count)]
+        # stream handle -> compute stream index (tokens carry their stream)
+        self.stream_index = {st.h.value: i for i, st in enumerate(self.compute_streams)}
         self.h2d = Stream(gpu, name="h2d")
         self.d2h = Stream(gpu, name="d2h")
 
@@ -709,8 +720,9 @@ class DeviceRegistry:
         token = CompletionToken(tid.value, TokenKind.TRANSFER, dev.device_id)
         self._tokens[token.token_id] = token
         self.clock.track_pending(token)
-        self.tracer.emit("transfer", device=dev.device_id, stream=stream.name, start=t0,
-                         end=t0, size=size)
+        if self.tracer.enabled:
+            self.tracer.emit("transfer", device=dev.device_id, stream=stream.name, start=t0,
+                             end=t0, size=size)
         return token
 
     def enqueue_kernel(
@@ -737,8 +749,10 @@ class DeviceRegistry:
         if not 0 <= stream_index < len(dev.compute_streams):
             raise HrtError(f"stream index {stream_index} out of range")
         stream = dev.compute_streams[stream_index]
+        here = stream.h.value
         for t in wait or ():
-            stream.wait(t)
+            if t is not None and t.stream != here:  # same stream: ordered already
+                stream.wait(t)
         views = [v for _, v in args]
         t0 = self.clock.now
         try:
@@ -749,9 +763,10 @@ class DeviceRegistry:
             return token
         token = stream.record(TokenKind.KERNEL, device_id)
         self._tokens[token.token_id] = token
-        self.clock.track(token)
-        self.tracer.emit("kernel", device=device_id, stream=stream.name, start=t0, end=t0,
-                         label=label or kernel_ref.name)
+        self.clock.track_pending(token)
+        if self.tracer.enabled:
+            self.tracer.emit("kernel", device=device_id, stream=stream.name, start=t0, end=t0,
+                             label=label or kernel_ref.name)
         return token
 
     def poll(self, token: Union[int, CompletionToken]) -> TokenStatus:
