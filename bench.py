@@ -544,7 +544,7 @@ def run_reference(args):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: the reference's initial state",
+        "data": "synthetic: the reference's initial state (interior 0.0, Dirichlet faces 1.0)",
         "config": config_for(wl, world, args.iters or wl["iters"]),
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
