@@ -365,7 +365,8 @@ def run_ours(args):
               2: f"slab_update_tma4_kernel<false,true,{cw},push>",
               1: "slab_update_tma_kernel", 0: "slab_update_kernel"}[args.variant])
     if grid.slab is False:
-        kname = "volume_update_tma_kernel<true>"
+        kname = ("volume_wave2_kernel<true,true>" if k == 2 else
+                 "volume_wave_kernel<true>" if persistent else "volume_update_tma_kernel<true>")
     traffic = (args.traffic if args.traffic is not None else
                _recorded_traffic(wl["name"] + ("_two_step" if k == 2 else ""), world))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -21,12 +21,15 @@
 //     with r=RN(1/6), which is correctly rounded (== IEEE s/6.0) whenever
 //     s/6 is normal; tiny/special inputs take the IEEE path.  Parity tests
 //     check it bitwise against IEEE division on the GPU.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -49,7 +52,7 @@ __device__ __forceinline__ double div6(double s) {
 #else
     const double r = 0x1.5555555555555p-3;  // RN(1/6)
     double q = __dmul_rn(s, r);
-    const double e = __fma_rn(-q, 6.0, s);  // exact remainder
+    const double e = -__fma_rn(q, 6.0, -s);  // exact remainder (sign of zero kept: -0/6 = -0)
     q = __fma_rn(e, r, q);
     const double a = fabs(s);
     if ((a < 0x1p-1019 && a != 0.0) || !(a <= 0x1p1000)) q = div6_ieee(s);
@@ -464,7 +467,7 @@ constexpr int T4_STAGES = 11;  // 11 x 4128 B ring: within the 48 KB static limi
 __device__ __forceinline__ double div6_fast(double s) {
     const double r = 0x1.5555555555555p-3;
     double q = __dmul_rn(s, r);
-    const double e = __fma_rn(-q, 6.0, s);
+    const double e = -__fma_rn(q, 6.0, -s);  // see div6
     return __fma_rn(e, r, q);
 }
 
@@ -1996,13 +1999,38 @@ halo_copy_kernel(const hrt_halo_seg_t* __restrict__ segs, int parity, int64_t bl
     }
 }
 
+// field scan at upload (volume plans): smallest positive value (as ~bits,
+// max-reduced: 0 = none yet) and a flag for any value the unguarded
+// division cannot take (negative, non-finite, > 2^997; -0.0 is fine)
+__device__ __forceinline__ void range_acc(unsigned long long& key, bool& bad, double v) {
+    const bool b = !(v >= 0.0) || v > 0x1p997;
+    bad |= b;
+    const unsigned long long k =
+        (v > 0.0 && !b) ? ~(unsigned long long)__double_as_longlong(v) : 0ull;
+    key = k > key ? k : key;
+}
+// whole warp
+__device__ __forceinline__ void range_flush(unsigned long long* range, unsigned long long key,
+                                            bool bad) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, key, o);
+        key = x > key ? x : key;
+    }
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if ((threadIdx.x & 31) == 0) {
+        if (anybad) atomicOr(range + 1, 1ull);
+        if (key > *reinterpret_cast<volatile unsigned long long*>(range)) atomicMax(range, key);
+    }
+}
+
 // contiguous (FX, FY, FZ) field <-> every chunk interior of a plan, one CTA
 // per interior row: upload scatter / gather (jacobi.py:425-435) in one launch
 __global__ void __launch_bounds__(256)
 field_copy_kernel(const ChunkBufs* __restrict__ chunks, const int64_t* __restrict__ offs, int parity,
                   int ndim, int64_t ex, int64_t ey, int64_t ez, int64_t sx, int64_t sy,
                   int64_t origin, double* __restrict__ field, int64_t FY, int64_t FZ,
-                  int to_chunks) {
+                  int to_chunks, unsigned long long* __restrict__ range) {
     const int64_t rows = ndim == 2 ? ex : ex * ey;
     const int64_t c = blockIdx.x / rows;
     const int64_t r = blockIdx.x - c * rows;
@@ -2021,7 +2049,16 @@ field_copy_kernel(const ChunkBufs* __restrict__ chunks, const int64_t* __restric
         frow = field + ((ox + i) * FY + (oy + j)) * FZ + oz;
         n = ez;
     }
-    if (to_chunks)
+    if (to_chunks && range) {
+        unsigned long long key = 0;
+        bool bad = false;
+        for (int64_t k = threadIdx.x; k < n; k += 256) {
+            const double v = frow[k];
+            crow[k] = v;
+            range_acc(key, bad, v);
+        }
+        range_flush(range, key, bad);
+    } else if (to_chunks)
         for (int64_t k = threadIdx.x; k < n; k += 256) crow[k] = frow[k];
     else
         for (int64_t k = threadIdx.x; k < n; k += 256) frow[k] = crow[k];
@@ -2215,6 +2252,460 @@ __global__ void div6_sweep_kernel(uint64_t seed, int64_t n, int mode,
 }
 
 // ---------------------------------------------------------------------------
+// TWO Jacobi steps per pass for volumes split along x (volume_wave2_kernel):
+// the 3D form of slab_wave2_kernel.  A tile is (all planes of a chunk) x
+// (VW_R y-rows) x (VW_TZ z-columns); pass k reads u(t) once — planes -1 ..
+// ex+2 (the first and last two from the x-neighbour chunks, in place), rows
+// j0-2 .. j0+VW_R+1, columns k0-2 .. k0+VW_TZ+1 — and writes only u(t+2).
+// 8 algorithmic bytes per lattice update instead of 16.
+//
+// Producer: one 3D TMA tensor copy per plane (box 124 x 8 x 1 of the chunk
+// buffer seen as a (ex+2, ey+2, sy) tensor); coordinates outside the buffer
+// (plane -1 / ex+2 at a domain face, row -1 / ey+2) are zero-filled by the
+// TMA unit and only ever feed values the consumer masks.
+// Consumer thread (warp w, lane L) owns column k = k0-1+30w+L and the
+// tile's VW_R rows; lanes 0 and 31 are rim columns (their u(t+2) is never
+// stored), so a warp outputs 30 columns and computes u(t+1) on 32.  u(t) of
+// the planes x-1, x, x+1 at the own column lives in registers (8 rows); its
+// z neighbours come from the ring stage of plane x; u(t+1) of three planes
+// lives in registers (6 rows) and its z neighbours come from the adjacent
+// lanes by shuffles.  Every value is computed with the reference's
+// operations in the reference's order (xm, xp, ym, yp, zm, zp), so the field
+// and both per-step residuals stay bitwise equal.
+// Dependencies: a tile of pass k needs its 3 x 3 x 3 neighbourhood — the
+// chunk and its x neighbours, y and z blocks +-1 — done with pass k-1 (RAW
+// on the rims it reads; WAR on the buffer it overwrites, which those tiles
+// read as rim).  Only chunks whose y and z faces are all domain faces.
+// Division: Markstein's sequence without a range check when the launch is
+// proven safe (vw2_fast below); otherwise the same sequence plus an integer
+// range test per sum, and a rare per-group recomputation with IEEE division
+// (no branch per cell: branches split the dependency chains the scheduler
+// interleaves).
+
+constexpr int VW_CW = 4;              // consumer warps, side by side in z
+constexpr int VW_R = 4;               // y rows per tile (per thread)
+constexpr int VW_ZO = 30;             // output columns per warp (lanes 1..30)
+constexpr int VW_TZ = VW_CW * VW_ZO;  // output columns per tile
+constexpr int VW_RS = VW_TZ + 4;      // ring row: columns k0-2 .. k0+VW_TZ+1
+constexpr int VW_RR = VW_R + 4;       // ring rows per plane: j0-2 .. j0+VW_R+1
+constexpr int VW_STAGES = 5;          // 5 x 8 x 124 doubles = 39.7 KB
+constexpr uint32_t VW_STAGE_BYTES = (uint32_t)(VW_RR * VW_RS * 8);
+
+struct VolW2Args {
+    const CUtensorMap* maps;   // [nchunks][2] tensor map of buffer 0 / 1
+    const ChunkBufs* chunks;
+    const int* xnb;            // [nchunks][2] -x / +x neighbour chunk or -1
+    unsigned int* done;        // [T] steps completed per tile (from 0 at launch)
+    unsigned long long* ticket;
+    const unsigned long long* range;  // field scan: [0] ~bits(min positive), [1] bad flag
+    double need;               // unguarded division is exact if min positive >= need
+    int nfused;                // passes (2 steps each)
+    int parity0;
+    int64_t ntiles, ex, ey, ez, sx, sy, origin, tiles_j, tiles_k;
+    unsigned long long* resid; // nullable: 2 * nfused slots
+    unsigned long long timeout_ns;
+    int* err;
+};
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+// |s| outside the range where Markstein's quotient is IEEE's: nonzero below
+// 2^-1019, or 2^1000 and above (incl. inf / NaN) — integer ops on the bits
+__device__ __forceinline__ bool div6_out_of_range(double s) {
+    const uint32_t h = (uint32_t)__double2hiint(s) & 0x7fffffffu;
+    const uint32_t l = (uint32_t)__double2loint(s);
+    return (h - 0x00400000u) >= (0x7E700000u - 0x00400000u) && (h | l) != 0u;
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+
+// planes -1 .. ex+2 of tile (c, j0, k0) into the ring, one tensor copy each
+__device__ __forceinline__ void vw2_produce(const VolW2Args& a, uint32_t ring, uint64_t* full,
+                                            uint64_t* empty, int& s, uint32_t& ph, int64_t c,
+                                            int64_t j0, int64_t k0, int parity) {
+    const int xm = a.xnb[2 * c], xp = a.xnb[2 * c + 1];
+    const CUtensorMap* own = a.maps + 2 * c + parity;
+    const CUtensorMap* mm = xm >= 0 ? a.maps + 2 * xm + parity : own;
+    const CUtensorMap* pm = xp >= 0 ? a.maps + 2 * xp + parity : own;
+    const int c0 = (int)(a.origin + k0 - 2), c1 = (int)(j0 - 2);
+    const int ex = (int)a.ex;
+    const int nplanes = ex + 4;
+    for (int q = 0; q < nplanes; ++q) {
+        const int i = q - 1;  // plane; neighbour planes in place, domain ghosts from own buffer
+        const CUtensorMap* m = own;
+        int ii = i;
+        if (i < 1 && xm >= 0) {
+            m = mm;
+            ii = i + ex;
+        } else if (i > ex && xp >= 0) {
+            m = pm;
+            ii = i - ex;
+        }
+        mbar_wait_sleep(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], VW_STAGE_BYTES);
+        tma_load_3d(ring + (uint32_t)s * VW_STAGE_BYTES, m, c0, c1, ii, smem_u32(&full[s]));
+        if (++s == VW_STAGES) {
+            s = 0;
+            ph ^= 1;
+        }
+    }
+}
+
+// Per-thread state of the volume two-step consumer (one tile).
+struct VW2Ctx {
+    uint32_t ring;        // shared address of this thread's column in stage 0, row 0
+    uint32_t full, empty;
+    int s;
+    uint32_t ph;
+    bool ready;
+    int lane;
+    bool tmask;           // some row or column of this warp's tile lies outside the domain
+    bool xlo, xhi;        // the x faces are domain faces
+    unsigned vrow;        // bit r: ring row r (0..7) inside the domain rows
+    bool colok;           // this lane's column is inside the domain
+    bool own;             // lane 1..30 with an inside column: stores + residuals
+    int64_t ex, sx, sy;
+    double* wr;           // plane 1, row j0, this column, buffer parity^1
+    double r1, r2;
+};
+
+template <int NP>
+__device__ __forceinline__ void vw2_take(VW2Ctx& x, double (&v)[NP], int& st) {
+    const uint32_t fb = x.full + 8u * (uint32_t)x.s;
+    if (!x.ready && !mbar_try_u32(fb, x.ph)) mbar_wait_u32_slow(fb, x.ph);
+    st = x.s;
+    const uint32_t base = x.ring + (uint32_t)x.s * VW_STAGE_BYTES;
+#pragma unroll
+    for (int r = 0; r < NP; ++r) v[r] = lds_f64(base + (uint32_t)(r * VW_RS * 8));
+    if (++x.s == VW_STAGES) {
+        x.s = 0;
+        x.ph ^= 1;
+    }
+    x.ready = mbar_try_u32(x.full + 8u * (uint32_t)x.s, x.ph);
+}
+
+__device__ __forceinline__ void vw2_release(VW2Ctx& x, int st) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
+    __syncwarp();
+    mbar_arrive_lane0_u32(x.empty + 8u * (uint32_t)st, x.lane);
+}
+
+// one pipeline step q (ring plane q = u(t) plane i = q-1 arrives as dn):
+// u(t+1) at plane q-2 (ring rows 1..6) -> u1n; u(t+2) at plane q-3 from
+// u(t+1) planes q-4 (u1a), q-3 (u1b), q-2 (u1n), stored.
+template <bool GUARD, bool RESID>
+__device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
+                                         const double (&mid)[VW_RR], double (&dn)[VW_RR],
+                                         int& smid, const double (&u1a)[VW_R + 2],
+                                         const double (&u1b)[VW_R + 2], double (&u1n)[VW_R + 2],
+                                         int q) {
+    int sdn;
+    vw2_take<VW_RR>(x, dn, sdn);
+    const int64_t i = q - 2;
+    // ---- u(t+1) at plane i, ring rows 1 .. VW_R+2 ----
+    {
+        const uint32_t mb = x.ring + (uint32_t)smid * VW_STAGE_BYTES;
+        bool bad = false;
+#pragma unroll
+        for (int m = 0; m < VW_R + 2; ++m) {
+            const uint32_t ra = mb + (uint32_t)((m + 1) * VW_RS * 8);
+            const double s = sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], lds_f64(ra - 8u),
+                                  lds_f64(ra + 8u));
+            u1n[m] = div6_fast(s);
+            if (GUARD) bad |= div6_out_of_range(s);
+        }
+        if (GUARD && bad) {  // rare: redo the group with IEEE division (unrolled:
+                             // a dynamic index would put the arrays in local memory)
+#pragma unroll
+            for (int m = 0; m < VW_R + 2; ++m) {
+                const uint32_t ra = mb + (uint32_t)((m + 1) * VW_RS * 8);
+                u1n[m] = __ddiv_rn(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2],
+                                        lds_f64(ra - 8u), lds_f64(ra + 8u)),
+                                   6.0);
+            }
+        }
+        vw2_release(x, smid);  // the stage of plane q-2 has served as mid: done
+        smid = sdn;
+        const bool xghost = (i < 1 && x.xlo) || (i > x.ex && x.xhi);
+        if (x.tmask || xghost) {  // edge tiles only (warp-uniform)
+            double d = 0.0;
+#pragma unroll
+            for (int m = 0; m < VW_R + 2; ++m) {
+                const bool in = !xghost && x.colok && ((x.vrow >> (m + 1)) & 1u);
+                if (!in) u1n[m] = HRT_BOUNDARY;
+                if (RESID && in && m >= 1 && m <= VW_R)
+                    d = dmax(d, abs_bits(__dsub_rn(u1n[m], mid[m + 1])));
+            }
+            if (RESID && x.own && i >= 1 && i <= x.ex) x.r1 = dmax(x.r1, d);
+        } else if (RESID) {
+            // every value here is an interior cell's u(t+1): the rim rows /
+            // lanes belong to neighbour tiles, and max is idempotent
+            double d = abs_bits(__dsub_rn(u1n[0], mid[1]));
+#pragma unroll
+            for (int m = 1; m < VW_R + 2; ++m) d = dmax(d, abs_bits(__dsub_rn(u1n[m], mid[m + 1])));
+            x.r1 = dmax(x.r1, d);
+        }
+    }
+    // ---- u(t+2) at plane q-3 (1 .. ex) -> HBM ----
+    if (q >= 4) {
+        double o[VW_R];
+        bool bad = false;
+#pragma unroll
+        for (int m = 1; m <= VW_R; ++m) {
+            const double s =
+                sum6(u1a[m], u1n[m], u1b[m - 1], u1b[m + 1], shfl_up1(u1b[m]), shfl_dn1(u1b[m]));
+            o[m - 1] = div6_fast(s);
+            if (GUARD) bad |= div6_out_of_range(s);
+        }
+        if (GUARD && __any_sync(0xffffffffu, bad)) {  // shuffles: the whole warp redoes it
+#pragma unroll
+            for (int m = 1; m <= VW_R; ++m)
+                o[m - 1] = __ddiv_rn(sum6(u1a[m], u1n[m], u1b[m - 1], u1b[m + 1],
+                                          shfl_up1(u1b[m]), shfl_dn1(u1b[m])),
+                                     6.0);
+        }
+        if (x.tmask) {
+            if (x.own) {
+                double d = 0.0;
+#pragma unroll
+                for (int m = 0; m < VW_R; ++m)
+                    if ((x.vrow >> (m + 2)) & 1u) {
+                        x.wr[m * x.sy] = o[m];
+                        if (RESID) d = dmax(d, abs_bits(__dsub_rn(o[m], u1b[m + 1])));
+                    }
+                if (RESID) x.r2 = dmax(x.r2, d);
+            }
+        } else {
+            if (x.own) {
+#pragma unroll
+                for (int m = 0; m < VW_R; ++m) x.wr[m * x.sy] = o[m];
+            }
+            if (RESID) {
+                double d = abs_bits(__dsub_rn(o[0], u1b[1]));
+#pragma unroll
+                for (int m = 1; m < VW_R; ++m) d = dmax(d, abs_bits(__dsub_rn(o[m], u1b[m + 1])));
+                if (x.own) x.r2 = dmax(x.r2, d);
+            }
+        }
+        x.wr += x.sx;
+    }
+}
+
+template <bool GUARD, bool RESID>
+__device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u32,
+                                            uint32_t full_u32, uint32_t empty_u32, int& s,
+                                            uint32_t& ph, int64_t c, int64_t j0, int64_t k0,
+                                            int parity, double& r1, double& r2) {
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    VW2Ctx x;
+    x.full = full_u32;
+    x.empty = empty_u32;
+    x.s = s;
+    x.ph = ph;
+    x.ready = false;
+    x.lane = tid & 31;
+    const int pc = 1 + VW_ZO * warp + x.lane;  // ring column of k
+    const int64_t k = k0 - 2 + pc;
+    x.ring = ring_u32 + 8u * (uint32_t)pc;
+    x.ex = a.ex;
+    x.sx = a.sx;
+    x.sy = a.sy;
+    x.xlo = a.xnb[2 * c] < 0;
+    x.xhi = a.xnb[2 * c + 1] < 0;
+    unsigned vrow = 0;
+#pragma unroll
+    for (int r = 0; r < VW_RR; ++r) {
+        const int64_t j = j0 - 2 + r;
+        if (j >= 1 && j <= a.ey) vrow |= 1u << r;
+    }
+    x.vrow = vrow;
+    x.colok = k >= 1 && k <= a.ez;
+    x.own = x.lane >= 1 && x.lane <= VW_ZO && x.colok;
+    x.tmask = __any_sync(0xffffffffu, !x.colok) || vrow != (1u << VW_RR) - 1u;
+    x.wr = a.chunks[c].b[parity ^ 1] + a.origin + a.sx + j0 * a.sy + k;
+    x.r1 = r1;
+    x.r2 = r2;
+    const int nplanes = (int)(a.ex + 4);
+
+    double t0[VW_RR], t1[VW_RR], t2[VW_RR];           // u(t) planes, rotating
+    double y0[VW_R + 2], y1[VW_R + 2], y2[VW_R + 2];  // u(t+1) planes, rotating
+    int st0, smid;
+    vw2_take<VW_RR>(x, t0, st0);  // plane -1: only ever "up"
+    vw2_release(x, st0);
+    vw2_take<VW_RR>(x, t1, smid);  // plane 0
+    int q = 2;
+    for (; q + 2 < nplanes; q += 3) {
+        vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q);
+        vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, q + 1);
+        vw2_step<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2, q + 2);
+    }
+    if (q < nplanes) vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q);
+    if (q + 1 < nplanes) vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, q + 1);
+    vw2_release(x, smid);  // the last plane only served as dn
+    s = x.s;
+    ph = x.ph;
+    r1 = x.r1;
+    r2 = x.r2;
+}
+
+// Unguarded division is exact for this launch: the uploaded field was
+// finite, >= 0 and <= 2^997 (so sums stay <= 2^1000), and its smallest
+// positive value m0 (or the 1.0 boundary) shrinks by at most a factor
+// 6(1+2^-52) per step, so every nonzero sum of the run is >= 2^-1019 as
+// long as m0 >= need = 2^-1019 * 6.000001^(steps since the scan + this run)
+// (computed by the host).  Non-negative sums cannot cancel to something
+// smaller than their largest term.
+__device__ __forceinline__ bool vw2_fast(const VolW2Args& a) {
+    if (!a.range || a.range[1] != 0ull) return false;
+    const unsigned long long key = a.range[0];
+    const double m0 = key == 0ull ? 1.0 : fmin(1.0, __longlong_as_double((long long)~key));
+    return m0 >= a.need;
+}
+
+// Launched as a pair on one stream: the FAST instance runs when vw2_fast
+// holds, the guarded one otherwise; the other returns at once (the decision
+// is on the device: the scan it reads was written by an upload kernel).
+template <bool FAST, bool RESID>
+__global__ void __launch_bounds__(32 * (VW_CW + 1), 3)
+volume_wave2_kernel(VolW2Args wa) {
+    if (vw2_fast(wa) != FAST) return;
+    __shared__ alignas(128) double ring[VW_STAGES][VW_RR][VW_RS];
+    __shared__ alignas(8) uint64_t full[VW_STAGES], empty[VW_STAGES], tq_full[WAVE_TQ],
+        tq_empty[WAVE_TQ];
+    __shared__ long long tq[WAVE_TQ];
+    __shared__ double red[2][VW_CW];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int64_t T = wa.ntiles;
+    const int64_t tj = wa.tiles_j, tk = wa.tiles_k;
+    const int64_t per_chunk = tj * tk;
+    const long long total = (long long)T * wa.nfused;
+
+    if (tid == 0) {
+        for (int k = 0; k < VW_STAGES; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], VW_CW);
+        }
+        for (int k = 0; k < WAVE_TQ; ++k) {
+            mbar_init(&tq_full[k], 1);
+            mbar_init(&tq_empty[k], VW_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t ring_u32 = smem_u32(&ring[0][0][0]);
+    if (warp >= VW_CW) {
+        if (lane != 0) return;
+        bool dead = false;
+        int slot = 0;
+        uint32_t tph = 0;
+        for (;;) {
+            const long long t = (long long)atomicAdd(wa.ticket, 1ull);
+            mbar_wait(&tq_empty[slot], tph ^ 1);
+            tq[slot] = t < total ? t : -1;
+            mbar_arrive(&tq_full[slot]);
+            if (++slot == WAVE_TQ) {
+                slot = 0;
+                tph ^= 1;
+            }
+            if (t >= total) break;
+            const int k = (int)(t / T);
+            const int64_t tile = t - (long long)k * T;
+            const int64_t c = tile / per_chunk;
+            const int64_t rem = tile - c * per_chunk;
+            const int64_t yb = rem / tk;
+            const int64_t zb = rem - yb * tk;
+            if (!dead) {
+                // the 3 x 3 x 3 tile neighbourhood must be done with step 2k
+                const unsigned need = 2u * (unsigned)k;
+                const unsigned int* q[27];
+                bool sys[27];
+                const int cx[3] = {wa.xnb[2 * c], (int)c, wa.xnb[2 * c + 1]};
+#pragma unroll
+                for (int d = 0; d < 27; ++d) {
+                    const int cc = cx[d / 9];
+                    const int64_t y2 = yb + (d / 3) % 3 - 1, z2 = zb + d % 3 - 1;
+                    const bool in = cc >= 0 && y2 >= 0 && y2 < tj && z2 >= 0 && z2 < tk;
+                    q[d] = in ? wa.done + (int64_t)cc * per_chunk + y2 * tk + z2 : nullptr;
+                    sys[d] = false;
+                }
+                dead = !wait_counters<27>(q, sys, need, wa.timeout_ns, wa.err);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            vw2_produce(wa, ring_u32, full, empty, s, ph, c, 1 + yb * VW_R, 1 + zb * VW_TZ,
+                        (wa.parity0 + k) & 1);
+        }
+        return;
+    }
+    const uint32_t full_u32 = smem_u32(&full[0]), empty_u32 = smem_u32(&empty[0]);
+    int slot = 0;
+    uint32_t tph = 0;
+    for (;;) {
+        mbar_wait(&tq_full[slot], tph);
+        const long long t = tq[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tq_empty[slot]);
+        if (++slot == WAVE_TQ) {
+            slot = 0;
+            tph ^= 1;
+        }
+        if (t < 0) break;
+        const int k = (int)(t / T);
+        const int64_t tile = t - (long long)k * T;
+        const int64_t c = tile / per_chunk;
+        const int64_t rem = tile - c * per_chunk;
+        const int64_t yb = rem / tk;
+        const int64_t zb = rem - yb * tk;
+        double r1 = 0.0, r2 = 0.0;
+        vw2_consume<!FAST, RESID>(wa, ring_u32, full_u32, empty_u32, s, ph, c, 1 + yb * VW_R,
+                                  1 + zb * VW_TZ, (wa.parity0 + k) & 1, r1, r2);
+        if (RESID && wa.resid) {
+            r1 = warp_max(r1);
+            r2 = warp_max(r2);
+            if (lane == 0) {
+                red[0][warp] = r1;
+                red[1][warp] = r2;
+            }
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * VW_CW));
+        if (tid == 0) {
+            if (RESID && wa.resid) {
+                double m1 = red[0][0], m2 = red[1][0];
+#pragma unroll
+                for (int w = 1; w < VW_CW; ++w) {
+                    m1 = fmax(m1, red[0][w]);
+                    m2 = fmax(m2, red[1][w]);
+                }
+                resid_max(wa.resid + 2 * k, m1);
+                resid_max(wa.resid + 2 * k + 1, m2);
+            }
+            __threadfence();
+            st_release_gpu_u32(wa.done + tile, 2u * (unsigned)k + 2u);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // plan: the per-GPU step engine
 
 struct Plan {
@@ -2312,6 +2803,18 @@ struct Plan {
     std::vector<uint64_t> r2buf, r2cnt;
     std::vector<int64_t> r2idx;
     double* d_ones = nullptr;      // BOUNDARY row (rows outside the domain)
+    // two steps per pass for x-band volumes (volume_wave2_kernel)
+    std::vector<hrt_vpush_t> h_vpush;  // host copy of the push table (face kinds)
+    unsigned int* d_v2done = nullptr;  // per-tile step counters, reset every launch
+    int* d_v2nb = nullptr;             // [nchunks][2] -x / +x neighbour chunk
+    CUtensorMap* d_v2maps = nullptr;   // [nchunks][2] 3D tensor maps of the buffers
+    // field scan of the last upload (volume plans; see vw2_fast) and the
+    // steps run since (saturating; "unknown" until the first scan)
+    unsigned long long* d_range = nullptr;
+    int64_t since_scan = int64_t(1) << 40;
+    void count_steps(int64_t n) { since_scan = std::min<int64_t>(since_scan + n, int64_t(1) << 40); }
+    int64_t v2_tiles = 0;
+    int pgrid3 = 0;                    // resident CTA slots of volume_wave2_kernel
     int pgrid2 = 0;                // resident CTA slots of slab_wave2_kernel
     int64_t pkey2 = -1;
     bool fuse2_on() const {
@@ -2777,8 +3280,9 @@ static bool fuse2_use(const Plan* p) {
 }
 
 // steps per fused pass this plan runs (0: one step per pass)
+static bool vfuse2_use(const Plan* p);
 static int pass_steps_of(const Plan* p) {
-    return fuse2_use(p) ? 2 : 0;
+    return (p->L.ndim == 3 ? vfuse2_use(p) : fuse2_use(p)) ? 2 : 0;
 }
 
 template <bool G, bool R, int CW, bool F>
@@ -2917,17 +3421,190 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     return HRT_OK;
 }
 
+// ---- two steps per pass for volumes (volume_wave2_kernel) ----
+// x-band volumes on one GPU: every y and z face a domain face, x faces to
+// chunks of this plan or the domain (never to another GPU or process)
+static bool vfuse2_on(const Plan* p) {
+    const hrt_chunk_layout_t& L = p->L;
+    if (!p->fuse2 || L.ndim != 3 || !p->persist_on() || p->wave_ipc || !p->remote.empty() || p->ipc)
+        return false;
+    if (L.ext[0] < 2 || L.origin % 2 != 1 || L.stride[0] % 2 != 0 || L.stride[1] % 2 != 0)
+        return false;
+    if ((int64_t)p->nbr.size() != 6 * (int64_t)p->nchunks ||
+        (int64_t)p->h_vpush.size() != (int64_t)p->nchunks)
+        return false;
+    for (int c = 0; c < p->nchunks; ++c)
+        for (int f = 0; f < 6; ++f) {
+            const int n = p->nbr[6 * (size_t)c + f];
+            const hrt_vpush_t& v = p->h_vpush[c];
+            if (f >= 2 && n >= 0) return false;                       // y / z: domain faces
+            if (n < 0 && (v.ptr[f][0] || v.ptr[f][1])) return false;  // a face to another GPU
+        }
+    return true;
+}
+
+static int64_t vw2_tiles(const Plan* p, int64_t* tj = nullptr, int64_t* tk = nullptr) {
+    const int64_t a = (p->L.ext[1] + VW_R - 1) / VW_R, b = (p->L.ext[2] + VW_TZ - 1) / VW_TZ;
+    if (tj) *tj = a;
+    if (tk) *tk = b;
+    return (int64_t)p->nchunks * a * b;
+}
+
+template <bool F, bool R>
+static int vw2_blocks_per_sm() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, volume_wave2_kernel<F, R>, 32 * (VW_CW + 1), 0);
+    return n;
+}
+
+// 3D tensor maps of every chunk buffer: dims (sy, ey+2, ex+2) from the
+// buffer base, box 124 x 8 x 1 (one plane of a tile), out-of-range
+// coordinates zero-filled
+static int build_vw2_maps(Plan* p) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        HRT_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000,
+                                                  cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return HRT_E_UNSUPPORTED;
+        }
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const hrt_chunk_layout_t& L = p->L;
+    std::vector<CUtensorMap> maps(2 * (size_t)p->nchunks);
+    const cuuint64_t dims[3] = {(cuuint64_t)L.stride[1], (cuuint64_t)(L.ext[1] + 2),
+                                (cuuint64_t)(L.ext[0] + 2)};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.stride[1] * 8, (cuuint64_t)L.stride[0] * 8};
+    const cuuint32_t box[3] = {VW_RS, VW_RR, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    for (int c = 0; c < p->nchunks; ++c)
+        for (int par = 0; par < 2; ++par) {
+            CUresult r = encode(&maps[2 * (size_t)c + par], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                                p->h_chunks[c].b[par], dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+                return HRT_E_CUDA;
+            }
+        }
+    cudaFree(p->d_v2maps);
+    p->d_v2maps = nullptr;
+    HRT_CUDA(cudaMalloc(&p->d_v2maps, sizeof(CUtensorMap) * maps.size()));
+    HRT_CUDA(cudaMemcpy(p->d_v2maps, maps.data(), sizeof(CUtensorMap) * maps.size(),
+                        cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
+// volume tiles are 2 x 4 x 120 (a pass is one tile per CTA slot at least)
+static bool vfuse2_use(const Plan* p) {
+    if (!vfuse2_on(p)) return false;
+    if (p->fuse2 == 2) return true;
+    const int64_t per_chunk = vw2_tiles(p) / std::max(1, p->nchunks);
+    return per_chunk * p->tn() >= (int64_t)sm_count(p->gpu) * 3;
+}
+
+static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
+                         unsigned long long* resid_base) {
+    if (nf <= 0) return HRT_OK;
+    const hrt_chunk_layout_t& L = p->L;
+    int64_t tj = 0, tk = 0;
+    const int64_t T = vw2_tiles(p, &tj, &tk);
+    if (T == 0) return HRT_OK;
+    if (!p->d_v2done || p->v2_tiles != T) {
+        HRT_CUDA(cudaStreamSynchronize(s));
+        cudaFree(p->d_v2done);
+        cudaFree(p->d_v2nb);
+        p->d_v2done = nullptr;
+        p->d_v2nb = nullptr;
+        HRT_CUDA(cudaMalloc(&p->d_v2done, sizeof(unsigned int) * T));
+        std::vector<int> nb(2 * (size_t)p->nchunks);
+        for (int c = 0; c < p->nchunks; ++c) {
+            nb[2 * (size_t)c] = p->nbr[6 * (size_t)c];
+            nb[2 * (size_t)c + 1] = p->nbr[6 * (size_t)c + 1];
+        }
+        HRT_CUDA(cudaMalloc(&p->d_v2nb, sizeof(int) * nb.size()));
+        HRT_CUDA(cudaMemcpy(p->d_v2nb, nb.data(), sizeof(int) * nb.size(), cudaMemcpyHostToDevice));
+        int rc = build_vw2_maps(p);
+        if (rc) return rc;
+        p->v2_tiles = T;
+    }
+    if (!p->d_range) {  // never scanned: "unknown" (guarded division)
+        HRT_CUDA(cudaMalloc(&p->d_range, 2 * sizeof(unsigned long long)));
+        const unsigned long long h[2] = {0ull, 1ull};
+        HRT_CUDA(cudaMemcpy(p->d_range, h, sizeof(h), cudaMemcpyHostToDevice));
+        p->since_scan = int64_t(1) << 40;
+    }
+    if (!p->d_pticket) HRT_CUDA(cudaMalloc(&p->d_pticket, sizeof(unsigned long long)));
+    if (!p->d_err) {
+        HRT_CUDA(cudaMalloc(&p->d_err, sizeof(int)));
+        HRT_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+    }
+    if (p->pgrid3 == 0) {
+        const int n = std::min(std::min(vw2_blocks_per_sm<true, true>(), vw2_blocks_per_sm<true, false>()),
+                               std::min(vw2_blocks_per_sm<false, true>(), vw2_blocks_per_sm<false, false>()));
+        HRT_CUDA(cudaGetLastError());
+        if (n <= 0) {
+            set_error("volume two-step kernel: no resident CTA slots");
+            return HRT_E_CUDA;
+        }
+        p->pgrid3 = n * sm_count(p->gpu);
+    }
+    HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
+    HRT_CUDA(cudaMemsetAsync(p->d_v2done, 0, sizeof(unsigned int) * T, s));
+    VolW2Args wa{};
+    wa.chunks = p->d_chunks;
+    wa.xnb = p->d_v2nb;
+    wa.done = p->d_v2done;
+    wa.ticket = p->d_pticket;
+    wa.nfused = (int)nf;
+    wa.parity0 = (int)(first & 1);
+    wa.ntiles = T;
+    wa.ex = L.ext[0];
+    wa.ey = L.ext[1];
+    wa.ez = L.ext[2];
+    wa.sx = L.stride[0];
+    wa.sy = L.stride[1];
+    wa.origin = L.origin;
+    wa.tiles_j = tj;
+    wa.tiles_k = tk;
+    wa.resid = resid_base ? resid_base + first : nullptr;
+    wa.maps = p->d_v2maps;
+    wa.range = p->d_range;
+    // exact unguarded division needs min positive >= 2^-1019 * 6.000001^n
+    // for n = steps since the scan, this run included (see vw2_fast)
+    wa.need = p->since_scan > 400 ? HUGE_VAL
+                                  : std::ldexp(1.0, -1019) * std::pow(6.000001, (double)p->since_scan);
+    wa.timeout_ns = p->persist_timeout_ns;
+    wa.err = p->d_err;
+    // the unguarded instance, then the guarded one: exactly one of them
+    // works (vw2_fast), the other returns at entry
+    void* fns[2] = {resid_base ? (void*)volume_wave2_kernel<true, true> : (void*)volume_wave2_kernel<true, false>,
+                    resid_base ? (void*)volume_wave2_kernel<false, true> : (void*)volume_wave2_kernel<false, false>};
+    const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid3, T);
+    void* args[] = {&wa};
+    for (void* fn : fns)
+        HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (VW_CW + 1)), args, 0, s));
+    p->ghosts_ready = false;  // passes read neighbours in place; ghost planes went stale
+    return HRT_OK;
+}
+
 // steps [first, first+n): on a single-GPU slab plan, passes of two steps
 // (after n mod 4 single steps, so the result lands in the buffer of parity
 // (first+n) mod 2 like single steps); otherwise one wavefront launch
 static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                           unsigned long long* resid_base) {
     if (n <= 0) return HRT_OK;
-    if (fuse2_use(p) && n >= 4) {
+    const bool vol = p->L.ndim == 3;
+    if ((vol ? vfuse2_use(p) : fuse2_use(p)) && n >= 4) {
         const int64_t nf = (n / 4) * 2, nr = n - 2 * nf;
         int rc = nr ? launch_persist1(p, s, first, nr, resid_base) : HRT_OK;
         if (rc) return rc;
-        return launch_fused(p, s, first + nr, nf, resid_base);
+        return vol ? launch_vfused(p, s, first + nr, nf, resid_base)
+                   : launch_fused(p, s, first + nr, nf, resid_base);
     }
     return launch_persist1(p, s, first, n, resid_base);
 }
@@ -3134,9 +3811,17 @@ int hrt_jacobi_plan_field_copy(void* plan, void* stream, double* field, int64_t 
     const hrt_chunk_layout_t& L = p->L;
     const int64_t rows = L.ndim == 2 ? L.ext[0] : L.ext[0] * L.ext[1];
     const int64_t grid = rows * p->nchunks;
-    field_copy_kernel<<<(unsigned)grid, 256, 0, as_stream(stream)->s>>>(
+    cudaStream_t cs = as_stream(stream)->s;
+    unsigned long long* range = nullptr;
+    if (to_chunks && L.ndim == 3) {
+        if (!p->d_range) HRT_CUDA(cudaMalloc(&p->d_range, 2 * sizeof(unsigned long long)));
+        HRT_CUDA(cudaMemsetAsync(p->d_range, 0, 2 * sizeof(unsigned long long), cs));
+        range = p->d_range;
+        p->since_scan = 0;
+    }
+    field_copy_kernel<<<(unsigned)grid, 256, 0, cs>>>(
         p->d_chunks, p->d_offs, parity & 1, L.ndim, L.ext[0], L.ext[1], L.ext[2], L.stride[0],
-        L.stride[1], L.origin, field, FY, FZ, to_chunks);
+        L.stride[1], L.origin, field, FY, FZ, to_chunks, range);
     HRT_CUDA(cudaGetLastError());
     if (to_chunks) p->ghosts_ready = false;  // new interiors: ghost planes are stale
     return HRT_OK;
@@ -3196,7 +3881,10 @@ int hrt_jacobi_plan_set_vpush(void* plan, const hrt_vpush_t* table) {
         cudaGraphExecDestroy(p->graph);
         p->graph = nullptr;
     }
+    p->h_vpush.clear();
+    p->pgrid3 = 0;
     if (!table || p->nchunks == 0) return HRT_OK;
+    p->h_vpush.assign(table, table + p->nchunks);
     HRT_CUDA(cudaMalloc(&p->d_vpush, sizeof(VolPush) * p->nchunks));
     HRT_CUDA(cudaMemcpy(p->d_vpush, table, sizeof(VolPush) * p->nchunks, cudaMemcpyHostToDevice));
     return HRT_OK;
@@ -3528,6 +4216,7 @@ int hrt_jacobi_plan_step(void* plan, void* stream, int64_t step, uint64_t* resid
     Plan* p = reinterpret_cast<Plan*>(plan);
     int rc = use_device(p->gpu);
     if (rc) return rc;
+    p->count_steps(1);
     return do_step(p, as_stream(stream)->s, step, reinterpret_cast<unsigned long long*>(resid));
 }
 
@@ -3559,6 +4248,7 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
     if (rc) return rc;
     cudaStream_t s = as_stream(stream)->s;
     unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
+    p->count_steps(n);
     if (p->persist_on()) return launch_persist(p, s, first, n, r);
     // IPC step tags are per launch; in push mode graph replays measured 40 %
     // slower than direct launches on B200 (cause not yet identified; the
@@ -3613,6 +4303,7 @@ int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n
     if (rc) return rc;
     cudaStream_t s = as_stream(stream)->s;
     unsigned long long* r = reinterpret_cast<unsigned long long*>(resid);
+    p->count_steps(n);
     // events are cached on the plan: creating thousands per call would leave
     // the GPU idle while the host allocates them
     std::vector<cudaEvent_t>& ev = p->events;
@@ -3715,6 +4406,10 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_peer_done);
     cudaFree(p->d_n9);
     cudaFree(p->d_ones);
+    cudaFree(p->d_v2done);
+    cudaFree(p->d_v2nb);
+    cudaFree(p->d_v2maps);
+    cudaFree(p->d_range);
     if (p->side) cudaStreamDestroy(p->side);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);

@@ -453,9 +453,15 @@ class JacobiSolver:
         if self.push:
             self._setup_push()
         # volumes: fused 6-face push + wavefront (opt-in: measured slower than
-        # tile launches + halo pass on B200 at 1024x1024x768)
+        # tile launches + halo pass on B200 at 1024x1024x768),
+        # except for x-band volumes on one GPU, where runs of >= 4 steps go
+        # as two-step passes (volume_wave2_kernel, built on the wavefront's
+        # neighbour table)
+        xband = (L.ndim == 3 and len(self.used_gpus) == 1 and not remote_ops and
+                 grid.grid[1] == 1 and grid.grid[2] == 1 and
+                 os.environ.get("HRT_FUSE2", "1") != "0")
         if vpush is None:
-            vpush = os.environ.get("HRT_VPUSH", "0") == "1"
+            vpush = os.environ.get("HRT_VPUSH", "0") == "1" or xband
         self.vpush = bool(vpush) and push is not False and \
             L.ndim == 3 and variant not in (0, CHECK_VARIANT) and not remote_ops
         if self.vpush:

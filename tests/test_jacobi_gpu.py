@@ -372,3 +372,99 @@ def test_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, rows, monkeypatc
     ref = oracle.jacobi_reference(dom, steps, initial=init, residuals=resid)
     assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
     assert np.array_equal(res, np.array(resid)), (res, resid)
+
+
+@pytest.mark.parametrize("dom,grid", [
+    ((16, 9, 37), (2, 1, 1)),        # partial y (4-row) and z (120-column) tiles
+    ((4, 5, 121), (2, 1, 1)),        # 2-plane chunks (the minimum): rims span the neighbour
+    ((30, 17, 240), (3, 1, 1)),      # two full z tiles
+    ((12, 8, 250), (1, 1, 1)),       # one chunk: both x faces are domain faces
+    ((21, 4, 119), (3, 1, 1)),       # 7-plane chunks, odd z extent
+    ((40, 33, 130), (4, 1, 1)),
+])
+@pytest.mark.parametrize("steps", [3, 4, 6, 9, 13])
+def test_volume_two_step_passes_bitwise(hrt, oracle, dom, grid, steps, monkeypatch):
+    """volume_wave2_kernel (x-band volumes, two Jacobi steps per pass, rims
+    from the x-neighbour chunks in place, u(t+1) in registers and lane
+    shuffles) against the numpy oracle on random signed data: field and
+    every step's residual bitwise, n mod 4 single steps first."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    monkeypatch.setenv("HRT_FUSE2", "2")  # small domains: force the passes
+    rng = np.random.default_rng(steps * 13 + dom[2])
+    init = rng.random(dom) * 4.0 - 1.0
+    s = JacobiSolver(ChunkGrid(dom, grid=grid))
+    assert s.persistent and s.steps_per_pass == 2
+    s.upload(init)
+    s.run(steps, residual=True)
+    got = s.download()
+    res = s.residual_history()
+    s.close()
+    resid = []
+    ref = oracle.jacobi_reference(dom, steps, initial=init, residuals=resid)
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
+    assert np.array_equal(res, np.array(resid)), (res, resid)
+
+
+@pytest.mark.parametrize("parts", [[4, 4], [5, 8], [4, 1, 4], [13]])
+def test_volume_two_step_split_runs(hrt, oracle, parts, monkeypatch):
+    """Runs alternating two-step passes and single steps over one upload
+    (the reference's initial state): the ghost planes the passes leave stale
+    are re-primed before the next single step."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    monkeypatch.setenv("HRT_FUSE2", "2")
+    dom, grid = (24, 20, 150), (3, 1, 1)
+    s = JacobiSolver(ChunkGrid(dom, grid=grid))
+    s.upload()
+    for n in parts:
+        s.run(n, residual=False)
+    got = s.download()
+    s.close()
+    ref = oracle.jacobi_c(dom, sum(parts))
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
+
+
+@pytest.mark.parametrize("steps", [4, 13])
+def test_volume_two_step_division_paths(hrt, oracle, steps, monkeypatch):
+    """The volume pass picks its division on the device from the upload's
+    field scan: a non-negative field whose smallest positive value is
+    1e-300 allows the unguarded instance for 4 steps (1e-300 * 6^-4 >>
+    2^-1019) but not for 13; both runs must match the oracle bitwise."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    monkeypatch.setenv("HRT_FUSE2", "2")
+    dom, grid = (24, 9, 130), (3, 1, 1)
+    rng = np.random.default_rng(5)
+    init = rng.random(dom)
+    init[rng.random(dom) < 0.05] = 1e-300
+    init[rng.random(dom) < 0.3] = 0.0
+    s = JacobiSolver(ChunkGrid(dom, grid=grid))
+    s.upload(init)
+    s.run(steps, residual=True)
+    got, res = s.download(), s.residual_history()
+    s.close()
+    resid = []
+    ref = oracle.jacobi_reference(dom, steps, initial=init, residuals=resid)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    assert np.array_equal(res, np.array(resid))
+
+
+def test_volume_negative_zero_kept(hrt, oracle, monkeypatch):
+    """-0.0 / 6 is -0.0 (numpy, the reference): a field of -0.0 keeps its
+    sign bits wherever all six neighbours are -0.0 — bitwise, through the
+    two-step passes, the one-step tiles and the persistent wavefront."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    dom, grid = (24, 12, 40), (3, 1, 1)
+    init = np.full(dom, -0.0)
+    ref = oracle.jacobi_reference(dom, 5, initial=init)
+    assert np.signbit(ref).any()
+    for fuse2, persistent in (("2", None), ("0", False), ("0", True)):
+        monkeypatch.setenv("HRT_FUSE2", fuse2)
+        s = JacobiSolver(ChunkGrid(dom, grid=grid), persistent=persistent, vpush=persistent)
+        s.upload(init)
+        s.run(5, residual=False)
+        got = s.download()
+        s.close()
+        assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (fuse2, persistent)
