@@ -2282,14 +2282,25 @@ __global__ void div6_sweep_kernel(uint64_t seed, int64_t n, int mode,
 // (no branch per cell: branches split the dependency chains the scheduler
 // interleaves).
 
+#ifndef HRT_VW_MINB
+#define HRT_VW_MINB 3  // resident CTAs per SM the register budget targets
+#endif
 constexpr int VW_CW = 4;              // consumer warps, side by side in z
-constexpr int VW_R = 4;               // y rows per tile (per thread)
+#ifndef HRT_VW_R
+#define HRT_VW_R 4
+#endif
+constexpr int VW_R = HRT_VW_R;        // y rows per tile (per thread)
 constexpr int VW_ZO = 30;             // output columns per warp (lanes 1..30)
 constexpr int VW_TZ = VW_CW * VW_ZO;  // output columns per tile
 constexpr int VW_RS = VW_TZ + 4;      // ring row: columns k0-2 .. k0+VW_TZ+1
 constexpr int VW_RR = VW_R + 4;       // ring rows per plane: j0-2 .. j0+VW_R+1
-constexpr int VW_STAGES = 5;          // 5 x 8 x 124 doubles = 39.7 KB
+#ifndef HRT_VW_STAGES
+#define HRT_VW_STAGES 5
+#endif
+constexpr int VW_STAGES = HRT_VW_STAGES;  // 5 x 8 x 124 doubles = 39.7 KB
 constexpr uint32_t VW_STAGE_BYTES = (uint32_t)(VW_RR * VW_RS * 8);
+constexpr size_t VW_SMEM = (size_t)VW_STAGES * VW_STAGE_BYTES;  // the ring (dynamic)
+static_assert(VW_STAGE_BYTES % 128 == 0, "TMA tensor destinations must stay 128-byte aligned");
 
 struct VolW2Args {
     const CUtensorMap* maps;   // [nchunks][2] tensor map of buffer 0 / 1
@@ -2394,6 +2405,12 @@ __device__ __forceinline__ void vw2_take(VW2Ctx& x, double (&v)[NP], int& st) {
         x.s = 0;
         x.ph ^= 1;
     }
+    x.ready = false;
+}
+
+// Poll the next stage once the step's shared loads are issued: try_wait
+// acquires, so shared loads after it wait for its ~90-cycle round trip.
+__device__ __forceinline__ void vw2_poll(VW2Ctx& x) {
     x.ready = mbar_try_u32(x.full + 8u * (uint32_t)x.s, x.ph);
 }
 
@@ -2502,6 +2519,82 @@ __device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
         }
         x.wr += x.sx;
     }
+    vw2_poll(x);
+}
+
+// The same step for planes 2 .. ex of a tile with nothing outside the domain
+// (no masks; q >= 4): one basic block apart from the barrier waits, so the
+// scheduler interleaves the ten independent sums.  The residual of u(t+1)
+// is taken on every lane — rim lanes hold neighbour tiles' interior values,
+// and max is idempotent — that of u(t+2) on the owning lanes only.
+template <bool GUARD, bool RESID>
+__device__ __forceinline__ void vw2_step_fast(VW2Ctx& x, const double (&up)[VW_RR],
+                                              const double (&mid)[VW_RR], double (&dn)[VW_RR],
+                                              int& smid, const double (&u1a)[VW_R + 2],
+                                              const double (&u1b)[VW_R + 2],
+                                              double (&u1n)[VW_R + 2]) {
+    int sdn;
+    vw2_take<VW_RR>(x, dn, sdn);
+    const uint32_t mb = x.ring + (uint32_t)smid * VW_STAGE_BYTES;
+    bool bad = false;
+#pragma unroll
+    for (int m = 0; m < VW_R + 2; ++m) {
+        const uint32_t ra = mb + (uint32_t)((m + 1) * VW_RS * 8);
+        const double s = sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], lds_f64(ra - 8u),
+                              lds_f64(ra + 8u));
+        u1n[m] = div6_fast(s);
+        if (GUARD) bad |= div6_out_of_range(s);
+    }
+    if (GUARD && bad) {
+#pragma unroll
+        for (int m = 0; m < VW_R + 2; ++m) {
+            const uint32_t ra = mb + (uint32_t)((m + 1) * VW_RS * 8);
+            u1n[m] = __ddiv_rn(sum6(up[m + 1], dn[m + 1], mid[m], mid[m + 2], lds_f64(ra - 8u),
+                                    lds_f64(ra + 8u)),
+                               6.0);
+        }
+    }
+    vw2_release(x, smid);
+    smid = sdn;
+    double o[VW_R];
+    bool bad2 = false;
+#pragma unroll
+    for (int m = 1; m <= VW_R; ++m) {
+        const double s =
+            sum6(u1a[m], u1n[m], u1b[m - 1], u1b[m + 1], shfl_up1(u1b[m]), shfl_dn1(u1b[m]));
+        o[m - 1] = div6_fast(s);
+        if (GUARD) bad2 |= div6_out_of_range(s);
+    }
+    if (GUARD && __any_sync(0xffffffffu, bad2)) {
+#pragma unroll
+        for (int m = 1; m <= VW_R; ++m)
+            o[m - 1] = __ddiv_rn(sum6(u1a[m], u1n[m], u1b[m - 1], u1b[m + 1], shfl_up1(u1b[m]),
+                                      shfl_dn1(u1b[m])),
+                                 6.0);
+    }
+    if (x.own) {
+#pragma unroll
+        for (int m = 0; m < VW_R; ++m) x.wr[m * x.sy] = o[m];
+    }
+    if (RESID) {
+        double e1[VW_R], e2[VW_R];
+#pragma unroll
+        for (int m = 0; m < VW_R; ++m) {
+            e1[m] = abs_bits(__dsub_rn(u1n[m + 1], mid[m + 2]));
+            e2[m] = abs_bits(__dsub_rn(o[m], u1b[m + 1]));
+        }
+#pragma unroll
+        for (int w = 1; w < VW_R; w *= 2)  // pairwise tree
+#pragma unroll
+            for (int m = 0; m + w < VW_R; m += 2 * w) {
+                e1[m] = dmax(e1[m], e1[m + w]);
+                e2[m] = dmax(e2[m], e2[m + w]);
+            }
+        x.r1 = dmax(x.r1, e1[0]);
+        if (x.own) x.r2 = dmax(x.r2, e2[0]);
+    }
+    x.wr += x.sx;
+    vw2_poll(x);
 }
 
 template <bool GUARD, bool RESID>
@@ -2547,14 +2640,23 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     vw2_take<VW_RR>(x, t0, st0);  // plane -1: only ever "up"
     vw2_release(x, st0);
     vw2_take<VW_RR>(x, t1, smid);  // plane 0
-    int q = 2;
+    // register roles rotate with period 3: step q uses set (q-2) % 3
+    vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, 2);  // u(t+1) at plane 0
+    vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, 3);
+    int q = 4;
+    if (!x.tmask)  // planes 2 .. ex: nothing outside the domain
+        for (; q + 2 <= (int)a.ex + 2; q += 3) {
+            vw2_step_fast<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2);
+            vw2_step_fast<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0);
+            vw2_step_fast<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1);
+        }
     for (; q + 2 < nplanes; q += 3) {
-        vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q);
-        vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, q + 1);
-        vw2_step<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2, q + 2);
+        vw2_step<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2, q);
+        vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q + 1);
+        vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, q + 2);
     }
-    if (q < nplanes) vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q);
-    if (q + 1 < nplanes) vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, q + 1);
+    if (q < nplanes) vw2_step<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2, q);
+    if (q + 1 < nplanes) vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q + 1);
     vw2_release(x, smid);  // the last plane only served as dn
     s = x.s;
     ph = x.ph;
@@ -2580,10 +2682,10 @@ __device__ __forceinline__ bool vw2_fast(const VolW2Args& a) {
 // holds, the guarded one otherwise; the other returns at once (the decision
 // is on the device: the scan it reads was written by an upload kernel).
 template <bool FAST, bool RESID>
-__global__ void __launch_bounds__(32 * (VW_CW + 1), 3)
+__global__ void __launch_bounds__(32 * (VW_CW + 1), HRT_VW_MINB)
 volume_wave2_kernel(VolW2Args wa) {
     if (vw2_fast(wa) != FAST) return;
-    __shared__ alignas(128) double ring[VW_STAGES][VW_RR][VW_RS];
+    extern __shared__ __align__(128) unsigned char vw2_dyn[];  // the ring: VW_SMEM bytes
     __shared__ alignas(8) uint64_t full[VW_STAGES], empty[VW_STAGES], tq_full[WAVE_TQ],
         tq_empty[WAVE_TQ];
     __shared__ long long tq[WAVE_TQ];
@@ -2612,7 +2714,7 @@ volume_wave2_kernel(VolW2Args wa) {
 
     int s = 0;
     uint32_t ph = 0;
-    const uint32_t ring_u32 = smem_u32(&ring[0][0][0]);
+    const uint32_t ring_u32 = smem_u32(vw2_dyn);
     if (warp >= VW_CW) {
         if (lane != 0) return;
         bool dead = false;
@@ -3453,7 +3555,10 @@ static int64_t vw2_tiles(const Plan* p, int64_t* tj = nullptr, int64_t* tk = nul
 template <bool F, bool R>
 static int vw2_blocks_per_sm() {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, volume_wave2_kernel<F, R>, 32 * (VW_CW + 1), 0);
+    cudaFuncSetAttribute(volume_wave2_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)VW_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, volume_wave2_kernel<F, R>, 32 * (VW_CW + 1),
+                                                  VW_SMEM);
     return n;
 }
 
@@ -3587,7 +3692,7 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid3, T);
     void* args[] = {&wa};
     for (void* fn : fns)
-        HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (VW_CW + 1)), args, 0, s));
+        HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (VW_CW + 1)), args, VW_SMEM, s));
     p->ghosts_ready = false;  // passes read neighbours in place; ghost planes went stale
     return HRT_OK;
 }
