@@ -1069,51 +1069,59 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[W 
                                            int64_t i1, int parity) {
     const int64_t j0 = 1 + cb * W;
     const int64_t last = min(j0 + W - 1, a.ey);
-    const Nbr9& n9 = a.n9[c];
+    const Nbr9* n9 = a.n9 + c;
     const bool wedge = cb == 0, eedge = last == a.ey;
     const int64_t lo = wedge ? 1 : j0 - 2;
     const int64_t hi = eedge ? a.ey : last + 2;
     const uint32_t mbytes = (uint32_t)((hi - lo + 1) * 8);  // even count: ey even
     const int mpos = (int)(lo - (j0 - 2));
     const int epos = (int)(last - j0 + 3);
-    const int nrows = (int)(i1 - i0 + 5);
-    for (int q = 0; q < nrows; ++q) {
-        const int64_t r = i0 - 2 + q;
-        const int di = r < 1 ? -1 : (r > a.ex ? 1 : 0);
+    // three row segments (north chunk rows, own rows, south chunk rows):
+    // the sources are fixed per segment, so the row loop only advances
+    // pointers (a table load per row stalled the producer thread)
+    int64_t r = i0 - 2;
+    const int64_t rend = i1 + 2;
+#pragma unroll 1
+    for (int di = -1; di <= 1; ++di) {
+        const int64_t cap = di < 0 ? 0 : (di == 0 ? a.ex : rend);
+        const int64_t seg_end = rend < cap ? rend : cap;
+        if (r > seg_end) continue;
+        const double* br = n9->b[(di + 1) * 3 + 1][parity];
+        const double* bw = (br && wedge) ? n9->b[(di + 1) * 3 + 0][parity] : nullptr;
+        const double* be = (br && eedge) ? n9->b[(di + 1) * 3 + 2][parity] : nullptr;
         const int64_t rr = r - di * a.ex;
-        const double* br = n9.b[(di + 1) * 3 + 1][parity];
-        mbar_wait_sleep(&empty[s], ph ^ 1);
-        uint32_t bytes = mbytes;
         const double* msrc = br ? br + a.origin + rr * a.sx + lo : a.ones;
-        const double* wsrc = nullptr;
-        const double* esrc = nullptr;
-        if (wedge) {
-            const double* bw = br ? n9.b[(di + 1) * 3 + 0][parity] : nullptr;
-            if (bw) {
-                wsrc = bw + a.origin + rr * a.sx + (a.ey - 1);
-                bytes += 16;
-            } else {
+        const double* wsrc = bw ? bw + a.origin + rr * a.sx + (a.ey - 1) : nullptr;
+        const double* esrc = be ? be + a.origin + rr * a.sx + 1 : nullptr;
+        const int64_t mstep = br ? a.sx : 0;
+        const uint32_t bytes = mbytes + (wsrc ? 16u : 0u) + (esrc ? 16u : 0u);
+        const bool wfill = wedge && !wsrc, efill = eedge && !esrc;
+#pragma unroll 1
+        for (; r <= seg_end; ++r) {
+            mbar_wait_sleep(&empty[s], ph ^ 1);
+            if (wfill) {
                 ring[s][0] = HRT_BOUNDARY;
                 ring[s][1] = HRT_BOUNDARY;
             }
-        }
-        if (eedge) {
-            const double* be = br ? n9.b[(di + 1) * 3 + 2][parity] : nullptr;
-            if (be) {
-                esrc = be + a.origin + rr * a.sx + 1;
-                bytes += 16;
-            } else {
+            if (efill) {
                 ring[s][epos] = HRT_BOUNDARY;
                 ring[s][epos + 1] = HRT_BOUNDARY;
             }
-        }
-        mbar_expect_tx(&full[s], bytes);
-        tma_row_load(&ring[s][mpos], msrc, mbytes, &full[s]);
-        if (wsrc) tma_row_load(&ring[s][0], wsrc, 16, &full[s]);
-        if (esrc) tma_row_load(&ring[s][epos], esrc, 16, &full[s]);
-        if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
+            mbar_expect_tx(&full[s], bytes);
+            tma_row_load(&ring[s][mpos], msrc, mbytes, &full[s]);
+            if (wsrc) {
+                tma_row_load(&ring[s][0], wsrc, 16, &full[s]);
+                wsrc += a.sx;
+            }
+            if (esrc) {
+                tma_row_load(&ring[s][epos], esrc, 16, &full[s]);
+                esrc += a.sx;
+            }
+            msrc += mstep;
+            if (++s == STAGES) {
+                s = 0;
+                ph ^= 1;
+            }
         }
     }
 }
