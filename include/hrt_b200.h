@@ -238,8 +238,8 @@ int hrt_jacobi_plan_set_wave_ipc(void *plan, const int32_t *rpeer4, const int32_
  * index in that rank's plan.  Only row faces qualify; otherwise a no-op. */
 int hrt_jacobi_plan_set_wave2_remote(void *plan, const uint64_t *bufs8, const uint64_t *cnt4,
                                      const int32_t *idx4);
-/* *on = 1 when runs of >= 4 steps use two-step passes (slabs) or
- * two-step launches (x-band volumes). */
+/* *on = 1 when runs of >= 4 steps use two-step passes: slab_wave2_kernel
+ * (slabs) or volume_wave2_kernel (x-band volumes on one GPU). */
 int hrt_jacobi_plan_two_step(void *plan, int *on);
 /* Chunk count the tiling decisions (tile rows, two-step passes or not) are
  * made for: pass the largest chunk count per GPU of the whole

@@ -4226,7 +4226,7 @@ int hrt_jacobi_plan_error(void* plan, int* err) {
 int hrt_jacobi_plan_two_step(void* plan, int* on) {
     HRT_CHECK_ARG(plan && on, "null argument");
     const Plan* p = reinterpret_cast<Plan*>(plan);
-    *on = fuse2_use(p) ? 1 : 0;
+    *on = pass_steps_of(p) == 2 ? 1 : 0;  // slab or volume two-step passes
     return HRT_OK;
 }
 

@@ -76,6 +76,33 @@ def test_cfg3_full_size_vs_oracle(solver_mod, oracle):
     assert cs == oracle.checksum(ref)
 
 
+def test_paper3d_as_benched_vs_oracle(solver_mod, oracle):
+    """The paper's Jacobi3D size as bench.py's paper3d runs it (1024x1024x768,
+    x-bands of 8 chunks, 100 iterations: 50 two-step passes of
+    volume_wave2_kernel, unguarded instance chosen on the device): field,
+    checksum and residual history vs the C oracle."""
+    dom, steps = (1024, 1024, 768), 100
+    got, res, cs, two, _, _ = _solve(solver_mod, dom, (8, 1, 1), steps)
+    assert two, "paper3d runs two-step passes"
+    ref, rref = oracle.jacobi_c(dom, steps, residual=True)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    assert np.array_equal(res, rref), np.nonzero(res != rref)[0][:4]
+    del got
+    assert cs == oracle.checksum(ref)
+
+
+def test_paper3d_shape_random_signed_vs_oracle(solver_mod, oracle):
+    """Random signed data at the paper3d shape: the guarded volume instance
+    (the upload scan flags negatives), 9 steps = 1 single + 4 passes."""
+    dom, steps = (1024, 1024, 768), 9
+    init = np.random.default_rng(7).random(dom) * 4.0 - 2.0
+    got, res, _, two, _, _ = _solve(solver_mod, dom, (8, 1, 1), steps, init)
+    assert two
+    ref, rref = oracle.jacobi_c(dom, steps, residual=True, initial=init)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    assert np.array_equal(res, rref)
+
+
 @pytest.mark.parametrize("dom,grid", [((40, 70, 1), (4, 5, 1)), ((600, 1024, 1), (2, 2, 1)),
                                       ((10, 12, 14), (2, 3, 2))])
 @pytest.mark.parametrize("steps", [1, 2, 5])
