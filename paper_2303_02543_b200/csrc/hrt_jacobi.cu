@@ -1126,9 +1126,6 @@ __device__ __forceinline__ void w2_produce(const Wave2Args& a, double (*ring)[W 
     }
 }
 
-#ifndef W2_EARLY
-#define W2_EARLY 1
-#endif
 // ---- shared-memory helpers on 32-bit shared addresses (computed once per
 // tile: a generic->shared conversion per row cost an S2R of the CTA id, a
 // LEA and an IMAD on every row) ----
@@ -1209,9 +1206,7 @@ __device__ __forceinline__ void w2_take(W2Ctx& x, double2 (&v)[NP]) {
         x.s = 0;
         x.ph ^= 1;
     }
-#if W2_EARLY
     x.ready = mbar_try_u32(x.full + 8u * (uint32_t)x.s, x.ph);
-#endif
 }
 
 template <int NP>
