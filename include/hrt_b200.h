@@ -225,6 +225,21 @@ int hrt_jacobi_plan_set_persistent(void *plan, const int32_t *nbr4, uint64_t tim
 /* The plan's wavefront tile counters (device address, for CUDA IPC export
  * to neighbour ranks) and their count. */
 int hrt_jacobi_plan_wave_counters(void *plan, uint64_t *ptr, int64_t *ntiles);
+/* Volume two-step passes across processes (x-band volumes split between
+ * ranks; replaces the per-step halo messages of _RankDriver jacobi.py:
+ * 219-273 like the slab wave).  vw2_counters: the plan's per-tile step
+ * counters of volume_wave2_kernel (allocated on first use, never moved)
+ * for CUDA IPC export.  set_vw2_remote: per chunk and x face (-x, +x) the
+ * neighbour process's chunk buffers for parity 0/1 (bufs4, mapped here; 0 =
+ * no such face), the base of that process's vw2 counters (cnt2, mapped)
+ * and the chunk's index in its plan (idx2).  range: device address of the
+ * upload scan (2 x uint64: ~bits of the smallest positive value, bad flag)
+ * that ranks max-reduce so every rank picks the division from the global
+ * field. */
+int hrt_jacobi_plan_vw2_counters(void *plan, uint64_t *ptr, int64_t *ntiles);
+int hrt_jacobi_plan_set_vw2_remote(void *plan, const uint64_t *bufs4, const uint64_t *cnt2,
+                                   const int32_t *idx2);
+int hrt_jacobi_plan_range(void *plan, uint64_t *ptr);
 /* Cross-process wavefront (the reference's halo messages between ranks,
  * jacobi.py:237 mp_send, as NVLink pushes + per-tile counters): per chunk and
  * face the peer slot (-1 none) and the neighbour chunk's index in that

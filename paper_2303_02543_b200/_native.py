@@ -119,6 +119,9 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_sides": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_set_vpush": (c_int, [c_void_p, c_void_p]),
     "hrt_jacobi_plan_wave_counters": (c_int, [c_void_p, P(c_u64), P(c_i64)]),
+    "hrt_jacobi_plan_vw2_counters": (c_int, [c_void_p, P(c_u64), P(c_i64)]),
+    "hrt_jacobi_plan_set_vw2_remote": (c_int, [c_void_p, P(c_u64), P(c_u64), P(ctypes.c_int32)]),
+    "hrt_jacobi_plan_range": (c_int, [c_void_p, P(c_u64)]),
     "hrt_jacobi_plan_two_step": (c_int, [c_void_p, P(c_int)]),
     "hrt_jacobi_plan_set_tiling_chunks": (c_int, [c_void_p, c_i64]),
     "hrt_jacobi_plan_set_fuse2": (c_int, [c_void_p, c_int]),

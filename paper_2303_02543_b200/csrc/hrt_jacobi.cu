@@ -2305,11 +2305,24 @@ constexpr uint32_t VW_STAGE_BYTES = (uint32_t)(VW_RR * VW_RS * 8);
 constexpr size_t VW_SMEM = (size_t)VW_STAGES * VW_STAGE_BYTES;  // the ring (dynamic)
 static_assert(VW_STAGE_BYTES % 128 == 0, "TMA tensor destinations must stay 128-byte aligned");
 
+// x neighbours of a chunk (faces -x, +x): the tensor maps their planes are
+// read through (null: a domain face, whose ghost plane is read from the own
+// buffer), the step counter of their tile 0 (this plan's, or mapped from
+// the neighbour process over CUDA IPC) and which of them live in another
+// process (system-scope counters)
+struct VW2Nbr {
+    const CUtensorMap* map[2][2];   // [face][parity]
+    const unsigned int* cnt[2];     // [face]
+    unsigned sys;                   // bit f: face f's neighbour is in another process
+    unsigned pad_;
+};
+
 struct VolW2Args {
     const CUtensorMap* maps;   // [nchunks][2] tensor map of buffer 0 / 1
     const ChunkBufs* chunks;
-    const int* xnb;            // [nchunks][2] -x / +x neighbour chunk or -1
-    unsigned int* done;        // [T] steps completed per tile (from 0 at launch)
+    const VW2Nbr* nbr;         // [nchunks]
+    unsigned int* done;        // [T] steps completed per tile (absolute: base at launch)
+    unsigned int base;
     unsigned long long* ticket;
     const unsigned long long* range;  // field scan: [0] ~bits(min positive), [1] bad flag
     double need;               // unguarded division is exact if min positive >= need
@@ -2350,10 +2363,10 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
 __device__ __forceinline__ void vw2_produce(const VolW2Args& a, uint32_t ring, uint64_t* full,
                                             uint64_t* empty, int& s, uint32_t& ph, int64_t c,
                                             int64_t j0, int64_t k0, int parity) {
-    const int xm = a.xnb[2 * c], xp = a.xnb[2 * c + 1];
+    const VW2Nbr& nb = a.nbr[c];
     const CUtensorMap* own = a.maps + 2 * c + parity;
-    const CUtensorMap* mm = xm >= 0 ? a.maps + 2 * xm + parity : own;
-    const CUtensorMap* pm = xp >= 0 ? a.maps + 2 * xp + parity : own;
+    const CUtensorMap* mm = nb.map[0][parity];
+    const CUtensorMap* pm = nb.map[1][parity];
     const int c0 = (int)(a.origin + k0 - 2), c1 = (int)(j0 - 2);
     const int ex = (int)a.ex;
     const int nplanes = ex + 4;
@@ -2361,10 +2374,10 @@ __device__ __forceinline__ void vw2_produce(const VolW2Args& a, uint32_t ring, u
         const int i = q - 1;  // plane; neighbour planes in place, domain ghosts from own buffer
         const CUtensorMap* m = own;
         int ii = i;
-        if (i < 1 && xm >= 0) {
+        if (i < 1 && mm) {
             m = mm;
             ii = i + ex;
-        } else if (i > ex && xp >= 0) {
+        } else if (i > ex && pm) {
             m = pm;
             ii = i - ex;
         }
@@ -2620,8 +2633,8 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     x.ex = a.ex;
     x.sx = a.sx;
     x.sy = a.sy;
-    x.xlo = a.xnb[2 * c] < 0;
-    x.xhi = a.xnb[2 * c + 1] < 0;
+    x.xlo = a.nbr[c].map[0][0] == nullptr;
+    x.xhi = a.nbr[c].map[1][0] == nullptr;
     unsigned vrow = 0;
 #pragma unroll
     for (int r = 0; r < VW_RR; ++r) {
@@ -2741,17 +2754,19 @@ volume_wave2_kernel(VolW2Args wa) {
             const int64_t zb = rem - yb * tk;
             if (!dead) {
                 // the 3 x 3 x 3 tile neighbourhood must be done with step 2k
-                const unsigned need = 2u * (unsigned)k;
+                const unsigned need = wa.base + 2u * (unsigned)k;
                 const unsigned int* q[27];
                 bool sys[27];
-                const int cx[3] = {wa.xnb[2 * c], (int)c, wa.xnb[2 * c + 1]};
+                const VW2Nbr& nb = wa.nbr[c];
+                const unsigned int* cx[3] = {nb.cnt[0], wa.done + c * per_chunk, nb.cnt[1]};
+                const bool sx[3] = {(nb.sys & 1u) != 0, false, (nb.sys & 2u) != 0};
 #pragma unroll
                 for (int d = 0; d < 27; ++d) {
-                    const int cc = cx[d / 9];
+                    const unsigned int* cc = cx[d / 9];
                     const int64_t y2 = yb + (d / 3) % 3 - 1, z2 = zb + d % 3 - 1;
-                    const bool in = cc >= 0 && y2 >= 0 && y2 < tj && z2 >= 0 && z2 < tk;
-                    q[d] = in ? wa.done + (int64_t)cc * per_chunk + y2 * tk + z2 : nullptr;
-                    sys[d] = false;
+                    const bool in = cc && y2 >= 0 && y2 < tj && z2 >= 0 && z2 < tk;
+                    q[d] = in ? cc + y2 * tk + z2 : nullptr;
+                    sys[d] = sx[d / 9];
                 }
                 dead = !wait_counters<27>(q, sys, need, wa.timeout_ns, wa.err);
                 asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -2791,7 +2806,11 @@ volume_wave2_kernel(VolW2Args wa) {
                 red[1][warp] = r2;
             }
         }
+        // every tile of a chunk with a neighbour in another process is read
+        // by it (a tile spans all planes): stores visible system-wide first
+        const bool xsys = wa.nbr[c].sys != 0;
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (xsys) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * VW_CW));
         if (tid == 0) {
             if (RESID && wa.resid) {
@@ -2804,8 +2823,15 @@ volume_wave2_kernel(VolW2Args wa) {
                 resid_max(wa.resid + 2 * k, m1);
                 resid_max(wa.resid + 2 * k + 1, m2);
             }
-            __threadfence();
-            st_release_gpu_u32(wa.done + tile, 2u * (unsigned)k + 2u);
+            const unsigned v = wa.base + 2u * (unsigned)k + 2u;
+            if (xsys) {
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
+                             : "memory");
+            } else {
+                __threadfence();
+                st_release_gpu_u32(wa.done + tile, v);
+            }
         }
     }
 }
@@ -2910,9 +2936,14 @@ struct Plan {
     double* d_ones = nullptr;      // BOUNDARY row (rows outside the domain)
     // two steps per pass for x-band volumes (volume_wave2_kernel)
     std::vector<hrt_vpush_t> h_vpush;  // host copy of the push table (face kinds)
-    unsigned int* d_v2done = nullptr;  // per-tile step counters, reset every launch
-    int* d_v2nb = nullptr;             // [nchunks][2] -x / +x neighbour chunk
-    CUtensorMap* d_v2maps = nullptr;   // [nchunks][2] 3D tensor maps of the buffers
+    unsigned int* d_v2done = nullptr;  // per-tile step counters (absolute; IPC-exported)
+    unsigned int v2base = 0;           // every d_v2done entry between launches
+    VW2Nbr* d_v2nbr = nullptr;         // [nchunks] x-neighbour table
+    bool v2dirty = true;               // maps / table to (re)build
+    CUtensorMap* d_v2maps = nullptr;   // own [nchunks][2], then remote [nchunks][2 faces][2]
+    // x faces to another process (hrt_jacobi_plan_set_vw2_remote): mapped
+    // buffers [nchunks][2 faces][2 parities] and tile-0 counters [nchunks][2]
+    std::vector<uint64_t> v2rbuf, v2rcnt;
     // field scan of the last upload (volume plans; see vw2_fast) and the
     // steps run since (saturating; "unknown" until the first scan)
     unsigned long long* d_range = nullptr;
@@ -3531,8 +3562,8 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
 // chunks of this plan or the domain (never to another GPU or process)
 static bool vfuse2_on(const Plan* p) {
     const hrt_chunk_layout_t& L = p->L;
-    if (!p->fuse2 || L.ndim != 3 || !p->persist_on() || p->wave_ipc || !p->remote.empty() || p->ipc)
-        return false;
+    if (!p->fuse2 || L.ndim != 3 || !p->persist_on() || p->ipc) return false;
+    if (!p->wave_ipc && !p->remote.empty()) return false;
     if (L.ext[0] < 2 || L.origin % 2 != 1 || L.stride[0] % 2 != 0 || L.stride[1] % 2 != 0)
         return false;
     if ((int64_t)p->nbr.size() != 6 * (int64_t)p->nchunks ||
@@ -3542,8 +3573,14 @@ static bool vfuse2_on(const Plan* p) {
         for (int f = 0; f < 6; ++f) {
             const int n = p->nbr[6 * (size_t)c + f];
             const hrt_vpush_t& v = p->h_vpush[c];
-            if (f >= 2 && n >= 0) return false;                       // y / z: domain faces
-            if (n < 0 && (v.ptr[f][0] || v.ptr[f][1])) return false;  // a face to another GPU
+            const bool other_gpu = n < 0 && (v.ptr[f][0] || v.ptr[f][1]);
+            if (f >= 2 && (n >= 0 || other_gpu)) return false;  // y / z: domain faces only
+            if (!other_gpu) continue;
+            // x face to another GPU: only another process's chunk whose
+            // buffers and counters are mapped (hrt_jacobi_plan_set_vw2_remote)
+            if (!p->wave_ipc || p->v2rcnt.empty() || !p->v2rcnt[2 * (size_t)c + f] ||
+                !p->v2rbuf[4 * (size_t)c + 2 * f] || !p->v2rbuf[4 * (size_t)c + 2 * f + 1])
+                return false;
         }
     return true;
 }
@@ -3582,21 +3619,33 @@ static int build_vw2_maps(Plan* p) {
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
     const hrt_chunk_layout_t& L = p->L;
-    std::vector<CUtensorMap> maps(2 * (size_t)p->nchunks);
+    std::vector<CUtensorMap> maps(6 * (size_t)p->nchunks);
+    memset(maps.data(), 0, sizeof(CUtensorMap) * maps.size());
     const cuuint64_t dims[3] = {(cuuint64_t)L.stride[1], (cuuint64_t)(L.ext[1] + 2),
                                 (cuuint64_t)(L.ext[0] + 2)};
     const cuuint64_t strides[2] = {(cuuint64_t)L.stride[1] * 8, (cuuint64_t)L.stride[0] * 8};
     const cuuint32_t box[3] = {VW_RS, VW_RR, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    auto enc = [&](CUtensorMap* m, void* base) -> int {
+        CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+            return HRT_E_CUDA;
+        }
+        return HRT_OK;
+    };
+    const size_t R = 2 * (size_t)p->nchunks;  // remote maps start here
     for (int c = 0; c < p->nchunks; ++c)
         for (int par = 0; par < 2; ++par) {
-            CUresult r = encode(&maps[2 * (size_t)c + par], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
-                                p->h_chunks[c].b[par], dims, strides, box, estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) {
-                set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
-                return HRT_E_CUDA;
+            int rc = enc(&maps[2 * (size_t)c + par], p->h_chunks[c].b[par]);
+            if (rc) return rc;
+            for (int f = 0; f < 2 && !p->v2rbuf.empty(); ++f) {
+                const uint64_t b = p->v2rbuf[4 * (size_t)c + 2 * f + par];
+                if (!b) continue;
+                rc = enc(&maps[R + 4 * (size_t)c + 2 * f + par], reinterpret_cast<void*>(b));
+                if (rc) return rc;
             }
         }
     cudaFree(p->d_v2maps);
@@ -3604,6 +3653,54 @@ static int build_vw2_maps(Plan* p) {
     HRT_CUDA(cudaMalloc(&p->d_v2maps, sizeof(CUtensorMap) * maps.size()));
     HRT_CUDA(cudaMemcpy(p->d_v2maps, maps.data(), sizeof(CUtensorMap) * maps.size(),
                         cudaMemcpyHostToDevice));
+    return HRT_OK;
+}
+
+// per-tile step counters of the volume two-step passes: allocated once
+// (zero), absolute (v2base between launches), exported over CUDA IPC to the
+// neighbour processes, so never reset or reallocated
+static int ensure_vw2_counters(Plan* p) {
+    const int64_t T = vw2_tiles(p);
+    if (p->d_v2done) {
+        if (p->v2_tiles != T) {
+            set_error("volume two-step tiling changed after the counters were allocated");
+            return HRT_E_INVALID;
+        }
+        return HRT_OK;
+    }
+    HRT_CUDA(cudaMalloc(&p->d_v2done, sizeof(unsigned int) * std::max<int64_t>(1, T)));
+    HRT_CUDA(cudaMemset(p->d_v2done, 0, sizeof(unsigned int) * std::max<int64_t>(1, T)));
+    p->v2_tiles = T;
+    p->v2base = 0;
+    return HRT_OK;
+}
+
+// x-neighbour table of the volume two-step kernel (maps already built)
+static int build_vw2_nbr(Plan* p) {
+    const int64_t per_chunk = vw2_tiles(p) / std::max(1, p->nchunks);
+    const size_t R = 2 * (size_t)p->nchunks;
+    std::vector<VW2Nbr> t((size_t)std::max(1, p->nchunks));
+    for (int c = 0; c < p->nchunks; ++c) {
+        VW2Nbr& o = t[c];
+        memset(&o, 0, sizeof(o));
+        for (int f = 0; f < 2; ++f) {
+            const int n = p->nbr[6 * (size_t)c + f];
+            if (n >= 0) {
+                o.map[f][0] = p->d_v2maps + 2 * (size_t)n;
+                o.map[f][1] = p->d_v2maps + 2 * (size_t)n + 1;
+                o.cnt[f] = p->d_v2done + (int64_t)n * per_chunk;
+            } else if (!p->v2rcnt.empty() && p->v2rcnt[2 * (size_t)c + f]) {
+                o.map[f][0] = p->d_v2maps + R + 4 * (size_t)c + 2 * f;
+                o.map[f][1] = p->d_v2maps + R + 4 * (size_t)c + 2 * f + 1;
+                o.cnt[f] = reinterpret_cast<const unsigned int*>(p->v2rcnt[2 * (size_t)c + f]);
+                o.sys |= 1u << f;
+            }
+        }
+    }
+    cudaFree(p->d_v2nbr);
+    p->d_v2nbr = nullptr;
+    HRT_CUDA(cudaMalloc(&p->d_v2nbr, sizeof(VW2Nbr) * t.size()));
+    HRT_CUDA(cudaMemcpy(p->d_v2nbr, t.data(), sizeof(VW2Nbr) * t.size(), cudaMemcpyHostToDevice));
     return HRT_OK;
 }
 
@@ -3622,23 +3719,15 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     int64_t tj = 0, tk = 0;
     const int64_t T = vw2_tiles(p, &tj, &tk);
     if (T == 0) return HRT_OK;
-    if (!p->d_v2done || p->v2_tiles != T) {
-        HRT_CUDA(cudaStreamSynchronize(s));
-        cudaFree(p->d_v2done);
-        cudaFree(p->d_v2nb);
-        p->d_v2done = nullptr;
-        p->d_v2nb = nullptr;
-        HRT_CUDA(cudaMalloc(&p->d_v2done, sizeof(unsigned int) * T));
-        std::vector<int> nb(2 * (size_t)p->nchunks);
-        for (int c = 0; c < p->nchunks; ++c) {
-            nb[2 * (size_t)c] = p->nbr[6 * (size_t)c];
-            nb[2 * (size_t)c + 1] = p->nbr[6 * (size_t)c + 1];
-        }
-        HRT_CUDA(cudaMalloc(&p->d_v2nb, sizeof(int) * nb.size()));
-        HRT_CUDA(cudaMemcpy(p->d_v2nb, nb.data(), sizeof(int) * nb.size(), cudaMemcpyHostToDevice));
-        int rc = build_vw2_maps(p);
+    int rc = ensure_vw2_counters(p);
+    if (rc) return rc;
+    if (p->v2dirty) {
+        HRT_CUDA(cudaStreamSynchronize(s));  // the table of a launch in flight
+        rc = build_vw2_maps(p);
         if (rc) return rc;
-        p->v2_tiles = T;
+        rc = build_vw2_nbr(p);
+        if (rc) return rc;
+        p->v2dirty = false;
     }
     if (!p->d_range) {  // never scanned: "unknown" (guarded division)
         HRT_CUDA(cudaMalloc(&p->d_range, 2 * sizeof(unsigned long long)));
@@ -3662,11 +3751,11 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
         p->pgrid3 = n * sm_count(p->gpu);
     }
     HRT_CUDA(cudaMemsetAsync(p->d_pticket, 0, sizeof(unsigned long long), s));
-    HRT_CUDA(cudaMemsetAsync(p->d_v2done, 0, sizeof(unsigned int) * T, s));
     VolW2Args wa{};
     wa.chunks = p->d_chunks;
-    wa.xnb = p->d_v2nb;
+    wa.nbr = p->d_v2nbr;
     wa.done = p->d_v2done;
+    wa.base = p->v2base;
     wa.ticket = p->d_pticket;
     wa.nfused = (int)nf;
     wa.parity0 = (int)(first & 1);
@@ -3696,6 +3785,7 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     void* args[] = {&wa};
     for (void* fn : fns)
         HRT_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (VW_CW + 1)), args, VW_SMEM, s));
+    p->v2base += 2u * (unsigned)nf;
     p->ghosts_ready = false;  // passes read neighbours in place; ghost planes went stale
     return HRT_OK;
 }
@@ -4175,6 +4265,7 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     }
     HRT_CUDA(cudaDeviceSynchronize());  // no launch of the old build in flight
     p->nbr.assign(nbr4, nbr4 + nf * p->nchunks);
+    p->v2dirty = true;
     cudaFree(p->d_pnbr);
     p->d_pnbr = nullptr;
     // two-step passes run best with 256-row tiles (rim rows 4/256 of the
@@ -4245,6 +4336,46 @@ int hrt_jacobi_plan_tiling(void* plan, int64_t* rows, int64_t* tiles_per_chunk, 
     *rows = p->rows;
     *tiles_per_chunk = wave_tiles(p) / std::max(1, p->nchunks);
     *two_step = pass_steps_of(p);
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_vw2_counters(void* plan, uint64_t* ptr, int64_t* ntiles) {
+    HRT_CHECK_ARG(plan && ptr && ntiles, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG(p->L.ndim == 3, "volume plans only");
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    rc = ensure_vw2_counters(p);
+    if (rc) return rc;
+    *ptr = reinterpret_cast<uint64_t>(p->d_v2done);
+    *ntiles = p->v2_tiles;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_vw2_remote(void* plan, const uint64_t* bufs4, const uint64_t* cnt2,
+                                   const int32_t* idx2) {
+    HRT_CHECK_ARG(plan && bufs4 && cnt2 && idx2, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG(p->L.ndim == 3, "volume plans only");
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaDeviceSynchronize());  // no launch reads the old table
+    const int64_t per_chunk = vw2_tiles(p) / std::max(1, p->nchunks);
+    p->v2rbuf.assign(bufs4, bufs4 + 4 * (size_t)p->nchunks);
+    p->v2rcnt.assign(2 * (size_t)p->nchunks, 0);
+    for (size_t k = 0; k < p->v2rcnt.size(); ++k)
+        if (cnt2[k]) {
+            HRT_CHECK_ARG(idx2[k] >= 0, "remote chunk index missing");
+            p->v2rcnt[k] = cnt2[k] + sizeof(unsigned int) * (uint64_t)(idx2[k] * per_chunk);
+        }
+    p->v2dirty = true;
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_range(void* plan, uint64_t* ptr) {
+    HRT_CHECK_ARG(plan && ptr, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    *ptr = reinterpret_cast<uint64_t>(p->d_range);
     return HRT_OK;
 }
 
@@ -4515,7 +4646,7 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_n9);
     cudaFree(p->d_ones);
     cudaFree(p->d_v2done);
-    cudaFree(p->d_v2nb);
+    cudaFree(p->d_v2nbr);
     cudaFree(p->d_v2maps);
     cudaFree(p->d_range);
     if (p->side) cudaStreamDestroy(p->side);

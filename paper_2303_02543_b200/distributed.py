@@ -85,11 +85,17 @@ class DistributedJacobi(JacobiSolver):
         rows_only = bool(cross) and all(f in (0, 1) for f, _, _ in cross)
         # column faces qualify once they are contiguous (side arrays)
         slab_ok = bool(cross) and self.push and (rows_only or self.side_mode)
+        # volumes split along x only: the cross-process wavefront, with
+        # two-step passes (volume_wave2_kernel) reading the neighbour rank's
+        # planes in place, by default
+        xband3 = (self.layout.ndim == 3 and rows_only and grid.grid[1] == 1 and grid.grid[2] == 1
+                  and os.environ.get("HRT_FUSE2", "1") != "0")
         if world > 1 and os.environ.get("HRT_IPC", "1") != "0" and (slab_ok or rows_only):
             if self.push:
                 self._setup_ipc(gpu)
             elif (self.layout.ndim == 3 and variant != 0
-                  and (vpush if vpush is not None else os.environ.get("HRT_VPUSH", "0") == "1")
+                  and (vpush if vpush is not None
+                       else (os.environ.get("HRT_VPUSH", "0") == "1" or xband3))
                   and os.environ.get("HRT_PUSH", "1") != "0"
                   and os.environ.get("HRT_PERSIST", "1") != "0"):
                 self._setup_ipc3(gpu)
@@ -210,7 +216,7 @@ class DistributedJacobi(JacobiSolver):
         self._setup_vpush(remote_buf)
         self.vpush = True
         self.ipc = True
-        self._setup_wave_ipc(g, mine, nbr_ranks)
+        self._setup_wave_ipc(g, mine, nbr_ranks, remote_buf)
         dist.barrier()
 
     def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list, remote_buf=None) -> None:
@@ -279,6 +285,37 @@ class DistributedJacobi(JacobiSolver):
                         idxs.append(rnbr[4 * k + f])
             N.call("hrt_jacobi_plan_set_wave2_remote", plan, _arr(ctypes.c_uint64, bufs),
                    _arr(ctypes.c_uint64, cnts), _arr(ctypes.c_int32, idxs))
+        if remote_buf is not None and nf == 6:
+            # volume two-step passes read the neighbour rank's x planes in
+            # place and wait on its tile counters (both mapped over IPC)
+            ptr2, n2 = ctypes.c_uint64(), ctypes.c_int64()
+            N.call("hrt_jacobi_plan_vw2_counters", plan, ctypes.byref(ptr2), ctypes.byref(n2))
+            h2 = ctypes.create_string_buffer(64)
+            N.call("hrt_ipc_get_handle", ctypes.c_void_p(ptr2.value), h2)
+            every2 = [None] * self.world
+            dist.all_gather_object(every2, h2.raw)
+            cnt_of = {}
+            for q in nbr_ranks:
+                pq = ctypes.c_void_p()
+                N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(every2[q], 64),
+                       ctypes.byref(pq))
+                self._ipc_maps.append(pq.value)
+                cnt_of[q] = pq.value
+            bufs, cnts, idxs = [], [], []
+            for k, lin in enumerate(mine):
+                for f in (0, 1):
+                    p = rpeer[nf * k + f]
+                    nb = self.grid.chunks[lin].neighbors.get(f)
+                    if p < 0:
+                        bufs += [0, 0]
+                        cnts.append(0)
+                        idxs.append(-1)
+                    else:
+                        bufs += [remote_buf(nb, 0), remote_buf(nb, 1)]
+                        cnts.append(cnt_of[nbr_ranks[p]])
+                        idxs.append(rnbr[nf * k + f])
+            N.call("hrt_jacobi_plan_set_vw2_remote", plan, _arr(ctypes.c_uint64, bufs),
+                   _arr(ctypes.c_uint64, cnts), _arr(ctypes.c_int32, idxs))
         # a rank with a column face to another process keeps one step per
         # pass; then no rank may run two-step passes (see _agree_tiling)
         tilings = [None] * self.world
@@ -303,6 +340,19 @@ class DistributedJacobi(JacobiSolver):
             N.call("hrt_nccl_allreduce_max_u64", ctypes.c_void_p(self.comm), self.streams[g].h,
                    ctypes.c_void_p(self.resid[g]), n)
         return self.residual_history()
+
+    def _after_scatter(self) -> None:
+        """Volumes: every rank's upload scan (smallest positive value, bad
+        flag) max-reduced over all ranks on the solver stream, so each
+        rank's two-step launch picks its division from the global field —
+        tiny values of one rank reach its neighbours within a few steps."""
+        if self.world > 1 and self.layout.ndim == 3 and self.comm:
+            g = self.used_gpus[0]
+            ptr = ctypes.c_uint64()
+            N.call("hrt_jacobi_plan_range", self.plans[g], ctypes.byref(ptr))
+            if ptr.value:
+                N.call("hrt_nccl_allreduce_max_u64", ctypes.c_void_p(self.comm),
+                       self.streams[g].h, ctypes.c_void_p(ptr.value), 2)
 
     def allreduce_residual(self) -> None:
         """Enqueue the cross-rank max of this run's residual history on the

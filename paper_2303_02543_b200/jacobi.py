@@ -550,6 +550,12 @@ class JacobiSolver:
         for g in self.used_gpus:
             N.call("hrt_jacobi_plan_field_copy", self.plans[g], self.streams[g].h,
                    ctypes.c_void_p(field_ptr), Y, Z, parity, 1 if to_chunks else 0)
+        if to_chunks:
+            self._after_scatter()
+
+    def _after_scatter(self) -> None:
+        """Hook after new interiors were scattered (distributed solvers
+        reduce the upload scan across ranks)."""
 
     def _setup_push(self) -> None:
         """Fused halo: for every owned chunk and slab face, where the update

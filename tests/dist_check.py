@@ -67,7 +67,9 @@ for dom, grid, steps in cases:
 # the residual history vs the numpy oracle
 os.environ["HRT_FUSE2"] = "2"  # small domains: force two-step passes
 for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
-                         ((96, 64, 1), (4 * world, 1, 1), 9)]:
+                         ((96, 64, 1), (4 * world, 1, 1), 9),
+                         # volumes: volume_wave2_kernel (guarded instance)
+                         ((12 * world, 20, 130), (2 * world, 1, 1), 13)]:
     cg = ChunkGrid(dom, ranks=world, grid=grid)
     s = DistributedJacobi(cg, rank, world, local)
     full_init = np.random.default_rng(7).random(dom) * 4.0 - 1.0
@@ -97,7 +99,9 @@ for dom, grid, steps in [((256, 130, 1), (2 * world, 1, 1), 14),
 # re-upload between jobs: single steps -> fused passes -> the next run's
 # ghost priming after stale ghosts (what bench's job stream does)
 for dom, grid, parts in [((256, 130, 1), (2 * world, 1, 1), (5, 1, 9)),
-                         ((96, 64, 1), (4 * world, 1, 1), (4, 7, 2))]:
+                         ((96, 64, 1), (4 * world, 1, 1), (4, 7, 2)),
+                         # volumes, non-negative: the unguarded instance
+                         ((12 * world, 20, 130), (2 * world, 1, 1), (5, 1, 9))]:
     cg = ChunkGrid(dom, ranks=world, grid=grid)
     s = DistributedJacobi(cg, rank, world, local)
     lo, bx = s.box_lo, s.box
