@@ -74,6 +74,7 @@ class DistributedJacobi(JacobiSolver):
             comm = nccl_comm(rank, world, gpu)
         self.world = world
         self._ipc_maps: list[int] = []
+        self._fence_buf = None
         super().__init__(grid, gpus=[gpu], rank=rank, comm=comm, rows=rows, variant=variant)
         self.ipc = False
         # decided from the global decomposition so every rank agrees: IPC
@@ -341,11 +342,38 @@ class DistributedJacobi(JacobiSolver):
                    ctypes.c_void_p(self.resid[g]), n)
         return self.residual_history()
 
+    def _rank_fence(self) -> None:
+        """Device-side barrier across ranks on the solver stream (a one-word
+        NCCL max all-reduce): what this rank enqueues after it runs only
+        once every rank has finished what it enqueued before."""
+        g = self.used_gpus[0]
+        if self._fence_buf is None:
+            self._fence_buf = DevicePool(g, 256)
+        N.call("hrt_nccl_allreduce_max_u64", ctypes.c_void_p(self.comm), self.streams[g].h,
+               ctypes.c_void_p(self._fence_buf.base), 1)
+
+    def _fenced(self) -> bool:
+        """Neighbour ranks read this rank's chunks in place (IPC: two-step
+        passes and their rims), so host-initiated writes need fences."""
+        return bool(self.world > 1 and self.comm and self.ipc)
+
+    def _chunk_copies(self, to_chunks: bool, parity: int, field_ptr: int, stream_of=None) -> None:
+        # new interiors: the previous job's kernels of the neighbour ranks
+        # may still read this rank's chunks in place — fence before
+        # overwriting them (and, in _after_scatter, before anyone reads the
+        # new ones: a two-step launch right after an upload has no ghost
+        # exchange that would order it after the neighbours' uploads)
+        if to_chunks and self._fenced():
+            self._rank_fence()
+        super()._chunk_copies(to_chunks, parity, field_ptr, stream_of)
+
     def _after_scatter(self) -> None:
         """Volumes: every rank's upload scan (smallest positive value, bad
         flag) max-reduced over all ranks on the solver stream, so each
         rank's two-step launch picks its division from the global field —
-        tiny values of one rank reach its neighbours within a few steps."""
+        tiny values of one rank reach its neighbours within a few steps.
+        The reduction (or a fence) also orders every rank's next launch
+        after all ranks' uploads."""
         if self.world > 1 and self.layout.ndim == 3 and self.comm:
             g = self.used_gpus[0]
             ptr = ctypes.c_uint64()
@@ -353,6 +381,9 @@ class DistributedJacobi(JacobiSolver):
             if ptr.value:
                 N.call("hrt_nccl_allreduce_max_u64", ctypes.c_void_p(self.comm),
                        self.streams[g].h, ctypes.c_void_p(ptr.value), 2)
+                return
+        if self._fenced():
+            self._rank_fence()
 
     def allreduce_residual(self) -> None:
         """Enqueue the cross-rank max of this run's residual history on the

@@ -547,6 +547,15 @@ class JacobiSolver:
         GPU's solver stream (the field lives on the first GPU; the others
         reach it over NVLink).  Callers order the GPUs (_fan_out/_fan_in)."""
         _, Y, Z = self.box
+        if to_chunks and len(self.used_gpus) > 1:
+            # the previous run's kernels on the other GPUs may still read
+            # these chunks in place (two-step passes): every GPU's copy waits
+            # for all of them; the next run orders itself after the copies
+            tok = {g: self.streams[g].record() for g in self.used_gpus}
+            for g in self.used_gpus:
+                for h in self.used_gpus:
+                    if h != g:
+                        self.streams[g].wait(tok[h])
         for g in self.used_gpus:
             N.call("hrt_jacobi_plan_field_copy", self.plans[g], self.streams[g].h,
                    ctypes.c_void_p(field_ptr), Y, Z, parity, 1 if to_chunks else 0)
