@@ -352,6 +352,10 @@ class DistributedJacobi(JacobiSolver):
         N.call("hrt_nccl_allreduce_max_u64", ctypes.c_void_p(self.comm), self.streams[g].h,
                ctypes.c_void_p(self._fence_buf.base), 1)
 
+    def _segment_fence(self) -> None:
+        if self._fenced():
+            self._rank_fence()
+
     def _fenced(self) -> bool:
         """Neighbour ranks read this rank's chunks in place (IPC: two-step
         passes and their rims), so host-initiated writes need fences."""

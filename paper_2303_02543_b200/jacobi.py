@@ -454,10 +454,10 @@ class JacobiSolver:
             self._setup_push()
         # volumes: fused 6-face push + wavefront (opt-in: measured slower than
         # tile launches + halo pass on B200 at 1024x1024x768),
-        # except for x-band volumes on one GPU, where runs of >= 4 steps go
-        # as two-step passes (volume_wave2_kernel, built on the wavefront's
-        # neighbour table)
-        xband = (L.ndim == 3 and len(self.used_gpus) == 1 and not remote_ops and
+        # except for x-band volumes in one process (one GPU or several),
+        # where runs of >= 4 steps go as two-step passes
+        # (volume_wave2_kernel, built on the wavefront's neighbour table)
+        xband = (L.ndim == 3 and not remote_ops and
                  grid.grid[1] == 1 and grid.grid[2] == 1 and
                  os.environ.get("HRT_FUSE2", "1") != "0")
         if vpush is None:
@@ -562,9 +562,50 @@ class JacobiSolver:
         if to_chunks:
             self._after_scatter()
 
+    def _run_segments(self, first: int, steps: int) -> list:
+        """A run as launches of one kind each.  Volume two-step passes and
+        one-step launches keep separate tile counters (different tilings),
+        so when neighbours live on other GPUs or processes nothing orders a
+        neighbour's single steps before this GPU's first pass: the n mod 4
+        single steps and the passes become separate launches with a
+        cross-device fence between them (slabs share one counter array
+        between both kinds and need none)."""
+        cross = len(self.used_gpus) > 1 or getattr(self, "world", 1) > 1
+        if (cross and steps >= 4 and self.layout.ndim == 3 and self.persistent
+                and self.steps_per_pass == 2 and steps % 4):
+            nr = steps % 4
+            return [(first, nr), (first + nr, steps - nr)]
+        return [(first, steps)]
+
+    def _segment_fence(self) -> None:
+        """Between the launches of one run on one GPU per process: the
+        distributed solver fences across ranks; GPUs of one process order
+        themselves with stream waits in run()."""
+
     def _after_scatter(self) -> None:
-        """Hook after new interiors were scattered (distributed solvers
-        reduce the upload scan across ranks)."""
+        """After new interiors were scattered: with volumes on several GPUs,
+        each plan's upload scan saw only its own chunks, but values cross
+        GPU faces within a few steps — every plan gets the max over all
+        (distributed solvers reduce across ranks instead)."""
+        if self.layout.ndim != 3 or len(self.used_gpus) < 2:
+            return
+        vals = {}
+        for g in self.used_gpus:
+            ptr = ctypes.c_uint64()
+            N.call("hrt_jacobi_plan_range", self.plans[g], ctypes.byref(ptr))
+            if not ptr.value:
+                return
+            buf = (ctypes.c_uint64 * 2)()
+            N.call("hrt_copy_async", self.streams[g].h, ctypes.cast(buf, ctypes.c_void_p),
+                   ctypes.c_void_p(ptr.value), 16)
+            self.streams[g].synchronize()
+            vals[g] = (ptr.value, buf[0], buf[1])
+        merged = (ctypes.c_uint64 * 2)(max(v[1] for v in vals.values()),
+                                       max(v[2] for v in vals.values()))
+        for g, (p, _, _) in vals.items():
+            N.call("hrt_copy_async", self.streams[g].h, ctypes.c_void_p(p),
+                   ctypes.cast(merged, ctypes.c_void_p), 16)
+            self.streams[g].synchronize()
 
     def _setup_push(self) -> None:
         """Fused halo: for every owned chunk and slab face, where the update
@@ -646,7 +687,7 @@ class JacobiSolver:
         mine = {g: [lin for lin in self.owned if self.placement[lin] == g]
                 for g in self.used_gpus}
         index = {g: {lin: i for i, lin in enumerate(m)} for g, m in mine.items()}
-        counters = {}
+        counters, counters2 = {}, {}
         for g in self.used_gpus:
             nbr = []
             for lin in mine[g]:
@@ -659,6 +700,10 @@ class JacobiSolver:
             N.call("hrt_jacobi_plan_wave_counters", self.plans[g], ctypes.byref(ptr),
                    ctypes.byref(nt))
             counters[g] = ptr.value
+            if nf == 6:
+                N.call("hrt_jacobi_plan_vw2_counters", self.plans[g], ctypes.byref(ptr),
+                       ctypes.byref(nt))
+                counters2[g] = ptr.value
         for g in self.used_gpus:
             peers = sorted({self.placement[nb] for lin in mine[g]
                             for nb in self.grid.chunks[lin].neighbors.values()
@@ -696,6 +741,26 @@ class JacobiSolver:
                             cnts.append(counters[h])
                             idxs.append(index[h][nb])
                 N.call("hrt_jacobi_plan_set_wave2_remote", self.plans[g],
+                       _arr(ctypes.c_uint64, bufs), _arr(ctypes.c_uint64, cnts),
+                       _arr(ctypes.c_int32, idxs))
+            if nf == 6:
+                # volume two-step passes: the other GPU's x planes through
+                # tensor maps of its buffers, its tile counters (peer)
+                bufs, cnts, idxs = [], [], []
+                for lin in mine[g]:
+                    for f in (0, 1):
+                        nb = self.grid.chunks[lin].neighbors.get(f)
+                        h = self.placement.get(nb) if nb is not None else None
+                        if h is None or h == g:
+                            bufs += [0, 0]
+                            cnts.append(0)
+                            idxs.append(-1)
+                        else:
+                            N.call("hrt_enable_peer_access", g, h)
+                            bufs += list(self.bufs[nb])
+                            cnts.append(counters2[h])
+                            idxs.append(index[h][nb])
+                N.call("hrt_jacobi_plan_set_vw2_remote", self.plans[g],
                        _arr(ctypes.c_uint64, bufs), _arr(ctypes.c_uint64, cnts),
                        _arr(ctypes.c_int32, idxs))
         self._agree_tiling(list(self.tiling().values()))
@@ -843,19 +908,24 @@ class JacobiSolver:
         first = self.steps_done
         if len(self.used_gpus) == 1:
             g = self.used_gpus[0]
-            N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, first, steps,
-                   ctypes.c_void_p(self.resid[g] if residual else 0), 1 if graph else 0)
+            for i, (f0, n0) in enumerate(self._run_segments(first, steps)):
+                if i:
+                    self._segment_fence()
+                N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, f0, n0,
+                       ctypes.c_void_p(self.resid[g] if residual else 0), 1 if graph else 0)
         elif self.persistent:
             # every GPU primes its ghosts (reading its peers' uploaded
             # interiors) after all uploads, then runs its wavefront; the
-            # cross-GPU tile counters order everything else
-            tok = {g: self.streams[g].record() for g in self.used_gpus}
-            for g in self.used_gpus:
-                for h in self.peer_deps[g]:
-                    self.streams[g].wait(tok[h])
-            for g in self.used_gpus:
-                N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, first, steps,
-                       ctypes.c_void_p(self.resid[g] if residual else 0), 0)
+            # cross-GPU tile counters order everything else — within one
+            # kind of launch (see _run_segments)
+            for f0, n0 in self._run_segments(first, steps):
+                tok = {g: self.streams[g].record() for g in self.used_gpus}
+                for g in self.used_gpus:
+                    for h in self.peer_deps[g]:
+                        self.streams[g].wait(tok[h])
+                for g in self.used_gpus:
+                    N.call("hrt_jacobi_plan_run", self.plans[g], self.streams[g].h, f0, n0,
+                           ctypes.c_void_p(self.resid[g] if residual else 0), 0)
         else:
             prev: dict[int, object] = {}
             for k in range(steps):
@@ -970,8 +1040,11 @@ class JacobiSolver:
             self.resid = {g: rptr} if residual else {}
             self._resid_steps = steps if residual else 0
             self.steps_done = 0
-            N.call("hrt_jacobi_plan_run", self.plans[g], comp.h, 0, steps,
-                   ctypes.c_void_p(rptr if residual else 0), 0)
+            for i, (f0, n0) in enumerate(self._run_segments(0, steps)):
+                if i:
+                    self._segment_fence()
+                N.call("hrt_jacobi_plan_run", self.plans[g], comp.h, f0, n0,
+                       ctypes.c_void_p(rptr if residual else 0), 0)
             self.steps_done = steps
             if after_run is not None:
                 after_run(self)

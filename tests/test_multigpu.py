@@ -121,3 +121,35 @@ def test_uneven_chunks_per_gpu(oracle, dom, grid, ngpus, fuse, monkeypatch):
     ref, rres = oracle.jacobi_c(dom, steps, residual=True)
     assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
     assert np.array_equal(res, rres)
+
+
+@pytest.mark.parametrize("signed", [True, False])
+def test_single_process_volume_two_step(oracle, signed, monkeypatch):
+    """x-band volumes on several GPUs of one process: volume_wave2_kernel
+    reads the other GPU's x planes through tensor maps of its buffers (peer
+    access) and waits on its tile counters; guarded (signed data) and
+    unguarded instances, runs split over launches, a re-upload between
+    jobs; bitwise vs the oracle."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    monkeypatch.setenv("HRT_FUSE2", "2")
+    n = min(ngpu(), 4)
+    dom, grid = (6 * 2 * n, 20, 130), (2 * n, 1, 1)
+    s = JacobiSolver(ChunkGrid(dom, ranks=1, devices_per_rank=n, grid=grid), gpus=list(range(n)))
+    assert len(s.used_gpus) == n and s.persistent and s.steps_per_pass == 2
+    for job in range(2):
+        rng = np.random.default_rng(31 + job)
+        init = rng.random(dom) * 4.0 - (1.0 if signed else 0.0)
+        s.upload(init)
+        for k in (5, 1, 8):
+            s.run(k, residual=False)
+        got = s.download()
+        ref = oracle.jacobi_reference(dom, 14, initial=init)
+        assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (job, np.argwhere(got != ref)[:4])
+    s.upload(init)
+    s.run(13, residual=True)
+    res = s.residual_history()
+    s.close()
+    rr = []
+    oracle.jacobi_reference(dom, 13, initial=init, residuals=rr)
+    assert np.array_equal(res, np.array(rr))
