@@ -3797,7 +3797,12 @@ static int launch_persist(Plan* p, cudaStream_t s, int64_t first, int64_t n,
                           unsigned long long* resid_base) {
     if (n <= 0) return HRT_OK;
     const bool vol = p->L.ndim == 3;
-    if ((vol ? vfuse2_use(p) : fuse2_use(p)) && n >= 4) {
+    // volume single steps and passes keep separate counters: with
+    // neighbours on other devices the caller issues them as separate
+    // launches with a fence between (jacobi.py _run_segments); a mixed run
+    // arriving here anyway runs as single steps
+    const bool mixed_ok = !vol || !p->wave_ipc || n % 4 == 0;
+    if ((vol ? vfuse2_use(p) : fuse2_use(p)) && n >= 4 && mixed_ok) {
         const int64_t nf = (n / 4) * 2, nr = n - 2 * nf;
         int rc = nr ? launch_persist1(p, s, first, nr, resid_base) : HRT_OK;
         if (rc) return rc;
