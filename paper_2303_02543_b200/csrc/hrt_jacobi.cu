@@ -2288,7 +2288,10 @@ __global__ void div6_sweep_kernel(uint64_t seed, int64_t n, int mode,
 #ifndef HRT_VW_MINB
 #define HRT_VW_MINB 3  // resident CTAs per SM the register budget targets
 #endif
-constexpr int VW_CW = 4;              // consumer warps, side by side in z
+#ifndef HRT_VW_CW
+#define HRT_VW_CW 4
+#endif
+constexpr int VW_CW = HRT_VW_CW;      // consumer warps, side by side in z
 #ifndef HRT_VW_R
 #define HRT_VW_R 4
 #endif
