@@ -253,6 +253,16 @@ int hrt_jacobi_plan_set_wave_ipc(void *plan, const int32_t *rpeer4, const int32_
  * index in that rank's plan.  Only row faces qualify; otherwise a no-op. */
 int hrt_jacobi_plan_set_wave2_remote(void *plan, const uint64_t *bufs8, const uint64_t *cnt4,
                                      const int32_t *idx4);
+/* The whole 3 x 3 chunk neighbourhood of every chunk for two-step slab
+ * passes whose neighbours (faces or corners) live on other GPUs or in other
+ * processes — e.g. column faces between ranks (cfg5's y-bands).  Per chunk
+ * (plan order) and position e (row-major NW N NE W C E SW S SE): kind9 0 =
+ * none (domain), 1 = this plan's chunk idx9, 2 = another device's chunk
+ * idx9 (its index in its own plan) with that plan's tile counters cnt9 and
+ * buffers bufs18 (both mapped: peer or CUDA IPC).  A corner must exist
+ * exactly when both faces next to it do. */
+int hrt_jacobi_plan_set_wave2_nbr9(void *plan, const int32_t *kind9, const int32_t *idx9,
+                                   const uint64_t *cnt9, const uint64_t *bufs18);
 /* *on = 1 when runs of >= 4 steps use two-step passes: slab_wave2_kernel
  * (slabs) or volume_wave2_kernel (x-band volumes on one GPU). */
 int hrt_jacobi_plan_two_step(void *plan, int *on);

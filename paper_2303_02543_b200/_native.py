@@ -127,6 +127,8 @@ SIGNATURES = {
     "hrt_jacobi_plan_set_fuse2": (c_int, [c_void_p, c_int]),
     "hrt_jacobi_plan_tiling": (c_int, [c_void_p, P(c_i64), P(c_i64), P(c_int)]),
     "hrt_jacobi_plan_set_wave2_remote": (c_int, [c_void_p, P(c_u64), P(c_u64), P(ctypes.c_int32)]),
+    "hrt_jacobi_plan_set_wave2_nbr9": (c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_int32),
+                                              P(c_u64), P(c_u64)]),
     "hrt_jacobi_plan_set_wave_ipc": (c_int, [c_void_p, P(ctypes.c_int32), P(ctypes.c_int32),
                                              P(c_u64), c_int, c_u64]),
     "hrt_ipc_get_handle": (c_int, [c_void_p, c_char_p]),

@@ -2934,8 +2934,16 @@ struct Plan {
     int64_t n9_key = -1;           // tiles per chunk the table was built for
     // faces to other processes (hrt_jacobi_plan_set_wave2_remote): per chunk
     // and face N,S,W,E the mapped buffers and tile-counter base, or null
-    std::vector<uint64_t> r2buf, r2cnt;
-    std::vector<int64_t> r2idx;
+    // 3 x 3 chunk neighbourhood of the two-step slab passes when some of it
+    // lives on other GPUs or in other processes ([nchunks][9], row-major
+    // NW N NE W C E SW S SE; empty = all local, derived from nbr)
+    struct R9 {
+        int32_t kind;   // 0 none (domain), 1 this plan's chunk idx, 2 another device's
+        int32_t idx;    // plan-local index, or the chunk's index in its own plan
+        uint64_t cnt;   // kind 2: that plan's tile counters (mapped)
+        uint64_t b[2];  // kind 2: its buffers (mapped)
+    };
+    std::vector<R9> r9;
     double* d_ones = nullptr;      // BOUNDARY row (rows outside the domain)
     // two steps per pass for x-band volumes (volume_wave2_kernel)
     std::vector<hrt_vpush_t> h_vpush;  // host copy of the push table (face kinds)
@@ -2958,7 +2966,7 @@ struct Plan {
     int64_t pkey2 = -1;
     bool fuse2_on() const {
         const bool local = !wave_ipc && remote.empty() && !ipc;
-        return fuse2 && persist_on() && L.ndim == 2 && (local || !r2buf.empty()) &&
+        return fuse2 && persist_on() && L.ndim == 2 && (local || !r9.empty()) &&
                L.ext[0] >= 2 && L.ext[1] >= 2 && L.ext[1] % 2 == 0 && rows >= 2 &&
                L.ext[0] % rows != 1 && (int64_t)nbr.size() == 4 * (int64_t)nchunks;
     }
@@ -3469,6 +3477,22 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
         for (int c = 0; c < p->nchunks; ++c) {
             Nbr9& o = n9[c];
             memset(&o, 0, sizeof(o));
+            if (!p->r9.empty()) {  // neighbourhood given, partly on other devices
+                for (int e = 0; e < 9; ++e) {
+                    const Plan::R9& r = p->r9[9 * (size_t)c + e];
+                    if (r.kind == 1) {
+                        o.b[e][0] = p->h_chunks[r.idx].b[0];
+                        o.b[e][1] = p->h_chunks[r.idx].b[1];
+                        o.cnt[e] = p->d_pdone + (int64_t)r.idx * per_chunk;
+                    } else if (r.kind == 2) {
+                        o.b[e][0] = reinterpret_cast<double*>(r.b[0]);
+                        o.b[e][1] = reinterpret_cast<double*>(r.b[1]);
+                        o.cnt[e] = reinterpret_cast<unsigned int*>(r.cnt) + (int64_t)r.idx * per_chunk;
+                        o.sysmask |= 1u << e;
+                    }
+                }
+                continue;
+            }
             const int n = at(c, 0), so = at(c, 1);
             const int idx[9] = {at(n, 2), n, at(n, 3), at(c, 2), c, at(c, 3),
                                 at(so, 2), so, at(so, 3)};
@@ -3477,18 +3501,6 @@ static int launch_fused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
                 o.b[e][0] = p->h_chunks[idx[e]].b[0];
                 o.b[e][1] = p->h_chunks[idx[e]].b[1];
                 o.cnt[e] = p->d_pdone + (int64_t)idx[e] * per_chunk;
-            }
-            if (!p->r2buf.empty()) {  // faces to other processes (N, S, W, E)
-                const int pos[4] = {1, 7, 3, 5};
-                for (int f = 0; f < 4; ++f) {
-                    const size_t k = 4 * (size_t)c + f;
-                    if (!p->r2cnt[k]) continue;
-                    o.b[pos[f]][0] = reinterpret_cast<double*>(p->r2buf[2 * k]);
-                    o.b[pos[f]][1] = reinterpret_cast<double*>(p->r2buf[2 * k + 1]);
-                    o.cnt[pos[f]] = reinterpret_cast<unsigned int*>(p->r2cnt[k]) +
-                                    p->r2idx[k] * per_chunk;
-                    o.sysmask |= 1u << pos[f];
-                }
             }
         }
         cudaFree(p->d_n9);
@@ -4236,20 +4248,70 @@ int hrt_jacobi_plan_set_wave2_remote(void* plan, const uint64_t* bufs8, const ui
     Plan* p = reinterpret_cast<Plan*>(plan);
     HRT_CHECK_ARG((int64_t)p->nbr.size() == 4 * (int64_t)p->nchunks && p->L.ndim == 2,
                   "set the slab plan persistent first");
-    p->r2buf.clear();
-    p->r2cnt.clear();
-    p->r2idx.clear();
+    p->r9.clear();
     cudaFree(p->d_n9);
     p->d_n9 = nullptr;
     for (int c = 0; c < p->nchunks; ++c) {
         const uint64_t* k = cnt4 + 4 * (size_t)c;
-        if (k[2] || k[3]) return HRT_OK;  // column faces to another process
+        if (k[2] || k[3]) return HRT_OK;  // column faces: use hrt_jacobi_plan_set_wave2_nbr9
         if ((k[0] || k[1]) && (p->nbr[4 * (size_t)c + 2] >= 0 || p->nbr[4 * (size_t)c + 3] >= 0))
-            return HRT_OK;  // diagonal chunks would live in another process
+            return HRT_OK;  // diagonal chunks on another device: likewise
     }
-    p->r2buf.assign(bufs8, bufs8 + 8 * (size_t)p->nchunks);
-    p->r2cnt.assign(cnt4, cnt4 + 4 * (size_t)p->nchunks);
-    p->r2idx.assign(idx4, idx4 + 4 * (size_t)p->nchunks);
+    // row faces only: the N / S positions from the table, the rest local
+    auto at = [&](int c, int f) { return c < 0 ? -1 : p->nbr[4 * (size_t)c + f]; };
+    p->r9.assign(9 * (size_t)p->nchunks, Plan::R9{0, -1, 0, {0, 0}});
+    for (int c = 0; c < p->nchunks; ++c) {
+        const int n = at(c, 0), so = at(c, 1);
+        const int idx[9] = {at(n, 2), n, at(n, 3), at(c, 2), c, at(c, 3),
+                            at(so, 2), so, at(so, 3)};
+        for (int e = 0; e < 9; ++e)
+            if (idx[e] >= 0) p->r9[9 * (size_t)c + e] = Plan::R9{1, idx[e], 0, {0, 0}};
+        const int pos[2] = {1, 7};
+        for (int f = 0; f < 2; ++f) {
+            const size_t k = 4 * (size_t)c + f;
+            if (!cnt4[k]) continue;
+            p->r9[9 * (size_t)c + pos[f]] =
+                Plan::R9{2, idx4[k], cnt4[k], {bufs8[2 * k], bufs8[2 * k + 1]}};
+        }
+    }
+    return HRT_OK;
+}
+
+int hrt_jacobi_plan_set_wave2_nbr9(void* plan, const int32_t* kind9, const int32_t* idx9,
+                                   const uint64_t* cnt9, const uint64_t* bufs18) {
+    HRT_CHECK_ARG(plan && kind9 && idx9 && cnt9 && bufs18, "null argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    HRT_CHECK_ARG((int64_t)p->nbr.size() == 4 * (int64_t)p->nchunks && p->L.ndim == 2,
+                  "set the slab plan persistent first");
+    int rc = use_device(p->gpu);
+    if (rc) return rc;
+    HRT_CUDA(cudaDeviceSynchronize());  // no launch reads the old table
+    std::vector<Plan::R9> t(9 * (size_t)p->nchunks);
+    for (int c = 0; c < p->nchunks; ++c)
+        for (int e = 0; e < 9; ++e) {
+            const size_t k = 9 * (size_t)c + e;
+            Plan::R9& r = t[k];
+            r.kind = kind9[k];
+            r.idx = idx9[k];
+            r.cnt = cnt9[k];
+            r.b[0] = bufs18[2 * k];
+            r.b[1] = bufs18[2 * k + 1];
+            HRT_CHECK_ARG(r.kind >= 0 && r.kind <= 2, "bad neighbour kind");
+            HRT_CHECK_ARG(r.kind != 1 || (r.idx >= 0 && r.idx < p->nchunks), "bad local index");
+            HRT_CHECK_ARG(r.kind != 2 || (r.idx >= 0 && r.cnt && r.b[0] && r.b[1]),
+                          "remote neighbour without buffers or counters");
+            HRT_CHECK_ARG(e != 4 || (r.kind == 1 && r.idx == c), "position 4 is the chunk itself");
+        }
+    // a corner exists exactly when both faces next to it do (regular grid)
+    for (int c = 0; c < p->nchunks; ++c) {
+        auto has = [&](int e) { return t[9 * (size_t)c + e].kind != 0; };
+        const int corner[4][3] = {{0, 1, 3}, {2, 1, 5}, {6, 7, 3}, {8, 7, 5}};
+        for (const auto& q : corner)
+            HRT_CHECK_ARG(has(q[0]) == (has(q[1]) && has(q[2])), "inconsistent 3x3 neighbourhood");
+    }
+    p->r9 = std::move(t);
+    cudaFree(p->d_n9);
+    p->d_n9 = nullptr;
     return HRT_OK;
 }
 

@@ -138,6 +138,16 @@ class DistributedJacobi(JacobiSolver):
             mapped_pool[q] = (pp.value, base_q)
             mapped_flags[q] = pf.value
             self._ipc_maps += [pp.value, pf.value]
+        # ranks holding only corner chunks of this rank's 3 x 3 neighbourhoods
+        # (two-step passes read their rims too): arenas mapped, no flags
+        diag_ranks = sorted({self.rank_of[q] for lin in mine for q in self.grid.nbhd9(lin)
+                             if q is not None and q not in self.placement} - set(nbr_ranks))
+        for q in diag_ranks:
+            _, hp, base_q = every[q][:3]
+            pp = ctypes.c_void_p()
+            N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(hp, 64), ctypes.byref(pp))
+            mapped_pool[q] = (pp.value, base_q)
+            self._ipc_maps.append(pp.value)
 
         def remote_buf(nb: int, p: int) -> int:
             q = self.rank_of[nb]
@@ -180,7 +190,7 @@ class DistributedJacobi(JacobiSolver):
                ctypes.c_uint64(30_000_000_000))
         self.ipc = True
         if os.environ.get("HRT_PERSIST", "1") != "0":
-            self._setup_wave_ipc(g, mine, nbr_ranks, remote_buf)
+            self._setup_wave_ipc(g, mine, nbr_ranks, remote_buf, diag_ranks)
         dist.barrier()
 
     def _setup_ipc3(self, gpu: int) -> None:
@@ -220,7 +230,8 @@ class DistributedJacobi(JacobiSolver):
         self._setup_wave_ipc(g, mine, nbr_ranks, remote_buf)
         dist.barrier()
 
-    def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list, remote_buf=None) -> None:
+    def _setup_wave_ipc(self, g: int, mine: list, nbr_ranks: list, remote_buf=None,
+                        diag_ranks=()) -> None:
         """Persistent wavefront across processes: every rank exports its
         per-tile step counters over CUDA IPC; an edge tile waits on the
         neighbour rank's adjacent tile counter (system scope) instead of a
@@ -249,7 +260,8 @@ class DistributedJacobi(JacobiSolver):
         if len({t for _, t in every}) != 1:
             raise HrtError(f"per-chunk tilings differ across ranks: {[t for _, t in every]}")
         peer_ptrs = []
-        for q in nbr_ranks:
+        all_ranks = list(nbr_ranks) + list(diag_ranks)  # face ranks first (rpeer indexes them)
+        for q in all_ranks:
             pq = ctypes.c_void_p()
             N.call("hrt_ipc_open_handle", g, ctypes.create_string_buffer(every[q][0], 64),
                    ctypes.byref(pq))
@@ -270,22 +282,31 @@ class DistributedJacobi(JacobiSolver):
                _arr(ctypes.c_int32, rnbr), _arr(ctypes.c_uint64, peer_ptrs), len(peer_ptrs),
                ctypes.c_uint64(30_000_000_000))
         if remote_buf is not None and nf == 4:
-            # two steps per pass read the neighbour rank's rim rows in place
-            bufs, cnts, idxs = [], [], []
-            for k, lin in enumerate(mine):
-                for f in range(4):
-                    p = rpeer[4 * k + f]
-                    nb = self.grid.chunks[lin].neighbors.get(f)
-                    if p < 0:
-                        bufs += [0, 0]
-                        cnts.append(0)
+            # two steps per pass read the rims of the whole 3 x 3 chunk
+            # neighbourhood in place: faces and corners on other ranks
+            # through their IPC-mapped arenas and tile counters
+            kinds, idxs, cnts, bufs = [], [], [], []
+            for lin in mine:
+                for q in self.grid.nbhd9(lin):
+                    if q is None:
+                        kinds.append(0)
                         idxs.append(-1)
+                        cnts.append(0)
+                        bufs += [0, 0]
+                    elif q in self.placement:
+                        kinds.append(1)
+                        idxs.append(index[q])
+                        cnts.append(0)
+                        bufs += [0, 0]
                     else:
-                        bufs += [remote_buf(nb, 0), remote_buf(nb, 1)]
-                        cnts.append(peer_ptrs[p])
-                        idxs.append(rnbr[4 * k + f])
-            N.call("hrt_jacobi_plan_set_wave2_remote", plan, _arr(ctypes.c_uint64, bufs),
-                   _arr(ctypes.c_uint64, cnts), _arr(ctypes.c_int32, idxs))
+                        r = self.rank_of[q]
+                        kinds.append(2)
+                        idxs.append(list(self.grid.per_rank[r]).index(q))
+                        cnts.append(peer_ptrs[all_ranks.index(r)])
+                        bufs += [remote_buf(q, 0), remote_buf(q, 1)]
+            N.call("hrt_jacobi_plan_set_wave2_nbr9", plan, _arr(ctypes.c_int32, kinds),
+                   _arr(ctypes.c_int32, idxs), _arr(ctypes.c_uint64, cnts),
+                   _arr(ctypes.c_uint64, bufs))
         if remote_buf is not None and nf == 6:
             # volume two-step passes read the neighbour rank's x planes in
             # place and wait on its tile counters (both mapped over IPC)

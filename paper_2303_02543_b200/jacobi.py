@@ -110,6 +110,15 @@ class ChunkGrid:
     def slab(self) -> bool:
         return self.domain[2] == 1
 
+    def nbhd9(self, lin: int) -> list:
+        """The 3 x 3 chunk neighbourhood in the x-y plane, row-major
+        NW N NE W C E SW S SE (N/S = faces 0/1 along x, W/E = faces 2/3
+        along y); None where the domain ends."""
+        def nb(q, f):
+            return None if q is None else self.chunks[q].neighbors.get(f)
+        n, s = nb(lin, 0), nb(lin, 1)
+        return [nb(n, 2), n, nb(n, 3), nb(lin, 2), lin, nb(lin, 3), nb(s, 2), s, nb(s, 3)]
+
     def domain_face_mask(self, ch: Chunk) -> int:
         m = 0
         for f in range(6):
@@ -725,24 +734,32 @@ class JacobiSolver:
                    _arr(ctypes.c_int32, rnbr), _arr(ctypes.c_uint64, [counters[h] for h in peers]),
                    len(peers), ctypes.c_uint64(30_000_000_000))
             if nf == 4:
-                # two-step passes read the other GPU's rim rows in place (peer)
-                bufs, cnts, idxs = [], [], []
-                for k, lin in enumerate(mine[g]):
-                    for f in range(4):
-                        nb = self.grid.chunks[lin].neighbors.get(f)
-                        h = self.placement.get(nb) if nb is not None else None
-                        if h is None or h == g:
-                            bufs += [0, 0]
-                            cnts.append(0)
+                # two-step passes read the rims of the whole 3 x 3 chunk
+                # neighbourhood in place, faces and corners on other GPUs
+                # through peer pointers
+                kinds, idxs, cnts, bufs = [], [], [], []
+                for lin in mine[g]:
+                    for q in self.grid.nbhd9(lin):
+                        h = self.placement.get(q) if q is not None else None
+                        if h is None:
+                            kinds.append(0)
                             idxs.append(-1)
+                            cnts.append(0)
+                            bufs += [0, 0]
+                        elif h == g:
+                            kinds.append(1)
+                            idxs.append(index[g][q])
+                            cnts.append(0)
+                            bufs += [0, 0]
                         else:
                             N.call("hrt_enable_peer_access", g, h)
-                            bufs += list(self.bufs[nb])
+                            kinds.append(2)
+                            idxs.append(index[h][q])
                             cnts.append(counters[h])
-                            idxs.append(index[h][nb])
-                N.call("hrt_jacobi_plan_set_wave2_remote", self.plans[g],
-                       _arr(ctypes.c_uint64, bufs), _arr(ctypes.c_uint64, cnts),
-                       _arr(ctypes.c_int32, idxs))
+                            bufs += list(self.bufs[q])
+                N.call("hrt_jacobi_plan_set_wave2_nbr9", self.plans[g],
+                       _arr(ctypes.c_int32, kinds), _arr(ctypes.c_int32, idxs),
+                       _arr(ctypes.c_uint64, cnts), _arr(ctypes.c_uint64, bufs))
             if nf == 6:
                 # volume two-step passes: the other GPU's x planes through
                 # tensor maps of its buffers, its tile counters (peer)

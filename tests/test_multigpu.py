@@ -153,3 +153,26 @@ def test_single_process_volume_two_step(oracle, signed, monkeypatch):
     rr = []
     oracle.jacobi_reference(dom, 13, initial=init, residuals=rr)
     assert np.array_equal(res, np.array(rr))
+
+
+@pytest.mark.parametrize("dom,grid", [((300, 700, 1), (3, 7, 1)),     # staircase: corners on other GPUs
+                                      ((64, 256, 1), (2, 8, 1))])      # y-bands: column faces
+def test_single_process_slab_two_step_nbr9(oracle, dom, grid, monkeypatch):
+    """Two-step slab passes on several GPUs of one process where faces AND
+    corners of the 3 x 3 chunk neighbourhood live on other GPUs (peer
+    pointers through hrt_jacobi_plan_set_wave2_nbr9): random signed data,
+    runs split over launches, bitwise vs the oracle."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    monkeypatch.setenv("HRT_FUSE2", "2")
+    n = min(ngpu(), 4)
+    s = JacobiSolver(ChunkGrid(dom, ranks=1, devices_per_rank=n, grid=grid), gpus=list(range(n)))
+    assert s.persistent and s.steps_per_pass == 2
+    init = np.random.default_rng(5).random(dom) * 4.0 - 1.0
+    s.upload(init)
+    for k in (5, 8):
+        s.run(k, residual=False)
+    got = s.download()
+    s.close()
+    ref = oracle.jacobi_reference(dom, 13, initial=init)
+    assert np.array_equal(got, ref), np.argwhere(got != ref)[:4]
