@@ -2324,6 +2324,12 @@ struct VolW2Args {
     const CUtensorMap* maps;   // [nchunks][2] tensor map of buffer 0 / 1
     const ChunkBufs* chunks;
     const VW2Nbr* nbr;         // [nchunks]
+    // chains: maximal runs of this plan's chunks linked along +x; a tile is
+    // (chain, y block, z block) and streams every plane of its chain
+    const int2* chains;        // [nchains] (offset into clist, length)
+    const int* clist;          // chunk indices in +x order, chain after chain
+    int64_t cdelta;            // output pointer step at a chunk boundary of a chain:
+                               // (next chunk's buffer - this one's) - ex * sx
     unsigned int* done;        // [T] steps completed per tile (absolute: base at launch)
     unsigned int base;
     unsigned long long* ticket;
@@ -2362,27 +2368,38 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
         : "memory");
 }
 
-// planes -1 .. ex+2 of tile (c, j0, k0) into the ring, one tensor copy each
+// planes -1 .. m*ex+2 of tile (chain, j0, k0) into the ring, one tensor
+// copy each: the chain's chunks in turn, the first and last two from the
+// x neighbours of its end chunks (in place) or their own ghost planes
 __device__ __forceinline__ void vw2_produce(const VolW2Args& a, uint32_t ring, uint64_t* full,
-                                            uint64_t* empty, int& s, uint32_t& ph, int64_t c,
+                                            uint64_t* empty, int& s, uint32_t& ph, int2 ch,
                                             int64_t j0, int64_t k0, int parity) {
-    const VW2Nbr& nb = a.nbr[c];
-    const CUtensorMap* own = a.maps + 2 * c + parity;
-    const CUtensorMap* mm = nb.map[0][parity];
-    const CUtensorMap* pm = nb.map[1][parity];
+    const int* cl = a.clist + ch.x;
+    const int cf = cl[0], cz = cl[ch.y - 1];
+    const CUtensorMap* mm = a.nbr[cf].map[0][parity];
+    const CUtensorMap* pm = a.nbr[cz].map[1][parity];
     const int c0 = (int)(a.origin + k0 - 2), c1 = (int)(j0 - 2);
     const int ex = (int)a.ex;
-    const int nplanes = ex + 4;
+    const int nx = ex * ch.y;  // planes of the chain
+    const int nplanes = nx + 4;
+    int j = 0, ii0 = 0;  // chunk of the chain and its plane, for planes 1 .. nx
     for (int q = 0; q < nplanes; ++q) {
-        const int i = q - 1;  // plane; neighbour planes in place, domain ghosts from own buffer
-        const CUtensorMap* m = own;
-        int ii = i;
-        if (i < 1 && mm) {
-            m = mm;
-            ii = i + ex;
-        } else if (i > ex && pm) {
-            m = pm;
-            ii = i - ex;
+        const int i = q - 1;  // plane of the chain
+        const CUtensorMap* m;
+        int ii;
+        if (i < 1) {
+            m = mm ? mm : a.maps + 2 * cf + parity;
+            ii = mm ? i + ex : i;
+        } else if (i > nx) {
+            m = pm ? pm : a.maps + 2 * cz + parity;
+            ii = pm ? i - nx : i - (nx - ex);
+        } else {
+            if (++ii0 > ex) {
+                ii0 = 1;
+                ++j;
+            }
+            m = a.maps + 2 * cl[j] + parity;
+            ii = ii0;
         }
         mbar_wait_sleep(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], VW_STAGE_BYTES);
@@ -2407,10 +2424,22 @@ struct VW2Ctx {
     unsigned vrow;        // bit r: ring row r (0..7) inside the domain rows
     bool colok;           // this lane's column is inside the domain
     bool own;             // lane 1..30 with an inside column: stores + residuals
-    int64_t ex, sx, sy;
+    int64_t ex, sx, sy;   // ex: planes of the chain
     double* wr;           // plane 1, row j0, this column, buffer parity^1
+    int rem, cex;         // output planes left in the current chunk / per chunk
+    int64_t cdelta;       // see VolW2Args
     double r1, r2;
 };
+
+// next output plane: within a chunk one x stride, across a chain's chunk
+// boundary the step to the next chunk's buffer
+__device__ __forceinline__ void vw2_next_plane(VW2Ctx& x) {
+    x.wr += x.sx;
+    if (--x.rem == 0) {
+        x.wr += x.cdelta;
+        x.rem = x.cex;
+    }
+}
 
 template <int NP>
 __device__ __forceinline__ void vw2_take(VW2Ctx& x, double (&v)[NP], int& st) {
@@ -2536,7 +2565,7 @@ __device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
                 if (x.own) x.r2 = dmax(x.r2, d);
             }
         }
-        x.wr += x.sx;
+        vw2_next_plane(x);
     }
     vw2_poll(x);
 }
@@ -2612,15 +2641,16 @@ __device__ __forceinline__ void vw2_step_fast(VW2Ctx& x, const double (&up)[VW_R
         x.r1 = dmax(x.r1, e1[0]);
         if (x.own) x.r2 = dmax(x.r2, e2[0]);
     }
-    x.wr += x.sx;
+    vw2_next_plane(x);
     vw2_poll(x);
 }
 
 template <bool GUARD, bool RESID>
 __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u32,
                                             uint32_t full_u32, uint32_t empty_u32, int& s,
-                                            uint32_t& ph, int64_t c, int64_t j0, int64_t k0,
+                                            uint32_t& ph, int2 ch, int64_t j0, int64_t k0,
                                             int parity, double& r1, double& r2) {
+    const int cf = a.clist[ch.x], cz = a.clist[ch.x + ch.y - 1];
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     VW2Ctx x;
@@ -2633,11 +2663,14 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     const int pc = 1 + VW_ZO * warp + x.lane;  // ring column of k
     const int64_t k = k0 - 2 + pc;
     x.ring = ring_u32 + 8u * (uint32_t)pc;
-    x.ex = a.ex;
+    x.ex = a.ex * ch.y;
     x.sx = a.sx;
     x.sy = a.sy;
-    x.xlo = a.nbr[c].map[0][0] == nullptr;
-    x.xhi = a.nbr[c].map[1][0] == nullptr;
+    x.rem = (int)a.ex;
+    x.cex = (int)a.ex;
+    x.cdelta = a.cdelta;
+    x.xlo = a.nbr[cf].map[0][0] == nullptr;
+    x.xhi = a.nbr[cz].map[1][0] == nullptr;
     unsigned vrow = 0;
 #pragma unroll
     for (int r = 0; r < VW_RR; ++r) {
@@ -2648,10 +2681,10 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     x.colok = k >= 1 && k <= a.ez;
     x.own = x.lane >= 1 && x.lane <= VW_ZO && x.colok;
     x.tmask = __any_sync(0xffffffffu, !x.colok) || vrow != (1u << VW_RR) - 1u;
-    x.wr = a.chunks[c].b[parity ^ 1] + a.origin + a.sx + j0 * a.sy + k;
+    x.wr = a.chunks[cf].b[parity ^ 1] + a.origin + a.sx + j0 * a.sy + k;
     x.r1 = r1;
     x.r2 = r2;
-    const int nplanes = (int)(a.ex + 4);
+    const int nplanes = (int)(x.ex + 4);
 
     double t0[VW_RR], t1[VW_RR], t2[VW_RR];           // u(t) planes, rotating
     double y0[VW_R + 2], y1[VW_R + 2], y2[VW_R + 2];  // u(t+1) planes, rotating
@@ -2664,7 +2697,7 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, 3);
     int q = 4;
     if (!x.tmask)  // planes 2 .. ex: nothing outside the domain
-        for (; q + 2 <= (int)a.ex + 2; q += 3) {
+        for (; q + 2 <= (int)x.ex + 2; q += 3) {
             vw2_step_fast<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2);
             vw2_step_fast<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0);
             vw2_step_fast<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1);
@@ -2751,18 +2784,24 @@ volume_wave2_kernel(VolW2Args wa) {
             if (t >= total) break;
             const int k = (int)(t / T);
             const int64_t tile = t - (long long)k * T;
-            const int64_t c = tile / per_chunk;
-            const int64_t rem = tile - c * per_chunk;
+            const int64_t h = tile / per_chunk;  // chain
+            const int64_t rem = tile - h * per_chunk;
             const int64_t yb = rem / tk;
             const int64_t zb = rem - yb * tk;
+            const int2 ch = wa.chains[h];
             if (!dead) {
-                // the 3 x 3 x 3 tile neighbourhood must be done with step 2k
+                // the 3 x 3 x 3 tile neighbourhood must be done with step 2k:
+                // y / z blocks +-1 of this chain (every chunk of a chain
+                // publishes together: its first chunk's counters stand for
+                // all) and of the x neighbours of its end chunks
                 const unsigned need = wa.base + 2u * (unsigned)k;
                 const unsigned int* q[27];
                 bool sys[27];
-                const VW2Nbr& nb = wa.nbr[c];
-                const unsigned int* cx[3] = {nb.cnt[0], wa.done + c * per_chunk, nb.cnt[1]};
-                const bool sx[3] = {(nb.sys & 1u) != 0, false, (nb.sys & 2u) != 0};
+                const int cf = wa.clist[ch.x], cz = wa.clist[ch.x + ch.y - 1];
+                const unsigned int* cx[3] = {wa.nbr[cf].cnt[0], wa.done + cf * per_chunk,
+                                             wa.nbr[cz].cnt[1]};
+                const bool sx[3] = {(wa.nbr[cf].sys & 1u) != 0, false,
+                                    (wa.nbr[cz].sys & 2u) != 0};
 #pragma unroll
                 for (int d = 0; d < 27; ++d) {
                     const unsigned int* cc = cx[d / 9];
@@ -2774,7 +2813,7 @@ volume_wave2_kernel(VolW2Args wa) {
                 dead = !wait_counters<27>(q, sys, need, wa.timeout_ns, wa.err);
                 asm volatile("fence.proxy.async.global;" ::: "memory");
             }
-            vw2_produce(wa, ring_u32, full, empty, s, ph, c, 1 + yb * VW_R, 1 + zb * VW_TZ,
+            vw2_produce(wa, ring_u32, full, empty, s, ph, ch, 1 + yb * VW_R, 1 + zb * VW_TZ,
                         (wa.parity0 + k) & 1);
         }
         return;
@@ -2794,12 +2833,13 @@ volume_wave2_kernel(VolW2Args wa) {
         if (t < 0) break;
         const int k = (int)(t / T);
         const int64_t tile = t - (long long)k * T;
-        const int64_t c = tile / per_chunk;
-        const int64_t rem = tile - c * per_chunk;
+        const int64_t h = tile / per_chunk;
+        const int64_t rem = tile - h * per_chunk;
         const int64_t yb = rem / tk;
         const int64_t zb = rem - yb * tk;
+        const int2 ch = wa.chains[h];
         double r1 = 0.0, r2 = 0.0;
-        vw2_consume<!FAST, RESID>(wa, ring_u32, full_u32, empty_u32, s, ph, c, 1 + yb * VW_R,
+        vw2_consume<!FAST, RESID>(wa, ring_u32, full_u32, empty_u32, s, ph, ch, 1 + yb * VW_R,
                                   1 + zb * VW_TZ, (wa.parity0 + k) & 1, r1, r2);
         if (RESID && wa.resid) {
             r1 = warp_max(r1);
@@ -2809,9 +2849,9 @@ volume_wave2_kernel(VolW2Args wa) {
                 red[1][warp] = r2;
             }
         }
-        // every tile of a chunk with a neighbour in another process is read
-        // by it (a tile spans all planes): stores visible system-wide first
-        const bool xsys = wa.nbr[c].sys != 0;
+        // a chain whose end chunk faces another device is read by it (a tile
+        // spans all planes): stores visible system-wide first
+        const bool xsys = (wa.nbr[wa.clist[ch.x]].sys | wa.nbr[wa.clist[ch.x + ch.y - 1]].sys) != 0;
         asm volatile("fence.proxy.async.global;" ::: "memory");
         if (xsys) __threadfence_system();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * VW_CW));
@@ -2826,14 +2866,16 @@ volume_wave2_kernel(VolW2Args wa) {
                 resid_max(wa.resid + 2 * k, m1);
                 resid_max(wa.resid + 2 * k + 1, m2);
             }
+            // the tile's (y, z) block of every chunk of the chain
             const unsigned v = wa.base + 2u * (unsigned)k + 2u;
-            if (xsys) {
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(wa.done + tile), "r"(v)
-                             : "memory");
-            } else {
-                __threadfence();
-                st_release_gpu_u32(wa.done + tile, v);
+            if (xsys) __threadfence_system();
+            else __threadfence();
+            for (int j = 0; j < ch.y; ++j) {
+                unsigned int* d = wa.done + wa.clist[ch.x + j] * per_chunk + rem;
+                if (xsys)
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d), "r"(v) : "memory");
+                else
+                    st_release_gpu_u32(d, v);
             }
         }
     }
@@ -2950,6 +2992,10 @@ struct Plan {
     unsigned int* d_v2done = nullptr;  // per-tile step counters (absolute; IPC-exported)
     unsigned int v2base = 0;           // every d_v2done entry between launches
     VW2Nbr* d_v2nbr = nullptr;         // [nchunks] x-neighbour table
+    int2* d_v2chains = nullptr;        // chains of chunks linked along +x
+    int* d_v2clist = nullptr;
+    int v2nchains = 0;
+    int64_t v2cdelta = 0;
     bool v2dirty = true;               // maps / table to (re)build
     CUtensorMap* d_v2maps = nullptr;   // own [nchunks][2], then remote [nchunks][2 faces][2]
     // x faces to another process (hrt_jacobi_plan_set_vw2_remote): mapped
@@ -3716,6 +3762,63 @@ static int build_vw2_nbr(Plan* p) {
     p->d_v2nbr = nullptr;
     HRT_CUDA(cudaMalloc(&p->d_v2nbr, sizeof(VW2Nbr) * t.size()));
     HRT_CUDA(cudaMemcpy(p->d_v2nbr, t.data(), sizeof(VW2Nbr) * t.size(), cudaMemcpyHostToDevice));
+    // chains: from each chunk without a -x neighbour in this plan, follow
+    // the +x neighbours.  A tile streams a whole chain (no rim planes and
+    // no tile start-up between its chunks: 32-plane chunks ran at 315
+    // GLUPS one by one vs 526 for 128-plane ones); the output pointer steps
+    // from chunk to chunk by one constant, so chains need equally spaced
+    // buffers (the solver allocates them in order) — else single chunks
+    std::vector<std::vector<int>> chains;
+    std::vector<char> seen((size_t)p->nchunks, 0);
+    for (int c = 0; c < p->nchunks; ++c) {
+        if (p->nbr[6 * (size_t)c] >= 0) continue;
+        std::vector<int> ch;
+        for (int x = c; x >= 0 && !seen[x]; x = p->nbr[6 * (size_t)x + 1]) {
+            seen[x] = 1;
+            ch.push_back(x);
+        }
+        chains.push_back(ch);
+    }
+    for (int c = 0; c < p->nchunks; ++c)
+        if (!seen[c]) chains.push_back({c});  // (a cycle cannot occur; defensive)
+    const hrt_chunk_layout_t& L = p->L;
+    int64_t cstride = 0;
+    bool uniform = true;
+    for (const auto& ch : chains)
+        for (size_t j = 0; j + 1 < ch.size(); ++j)
+            for (int par = 0; par < 2; ++par) {
+                const int64_t d = (reinterpret_cast<intptr_t>(p->h_chunks[ch[j + 1]].b[par]) -
+                                   reinterpret_cast<intptr_t>(p->h_chunks[ch[j]].b[par]));
+                if (d % 8 != 0 || (cstride != 0 && d != cstride)) uniform = false;
+                cstride = d;
+            }
+    if (!uniform) {
+        std::vector<std::vector<int>> single;
+        for (const auto& ch : chains)
+            for (int c : ch) single.push_back({c});
+        chains.swap(single);
+        cstride = 0;
+    }
+    std::vector<int2> ctab;
+    std::vector<int> clist;
+    for (const auto& ch : chains) {
+        ctab.push_back(make_int2((int)clist.size(), (int)ch.size()));
+        clist.insert(clist.end(), ch.begin(), ch.end());
+    }
+    p->v2nchains = (int)ctab.size();
+    p->v2cdelta = cstride / 8 - L.ext[0] * L.stride[0];
+    cudaFree(p->d_v2chains);
+    cudaFree(p->d_v2clist);
+    p->d_v2chains = nullptr;
+    p->d_v2clist = nullptr;
+    HRT_CUDA(cudaMalloc(&p->d_v2chains, sizeof(int2) * std::max<size_t>(1, ctab.size())));
+    HRT_CUDA(cudaMalloc(&p->d_v2clist, sizeof(int) * std::max<size_t>(1, clist.size())));
+    if (!ctab.empty()) {
+        HRT_CUDA(cudaMemcpy(p->d_v2chains, ctab.data(), sizeof(int2) * ctab.size(),
+                            cudaMemcpyHostToDevice));
+        HRT_CUDA(cudaMemcpy(p->d_v2clist, clist.data(), sizeof(int) * clist.size(),
+                            cudaMemcpyHostToDevice));
+    }
     return HRT_OK;
 }
 
@@ -3732,8 +3835,7 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     if (nf <= 0) return HRT_OK;
     const hrt_chunk_layout_t& L = p->L;
     int64_t tj = 0, tk = 0;
-    const int64_t T = vw2_tiles(p, &tj, &tk);
-    if (T == 0) return HRT_OK;
+    if (vw2_tiles(p, &tj, &tk) == 0) return HRT_OK;
     int rc = ensure_vw2_counters(p);
     if (rc) return rc;
     if (p->v2dirty) {
@@ -3744,6 +3846,7 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
         if (rc) return rc;
         p->v2dirty = false;
     }
+    const int64_t T = (int64_t)p->v2nchains * tj * tk;  // tiles: (chain, y block, z block)
     if (!p->d_range) {  // never scanned: "unknown" (guarded division)
         HRT_CUDA(cudaMalloc(&p->d_range, 2 * sizeof(unsigned long long)));
         const unsigned long long h[2] = {0ull, 1ull};
@@ -3769,6 +3872,9 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     VolW2Args wa{};
     wa.chunks = p->d_chunks;
     wa.nbr = p->d_v2nbr;
+    wa.chains = p->d_v2chains;
+    wa.clist = p->d_v2clist;
+    wa.cdelta = p->v2cdelta;
     wa.done = p->d_v2done;
     wa.base = p->v2base;
     wa.ticket = p->d_pticket;
@@ -4717,6 +4823,8 @@ int hrt_jacobi_plan_destroy(void* plan) {
     cudaFree(p->d_ones);
     cudaFree(p->d_v2done);
     cudaFree(p->d_v2nbr);
+    cudaFree(p->d_v2chains);
+    cudaFree(p->d_v2clist);
     cudaFree(p->d_v2maps);
     cudaFree(p->d_range);
     if (p->side) cudaStreamDestroy(p->side);
