@@ -2424,20 +2424,22 @@ struct VW2Ctx {
     unsigned vrow;        // bit r: ring row r (0..7) inside the domain rows
     bool colok;           // this lane's column is inside the domain
     bool own;             // lane 1..30 with an inside column: stores + residuals
-    int64_t ex, sx, sy;   // ex: planes of the chain
+    int64_t ex;           // planes of the chain
     double* wr;           // plane 1, row j0, this column, buffer parity^1
-    int rem, cex;         // output planes left in the current chunk / per chunk
-    int64_t cdelta;       // see VolW2Args
+    int rem;              // output planes left in the current chunk
     double r1, r2;
 };
 
 // next output plane: within a chunk one x stride, across a chain's chunk
-// boundary the step to the next chunk's buffer
-__device__ __forceinline__ void vw2_next_plane(VW2Ctx& x) {
-    x.wr += x.sx;
-    if (--x.rem == 0) {
-        x.wr += x.cdelta;
-        x.rem = x.cex;
+// boundary the step to the next chunk's buffer (strides and extents come
+// from the kernel parameters, not registers: the consumer runs at the
+// register limit)
+template <bool CHAIN>
+__device__ __forceinline__ void vw2_next_plane(VW2Ctx& x, const VolW2Args& a) {
+    x.wr += a.sx;
+    if (CHAIN && --x.rem == 0) {
+        x.wr += a.cdelta;
+        x.rem = (int)a.ex;
     }
 }
 
@@ -2471,8 +2473,8 @@ __device__ __forceinline__ void vw2_release(VW2Ctx& x, int st) {
 // one pipeline step q (ring plane q = u(t) plane i = q-1 arrives as dn):
 // u(t+1) at plane q-2 (ring rows 1..6) -> u1n; u(t+2) at plane q-3 from
 // u(t+1) planes q-4 (u1a), q-3 (u1b), q-2 (u1n), stored.
-template <bool GUARD, bool RESID>
-__device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
+template <bool GUARD, bool RESID, bool CHAIN>
+__device__ __forceinline__ void vw2_step(VW2Ctx& x, const VolW2Args& a, const double (&up)[VW_RR],
                                          const double (&mid)[VW_RR], double (&dn)[VW_RR],
                                          int& smid, const double (&u1a)[VW_R + 2],
                                          const double (&u1b)[VW_R + 2], double (&u1n)[VW_R + 2],
@@ -2548,7 +2550,7 @@ __device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
 #pragma unroll
                 for (int m = 0; m < VW_R; ++m)
                     if ((x.vrow >> (m + 2)) & 1u) {
-                        x.wr[m * x.sy] = o[m];
+                        x.wr[m * a.sy] = o[m];
                         if (RESID) d = dmax(d, abs_bits(__dsub_rn(o[m], u1b[m + 1])));
                     }
                 if (RESID) x.r2 = dmax(x.r2, d);
@@ -2556,7 +2558,7 @@ __device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
         } else {
             if (x.own) {
 #pragma unroll
-                for (int m = 0; m < VW_R; ++m) x.wr[m * x.sy] = o[m];
+                for (int m = 0; m < VW_R; ++m) x.wr[m * a.sy] = o[m];
             }
             if (RESID) {
                 double d = abs_bits(__dsub_rn(o[0], u1b[1]));
@@ -2565,7 +2567,7 @@ __device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
                 if (x.own) x.r2 = dmax(x.r2, d);
             }
         }
-        vw2_next_plane(x);
+        vw2_next_plane<CHAIN>(x, a);
     }
     vw2_poll(x);
 }
@@ -2575,8 +2577,9 @@ __device__ __forceinline__ void vw2_step(VW2Ctx& x, const double (&up)[VW_RR],
 // scheduler interleaves the ten independent sums.  The residual of u(t+1)
 // is taken on every lane — rim lanes hold neighbour tiles' interior values,
 // and max is idempotent — that of u(t+2) on the owning lanes only.
-template <bool GUARD, bool RESID>
-__device__ __forceinline__ void vw2_step_fast(VW2Ctx& x, const double (&up)[VW_RR],
+template <bool GUARD, bool RESID, bool CHAIN>
+__device__ __forceinline__ void vw2_step_fast(VW2Ctx& x, const VolW2Args& a,
+                                              const double (&up)[VW_RR],
                                               const double (&mid)[VW_RR], double (&dn)[VW_RR],
                                               int& smid, const double (&u1a)[VW_R + 2],
                                               const double (&u1b)[VW_R + 2],
@@ -2622,7 +2625,7 @@ __device__ __forceinline__ void vw2_step_fast(VW2Ctx& x, const double (&up)[VW_R
     }
     if (x.own) {
 #pragma unroll
-        for (int m = 0; m < VW_R; ++m) x.wr[m * x.sy] = o[m];
+        for (int m = 0; m < VW_R; ++m) x.wr[m * a.sy] = o[m];
     }
     if (RESID) {
         double e1[VW_R], e2[VW_R];
@@ -2641,11 +2644,11 @@ __device__ __forceinline__ void vw2_step_fast(VW2Ctx& x, const double (&up)[VW_R
         x.r1 = dmax(x.r1, e1[0]);
         if (x.own) x.r2 = dmax(x.r2, e2[0]);
     }
-    vw2_next_plane(x);
+    vw2_next_plane<CHAIN>(x, a);
     vw2_poll(x);
 }
 
-template <bool GUARD, bool RESID>
+template <bool GUARD, bool RESID, bool CHAIN>
 __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u32,
                                             uint32_t full_u32, uint32_t empty_u32, int& s,
                                             uint32_t& ph, int2 ch, int64_t j0, int64_t k0,
@@ -2664,11 +2667,7 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     const int64_t k = k0 - 2 + pc;
     x.ring = ring_u32 + 8u * (uint32_t)pc;
     x.ex = a.ex * ch.y;
-    x.sx = a.sx;
-    x.sy = a.sy;
     x.rem = (int)a.ex;
-    x.cex = (int)a.ex;
-    x.cdelta = a.cdelta;
     x.xlo = a.nbr[cf].map[0][0] == nullptr;
     x.xhi = a.nbr[cz].map[1][0] == nullptr;
     unsigned vrow = 0;
@@ -2693,22 +2692,22 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     vw2_release(x, st0);
     vw2_take<VW_RR>(x, t1, smid);  // plane 0
     // register roles rotate with period 3: step q uses set (q-2) % 3
-    vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, 2);  // u(t+1) at plane 0
-    vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, 3);
+    vw2_step<GUARD, RESID, CHAIN>(x, a, t0, t1, t2, smid, y1, y2, y0, 2);  // u(t+1) at plane 0
+    vw2_step<GUARD, RESID, CHAIN>(x, a, t1, t2, t0, smid, y2, y0, y1, 3);
     int q = 4;
     if (!x.tmask)  // planes 2 .. ex: nothing outside the domain
         for (; q + 2 <= (int)x.ex + 2; q += 3) {
-            vw2_step_fast<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2);
-            vw2_step_fast<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0);
-            vw2_step_fast<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1);
+            vw2_step_fast<GUARD, RESID, CHAIN>(x, a, t2, t0, t1, smid, y0, y1, y2);
+            vw2_step_fast<GUARD, RESID, CHAIN>(x, a, t0, t1, t2, smid, y1, y2, y0);
+            vw2_step_fast<GUARD, RESID, CHAIN>(x, a, t1, t2, t0, smid, y2, y0, y1);
         }
     for (; q + 2 < nplanes; q += 3) {
-        vw2_step<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2, q);
-        vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q + 1);
-        vw2_step<GUARD, RESID>(x, t1, t2, t0, smid, y2, y0, y1, q + 2);
+        vw2_step<GUARD, RESID, CHAIN>(x, a, t2, t0, t1, smid, y0, y1, y2, q);
+        vw2_step<GUARD, RESID, CHAIN>(x, a, t0, t1, t2, smid, y1, y2, y0, q + 1);
+        vw2_step<GUARD, RESID, CHAIN>(x, a, t1, t2, t0, smid, y2, y0, y1, q + 2);
     }
-    if (q < nplanes) vw2_step<GUARD, RESID>(x, t2, t0, t1, smid, y0, y1, y2, q);
-    if (q + 1 < nplanes) vw2_step<GUARD, RESID>(x, t0, t1, t2, smid, y1, y2, y0, q + 1);
+    if (q < nplanes) vw2_step<GUARD, RESID, CHAIN>(x, a, t2, t0, t1, smid, y0, y1, y2, q);
+    if (q + 1 < nplanes) vw2_step<GUARD, RESID, CHAIN>(x, a, t0, t1, t2, smid, y1, y2, y0, q + 1);
     vw2_release(x, smid);  // the last plane only served as dn
     s = x.s;
     ph = x.ph;
@@ -2733,7 +2732,11 @@ __device__ __forceinline__ bool vw2_fast(const VolW2Args& a) {
 // Launched as a pair on one stream: the FAST instance runs when vw2_fast
 // holds, the guarded one otherwise; the other returns at once (the decision
 // is on the device: the scan it reads was written by an upload kernel).
-template <bool FAST, bool RESID>
+// CHAIN: the output pointer steps between the buffers of a chain's chunks
+// (the product launches CHAIN = true only: an instance without that
+// bookkeeping measured no faster — 492 vs 510 GLUPS on paper3d — its
+// register allocation spilled more)
+template <bool FAST, bool RESID, bool CHAIN>
 __global__ void __launch_bounds__(32 * (VW_CW + 1), HRT_VW_MINB)
 volume_wave2_kernel(VolW2Args wa) {
     if (vw2_fast(wa) != FAST) return;
@@ -2839,7 +2842,7 @@ volume_wave2_kernel(VolW2Args wa) {
         const int64_t zb = rem - yb * tk;
         const int2 ch = wa.chains[h];
         double r1 = 0.0, r2 = 0.0;
-        vw2_consume<!FAST, RESID>(wa, ring_u32, full_u32, empty_u32, s, ph, ch, 1 + yb * VW_R,
+        vw2_consume<!FAST, RESID, CHAIN>(wa, ring_u32, full_u32, empty_u32, s, ph, ch, 1 + yb * VW_R,
                                   1 + zb * VW_TZ, (wa.parity0 + k) & 1, r1, r2);
         if (RESID && wa.resid) {
             r1 = warp_max(r1);
@@ -2996,6 +2999,7 @@ struct Plan {
     int* d_v2clist = nullptr;
     int v2nchains = 0;
     int64_t v2cdelta = 0;
+    bool v2chained = false;            // some chain has more than one chunk
     bool v2dirty = true;               // maps / table to (re)build
     CUtensorMap* d_v2maps = nullptr;   // own [nchunks][2], then remote [nchunks][2 faces][2]
     // x faces to another process (hrt_jacobi_plan_set_vw2_remote): mapped
@@ -3653,13 +3657,13 @@ static int64_t vw2_tiles(const Plan* p, int64_t* tj = nullptr, int64_t* tk = nul
     return (int64_t)p->nchunks * a * b;
 }
 
-template <bool F, bool R>
+template <bool F, bool R, bool C>
 static int vw2_blocks_per_sm() {
     int n = 0;
-    cudaFuncSetAttribute(volume_wave2_kernel<F, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(volume_wave2_kernel<F, R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)VW_SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, volume_wave2_kernel<F, R>, 32 * (VW_CW + 1),
-                                                  VW_SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, volume_wave2_kernel<F, R, C>,
+                                                  32 * (VW_CW + 1), VW_SMEM);
     return n;
 }
 
@@ -3781,6 +3785,17 @@ static int build_vw2_nbr(Plan* p) {
     }
     for (int c = 0; c < p->nchunks; ++c)
         if (!seen[c]) chains.push_back({c});  // (a cycle cannot occur; defensive)
+    {
+        // whole chains by default (HRT_VW2_CHAIN caps the chunks per chain:
+        // experiments)
+        size_t cap = (size_t)p->nchunks;
+        if (const char* e = getenv("HRT_VW2_CHAIN")) cap = (size_t)std::max(1, atoi(e));
+        std::vector<std::vector<int>> cut;
+        for (const auto& ch : chains)
+            for (size_t j = 0; j < ch.size(); j += cap)
+                cut.emplace_back(ch.begin() + j, ch.begin() + std::min(ch.size(), j + cap));
+        chains.swap(cut);
+    }
     const hrt_chunk_layout_t& L = p->L;
     int64_t cstride = 0;
     bool uniform = true;
@@ -3807,6 +3822,8 @@ static int build_vw2_nbr(Plan* p) {
     }
     p->v2nchains = (int)ctab.size();
     p->v2cdelta = cstride / 8 - L.ext[0] * L.stride[0];
+    p->v2chained = false;
+    for (const auto& c : ctab) p->v2chained |= c.y > 1;
     cudaFree(p->d_v2chains);
     cudaFree(p->d_v2clist);
     p->d_v2chains = nullptr;
@@ -3859,8 +3876,8 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
         HRT_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
     }
     if (p->pgrid3 == 0) {
-        const int n = std::min(std::min(vw2_blocks_per_sm<true, true>(), vw2_blocks_per_sm<true, false>()),
-                               std::min(vw2_blocks_per_sm<false, true>(), vw2_blocks_per_sm<false, false>()));
+        const int n = std::min(std::min(vw2_blocks_per_sm<true, true, true>(), vw2_blocks_per_sm<true, false, true>()),
+                               std::min(vw2_blocks_per_sm<false, true, true>(), vw2_blocks_per_sm<false, false, true>()));
         HRT_CUDA(cudaGetLastError());
         if (n <= 0) {
             set_error("volume two-step kernel: no resident CTA slots");
@@ -3900,8 +3917,10 @@ static int launch_vfused(Plan* p, cudaStream_t s, int64_t first, int64_t nf,
     wa.err = p->d_err;
     // the unguarded instance, then the guarded one: exactly one of them
     // works (vw2_fast), the other returns at entry
-    void* fns[2] = {resid_base ? (void*)volume_wave2_kernel<true, true> : (void*)volume_wave2_kernel<true, false>,
-                    resid_base ? (void*)volume_wave2_kernel<false, true> : (void*)volume_wave2_kernel<false, false>};
+#define VW2K(F, R) ((void*)volume_wave2_kernel<F, R, true>)
+    void* fns[2] = {resid_base ? VW2K(true, true) : VW2K(true, false),
+                    resid_base ? VW2K(false, true) : VW2K(false, false)};
+#undef VW2K
     const unsigned grid = (unsigned)std::min<int64_t>(p->pgrid3, T);
     void* args[] = {&wa};
     for (void* fn : fns)
