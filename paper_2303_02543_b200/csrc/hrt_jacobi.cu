@@ -3474,8 +3474,12 @@ static int64_t fuse2_slots(const Plan* p) {
 static bool fuse2_use(const Plan* p) {
     if (!p->fuse2_on()) return false;
     if (p->fuse2 == 2) return true;
+    // with tile heights chosen for parallelism (hrt_jacobi_plan_set_persistent)
+    // two-step passes measured faster at every size, also where tiles are
+    // fewer than CTA slots (1024^2: 110 vs 85 GLUPS one step per pass);
+    // explicitly tall tiles on a small problem keep one step per pass
     const int64_t per_chunk = wave_tiles(p) / std::max(1, p->nchunks);
-    return per_chunk * p->tn() >= fuse2_slots(p);
+    return p->rows <= 16 || per_chunk * p->tn() >= fuse2_slots(p);
 }
 
 // steps per fused pass this plan runs (0: one step per pass)
@@ -4469,13 +4473,30 @@ int hrt_jacobi_plan_set_persistent(void* plan, const int32_t* nbr4, uint64_t tim
     // reads, fewer tile hand-offs: cfg2 591 -> 620 GLUPS); every rank of a
     // decomposition derives the same tiling from the same layout
     if (!p->rows_explicit && p->L.ndim == 2 && p->fuse2) {
-        // 256-row tiles when that still leaves at least one tile per
-        // resident CTA of the two-step kernel; otherwise 64-row tiles
+        // the tallest tiles (256, 64, 32 or 16 rows) that still leave at
+        // least one tile per resident CTA of the two-step kernel; 16-row
+        // tiles when none does (small problems live in L2 and are bound by
+        // parallelism: 1024^2 in 4x4 chunks 36 -> 110 GLUPS, 2048^2 in 8x8
+        // 130 -> 315, 4096^2 in 8x8 590 -> 596; 8192^2 and up keep 256)
         const int64_t ex = p->L.ext[0];
         const int64_t w = p->narrow_chunk() ? 256 : T4_COLS;
         const int64_t tc = (p->L.ext[1] + w - 1) / w;
-        const int64_t t256 = p->tn() * ((ex + 255) / 256) * tc;
-        p->rows = (ex % 256 != 1 && t256 >= fuse2_slots(p)) ? 256 : 64;
+        const int64_t slots = fuse2_slots(p);
+        int64_t pick = 0;
+        for (int64_t R : {256, 64, 32, 16}) {
+            if (ex % R == 1) continue;  // a 1-row last tile (two-step tiles need 2)
+            if (p->tn() * ((ex + R - 1) / R) * tc >= slots) {
+                pick = R;
+                break;
+            }
+        }
+        if (!pick)
+            for (int64_t R : {16, 32, 64})
+                if (ex % R != 1) {
+                    pick = R;
+                    break;
+                }
+        p->rows = pick ? pick : 64;
         if (p->graph) {
             cudaGraphExecDestroy(p->graph);
             p->graph = nullptr;
