@@ -156,3 +156,50 @@ def test_nonneg_bound_selects_guarded_division():
     assert not _nonneg(np.array([[[np.inf]]]))
     assert not _nonneg(np.array([[[np.nan]]]))
     assert 6 * NONNEG_MAX + 2 <= 2.0 ** 1000
+
+
+@pytest.mark.parametrize("grid", [(3, 5, 1), (4, 4, 1), (1, 7, 1), (6, 1, 1)])
+def test_nbhd9_is_the_3x3_block(grid):
+    """ChunkGrid.nbhd9 (the table behind hrt_jacobi_plan_set_wave2_nbr9):
+    row-major NW N NE W C E SW S SE by chunk coordinates, None off the
+    domain, and a corner present exactly when both faces next to it are
+    (the C side rejects anything else)."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid
+
+    cx, cy, _ = grid
+    cg = ChunkGrid((cx * 8, cy * 8, 1), grid=grid)
+    for lin in range(cg.nchunks):
+        ix, iy = lin % cx, lin // cx
+        want = []
+        for dx in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                x, y = ix + dx, iy + dy
+                want.append(x + cx * y if 0 <= x < cx and 0 <= y < cy else None)
+        got = cg.nbhd9(lin)
+        assert got == want, (lin, got, want)
+        for corner, a, b in ((0, 1, 3), (2, 1, 5), (6, 7, 3), (8, 7, 5)):
+            assert (got[corner] is not None) == (got[a] is not None and got[b] is not None)
+
+
+def test_run_segments_split_mixed_volume_runs_across_devices():
+    """Volume one-step and two-step launches keep separate counters: with
+    neighbours on other devices a run becomes the n mod 4 single steps, then
+    the passes (a fence between them); slabs, single devices and runs that
+    are all passes or all single steps stay whole."""
+    from types import SimpleNamespace
+
+    from paper_2303_02543_b200.jacobi import JacobiSolver
+
+    def solver(ndim, ngpu, world=1, persistent=True, k=2):
+        s = SimpleNamespace(used_gpus=list(range(ngpu)), world=world, persistent=persistent,
+                            layout=SimpleNamespace(ndim=ndim), steps_per_pass=k)
+        return s
+
+    seg = JacobiSolver._run_segments
+    assert seg(solver(3, 2), 10, 13) == [(10, 1), (11, 12)]
+    assert seg(solver(3, 1, world=4), 0, 6) == [(0, 2), (2, 4)]
+    assert seg(solver(3, 2), 0, 8) == [(0, 8)]        # passes only
+    assert seg(solver(3, 2), 0, 3) == [(0, 3)]        # single steps only
+    assert seg(solver(3, 1), 0, 13) == [(0, 13)]      # one device: stream order suffices
+    assert seg(solver(2, 2), 0, 13) == [(0, 13)]      # slabs share one counter array
+    assert seg(solver(3, 2, k=1), 0, 13) == [(0, 13)]  # no two-step passes
