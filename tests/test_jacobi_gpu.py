@@ -468,3 +468,28 @@ def test_volume_negative_zero_kept(hrt, oracle, monkeypatch):
         got = s.download()
         s.close()
         assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (fuse2, persistent)
+
+
+@pytest.mark.parametrize("dom,grid,rows_want", [((1024, 1024, 1), (4, 4, 1), 16),    # cfg1
+                                                ((2048, 2048, 1), (8, 8, 1), 16),
+                                                ((4096, 4096, 1), (8, 8, 1), 64),
+                                                ((8192, 8192, 1), (8, 8, 1), 256)])
+def test_tile_height_for_parallelism(hrt, oracle, dom, grid, rows_want):
+    """The tallest tile height (256/64/32/16 rows) leaving one two-step tile
+    per resident CTA, else 16, and two-step passes throughout; the small
+    shapes bitwise vs the oracle on random data (16-row tiles: rims of 2
+    rows from the tiles above and below are 25 % of the reads)."""
+    from paper_2303_02543_b200.jacobi import ChunkGrid, JacobiSolver
+
+    s = JacobiSolver(ChunkGrid(dom, grid=grid))
+    rows = {t[0] for t in s.tiling().values()}
+    assert rows == {rows_want} and s.steps_per_pass == 2, (rows, s.tiling())
+    if dom[0] <= 2048:
+        init = np.random.default_rng(dom[0]).random(dom) * 3.0 - 1.0
+        s.upload(init)
+        s.run(14, residual=True)
+        got, res = s.download(), s.residual_history()
+        ref, rref = oracle.jacobi_c(dom, 14, residual=True, initial=init)
+        assert np.array_equal(got, ref)
+        assert np.array_equal(res, rref)
+    s.close()
