@@ -219,6 +219,39 @@ if os.environ.get("DIST_CHECK_FULL", "1") != "0":
         ok_all &= ok
         print(f"dist_check world={world} full cfg3 {dom} steps={steps} (ipc, wavefront)={ipc}: "
               f"{'OK' if ok else 'DIFF'}", flush=True)
+# full paper3d size: the N-rank x-band volume run (cross-process two-step
+# passes through chains) against one GPU (itself bitwise vs the oracle in
+# test_parity_fullsize_gpu), field samples, sums and residual history
+if os.environ.get("DIST_CHECK_FULL", "1") != "0" and os.environ.get("HRT_PERSIST", "1") != "0":
+    dom, steps = (1024, 1024, 768), 100
+    cg = ChunkGrid(dom, ranks=world, grid=(8 * world, 1, 1))
+    s = DistributedJacobi(cg, rank, world, local)
+    s.upload()
+    s.run(steps, residual=True)
+    band, lo = s.download(), s.box_lo
+    res = s.global_residual_history()
+    two = s.two_step
+    s.close()
+    parts = [None] * world
+    dist.all_gather_object(parts, (lo, band.shape, float(band.sum()), band[::31, ::29, ::7].copy(), two))
+    if rank == 0:
+        from paper_2303_02543_b200.jacobi import JacobiSolver
+
+        one = JacobiSolver(ChunkGrid(dom, grid=(8, 1, 1)), gpus=[local])
+        one.upload()
+        one.run(steps, residual=True)
+        full = one.download()
+        r1 = one.residual_history()
+        one.close()
+        ok = np.array_equal(res, r1) and all(p[4] for p in parts)
+        for (l0, shape, ssum, sample, _) in parts:
+            ref = full[l0[0]:l0[0] + shape[0]]
+            ok &= float(ref.sum()) == ssum and np.array_equal(ref[::31, ::29, ::7], sample)
+        ok &= np.array_equal(band.view(np.uint64), full[lo[0]:lo[0] + band.shape[0]].view(np.uint64))
+        ok_all &= ok
+        print(f"dist_check world={world} full paper3d {dom} steps={steps} two-step="
+              f"{[p[4] for p in parts]}: {'OK' if ok else 'DIFF'}", flush=True)
+        del full
 dist.barrier()
 if rank == 0:
     print("DIST_CHECK", "PASS" if ok_all else "FAIL", flush=True)
