@@ -250,7 +250,9 @@ int hrt_jacobi_plan_set_wave_ipc(void *plan, const int32_t *rpeer4, const int32_
  * straight from the neighbour's chunk): per chunk and face N,S,W,E the
  * neighbour chunk's two buffers (bufs8, mapped here), the base of its
  * rank's tile counters (cnt4, mapped; 0 = not another process) and its
- * index in that rank's plan.  Only row faces qualify; otherwise a no-op. */
+ * index in that rank's plan.  Only row faces qualify; otherwise a no-op.
+ * (Kept for callers with row faces only; hrt_jacobi_plan_set_wave2_nbr9
+ * below covers every decomposition and is what the Python layer uses.) */
 int hrt_jacobi_plan_set_wave2_remote(void *plan, const uint64_t *bufs8, const uint64_t *cnt4,
                                      const int32_t *idx4);
 /* The whole 3 x 3 chunk neighbourhood of every chunk for two-step slab
