@@ -2789,8 +2789,11 @@ volume_wave2_kernel(VolW2Args wa) {
             const int64_t tile = t - (long long)k * T;
             const int64_t h = tile / per_chunk;  // chain
             const int64_t rem = tile - h * per_chunk;
-            const int64_t yb = rem / tk;
-            const int64_t zb = rem - yb * tk;
+            // y fastest in ticket order: y-adjacent tiles share half their
+            // rows (4 of 8) and should run nearly together, so the shared
+            // rows are still in L2 (z neighbours share 4 of 124 columns)
+            const int64_t zb = rem / tj;
+            const int64_t yb = rem - zb * tj;
             const int2 ch = wa.chains[h];
             if (!dead) {
                 // the 3 x 3 x 3 tile neighbourhood must be done with step 2k:
@@ -2838,8 +2841,9 @@ volume_wave2_kernel(VolW2Args wa) {
         const int64_t tile = t - (long long)k * T;
         const int64_t h = tile / per_chunk;
         const int64_t rem = tile - h * per_chunk;
-        const int64_t yb = rem / tk;
-        const int64_t zb = rem - yb * tk;
+        const int64_t zb = rem / tj;  // y fastest (see the producer)
+        const int64_t yb = rem - zb * tj;
+        const int64_t cidx = yb * tk + zb;  // the tile's counter within a chunk
         const int2 ch = wa.chains[h];
         double r1 = 0.0, r2 = 0.0;
         vw2_consume<!FAST, RESID, CHAIN>(wa, ring_u32, full_u32, empty_u32, s, ph, ch, 1 + yb * VW_R,
@@ -2876,7 +2880,7 @@ volume_wave2_kernel(VolW2Args wa) {
             if (xsys) __threadfence_system();
             else __threadfence();
             for (int j = 0; j < ch.y; ++j) {
-                unsigned int* d = wa.done + wa.clist[ch.x + j] * per_chunk + rem;
+                unsigned int* d = wa.done + wa.clist[ch.x + j] * per_chunk + cidx;
                 if (xsys)
                     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(d), "r"(v) : "memory");
                 else
