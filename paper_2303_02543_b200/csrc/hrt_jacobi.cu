@@ -3796,9 +3796,12 @@ static int build_vw2_nbr(Plan* p) {
     for (int c = 0; c < p->nchunks; ++c)
         if (!seen[c]) chains.push_back({c});  // (a cycle cannot occur; defensive)
     {
-        // whole chains by default (HRT_VW2_CHAIN caps the chunks per chain:
-        // experiments)
-        size_t cap = (size_t)p->nchunks;
+        // chains of up to ~256 planes: long enough that short chunks pay
+        // no per-tile start-up, short enough that adjacent tiles do not
+        // drift apart by more than L2 keeps their shared rows (1028-plane
+        // chains read 39 GB of DRAM per 4 paper3d passes, 256-plane ones
+        // less at the same speed); HRT_VW2_CHAIN overrides (experiments)
+        size_t cap = (size_t)std::max<int64_t>(1, 256 / std::max<int64_t>(1, p->L.ext[0]));
         if (const char* e = getenv("HRT_VW2_CHAIN")) cap = (size_t)std::max(1, atoi(e));
         std::vector<std::vector<int>> cut;
         for (const auto& ch : chains)
