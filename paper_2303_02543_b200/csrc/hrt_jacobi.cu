@@ -2414,17 +2414,16 @@ __device__ __forceinline__ void vw2_produce(const VolW2Args& a, uint32_t ring, u
 // Per-thread state of the volume two-step consumer (one tile).
 struct VW2Ctx {
     uint32_t ring;        // shared address of this thread's column in stage 0, row 0
-    uint32_t full, empty;
+    uint32_t full;        // full barriers; the empty ones follow them (VW_STAGES later)
     int s;
     uint32_t ph;
     bool ready;
-    int lane;
     bool tmask;           // some row or column of this warp's tile lies outside the domain
     bool xlo, xhi;        // the x faces are domain faces
     unsigned vrow;        // bit r: ring row r (0..7) inside the domain rows
     bool colok;           // this lane's column is inside the domain
     bool own;             // lane 1..30 with an inside column: stores + residuals
-    int64_t ex;           // planes of the chain
+    int ex;               // planes of the chain
     double* wr;           // plane 1, row j0, this column, buffer parity^1
     int rem;              // output planes left in the current chunk
     double r1, r2;
@@ -2467,7 +2466,13 @@ __device__ __forceinline__ void vw2_poll(VW2Ctx& x) {
 __device__ __forceinline__ void vw2_release(VW2Ctx& x, int st) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the next TMA
     __syncwarp();
-    mbar_arrive_lane0_u32(x.empty + 8u * (uint32_t)st, x.lane);
+    // lane 0 arrives (%laneid read in place: no register for it across the loop)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .u32 l;\n\t"
+        "mov.u32 l, %%laneid;\n\t"
+        "setp.eq.u32 p, l, 0;\n\t"
+        "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(x.full + 8u * (uint32_t)(VW_STAGES + st))
+        : "memory");
 }
 
 // one pipeline step q (ring plane q = u(t) plane i = q-1 arrives as dn):
@@ -2657,16 +2662,16 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     VW2Ctx x;
-    x.full = full_u32;
-    x.empty = empty_u32;
+    x.full = full_u32;  // (the empty barriers follow at full_u32 + 8 * VW_STAGES)
+    (void)empty_u32;
     x.s = s;
     x.ph = ph;
     x.ready = false;
-    x.lane = tid & 31;
-    const int pc = 1 + VW_ZO * warp + x.lane;  // ring column of k
+    const int lane = tid & 31;
+    const int pc = 1 + VW_ZO * warp + lane;  // ring column of k
     const int64_t k = k0 - 2 + pc;
     x.ring = ring_u32 + 8u * (uint32_t)pc;
-    x.ex = a.ex * ch.y;
+    x.ex = (int)a.ex * ch.y;
     x.rem = (int)a.ex;
     x.xlo = a.nbr[cf].map[0][0] == nullptr;
     x.xhi = a.nbr[cz].map[1][0] == nullptr;
@@ -2678,7 +2683,7 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     }
     x.vrow = vrow;
     x.colok = k >= 1 && k <= a.ez;
-    x.own = x.lane >= 1 && x.lane <= VW_ZO && x.colok;
+    x.own = lane >= 1 && lane <= VW_ZO && x.colok;
     x.tmask = __any_sync(0xffffffffu, !x.colok) || vrow != (1u << VW_RR) - 1u;
     x.wr = a.chunks[cf].b[parity ^ 1] + a.origin + a.sx + j0 * a.sy + k;
     x.r1 = r1;
@@ -2741,8 +2746,9 @@ __global__ void __launch_bounds__(32 * (VW_CW + 1), HRT_VW_MINB)
 volume_wave2_kernel(VolW2Args wa) {
     if (vw2_fast(wa) != FAST) return;
     extern __shared__ __align__(128) unsigned char vw2_dyn[];  // the ring: VW_SMEM bytes
-    __shared__ alignas(8) uint64_t full[VW_STAGES], empty[VW_STAGES], tq_full[WAVE_TQ],
-        tq_empty[WAVE_TQ];
+    __shared__ alignas(8) uint64_t fe[2 * VW_STAGES], tq_full[WAVE_TQ], tq_empty[WAVE_TQ];
+    uint64_t* full = fe;                // ring barriers: full, then empty
+    uint64_t* empty = fe + VW_STAGES;
     __shared__ long long tq[WAVE_TQ];
     __shared__ double red[2][VW_CW];
     const int tid = threadIdx.x;
