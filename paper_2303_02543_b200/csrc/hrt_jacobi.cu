@@ -2412,9 +2412,14 @@ __device__ __forceinline__ void vw2_produce(const VolW2Args& a, uint32_t ring, u
 }
 
 // Per-thread state of the volume two-step consumer (one tile).
+// the ring's barriers (full, then empty) at file scope: their shared
+// addresses are link-time constants, so the consumer keeps no register
+// for them
+__shared__ alignas(8) uint64_t vw2_fe[2 * VW_STAGES];
+__device__ __forceinline__ uint32_t vw2_bar(int k) { return smem_u32(&vw2_fe[k]); }
+
 struct VW2Ctx {
     uint32_t ring;        // shared address of this thread's column in stage 0, row 0
-    uint32_t full;        // full barriers; the empty ones follow them (VW_STAGES later)
     int s;
     uint32_t ph;
     bool ready;
@@ -2444,7 +2449,7 @@ __device__ __forceinline__ void vw2_next_plane(VW2Ctx& x, const VolW2Args& a) {
 
 template <int NP>
 __device__ __forceinline__ void vw2_take(VW2Ctx& x, double (&v)[NP], int& st) {
-    const uint32_t fb = x.full + 8u * (uint32_t)x.s;
+    const uint32_t fb = vw2_bar(x.s);
     if (!x.ready && !mbar_try_u32(fb, x.ph)) mbar_wait_u32_slow(fb, x.ph);
     st = x.s;
     const uint32_t base = x.ring + (uint32_t)x.s * VW_STAGE_BYTES;
@@ -2460,7 +2465,7 @@ __device__ __forceinline__ void vw2_take(VW2Ctx& x, double (&v)[NP], int& st) {
 // Poll the next stage once the step's shared loads are issued: try_wait
 // acquires, so shared loads after it wait for its ~90-cycle round trip.
 __device__ __forceinline__ void vw2_poll(VW2Ctx& x) {
-    x.ready = mbar_try_u32(x.full + 8u * (uint32_t)x.s, x.ph);
+    x.ready = mbar_try_u32(vw2_bar(x.s), x.ph);
 }
 
 __device__ __forceinline__ void vw2_release(VW2Ctx& x, int st) {
@@ -2471,7 +2476,7 @@ __device__ __forceinline__ void vw2_release(VW2Ctx& x, int st) {
         "{\n\t.reg .pred p;\n\t.reg .u32 l;\n\t"
         "mov.u32 l, %%laneid;\n\t"
         "setp.eq.u32 p, l, 0;\n\t"
-        "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(x.full + 8u * (uint32_t)(VW_STAGES + st))
+        "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(vw2_bar(VW_STAGES + st))
         : "memory");
 }
 
@@ -2662,7 +2667,7 @@ __device__ __forceinline__ void vw2_consume(const VolW2Args& a, uint32_t ring_u3
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     VW2Ctx x;
-    x.full = full_u32;  // (the empty barriers follow at full_u32 + 8 * VW_STAGES)
+    (void)full_u32;  // (vw2_fe: full barriers, then the empty ones)
     (void)empty_u32;
     x.s = s;
     x.ph = ph;
@@ -2746,9 +2751,9 @@ __global__ void __launch_bounds__(32 * (VW_CW + 1), HRT_VW_MINB)
 volume_wave2_kernel(VolW2Args wa) {
     if (vw2_fast(wa) != FAST) return;
     extern __shared__ __align__(128) unsigned char vw2_dyn[];  // the ring: VW_SMEM bytes
-    __shared__ alignas(8) uint64_t fe[2 * VW_STAGES], tq_full[WAVE_TQ], tq_empty[WAVE_TQ];
-    uint64_t* full = fe;                // ring barriers: full, then empty
-    uint64_t* empty = fe + VW_STAGES;
+    __shared__ alignas(8) uint64_t tq_full[WAVE_TQ], tq_empty[WAVE_TQ];
+    uint64_t* full = vw2_fe;            // ring barriers: full, then empty
+    uint64_t* empty = vw2_fe + VW_STAGES;
     __shared__ long long tq[WAVE_TQ];
     __shared__ double red[2][VW_CW];
     const int tid = threadIdx.x;
