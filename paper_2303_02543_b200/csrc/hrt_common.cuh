@@ -15,6 +15,10 @@ int cuda_fail(cudaError_t e, const char* what);
 struct Stream {
     cudaStream_t s = nullptr;
     int gpu = 0;
+    // hrt_bytes_equal's result word (device) and its pinned host mirror,
+    // allocated on first use, freed with the handle
+    unsigned long long* cmp_d = nullptr;
+    unsigned long long* cmp_h = nullptr;
 };
 
 inline Stream* as_stream(void* h) { return reinterpret_cast<Stream*>(h); }

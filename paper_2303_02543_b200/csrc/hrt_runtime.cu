@@ -342,10 +342,13 @@ int hrt_stream_destroy(void* stream, int owned) {
     if (!stream) return HRT_OK;
     Stream* s = as_stream(stream);
     cudaError_t e = cudaSuccess;
-    if (owned) {
-        use_device(s->gpu);
-        e = cudaStreamDestroy(s->s);
+    if (owned || s->cmp_d) use_device(s->gpu);
+    if (s->cmp_d) {
+        cudaStreamSynchronize(s->s);
+        cudaFree(s->cmp_d);
+        cudaFreeHost(s->cmp_h);
     }
+    if (owned) e = cudaStreamDestroy(s->s);
     delete s;
     HRT_CUDA(e);
     return HRT_OK;
@@ -576,20 +579,27 @@ int hrt_bytes_equal(void* stream, const void* a, const void* b, uint64_t bytes, 
     Stream* s = as_stream(stream);
     int rc = use_device(s->gpu);
     if (rc) return rc;
-    unsigned long long* d = nullptr;
-    HRT_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), s->s));
+    if (!s->cmp_d) {
+        // one word per stream handle, kept: a cudaMallocAsync per call went
+        // back to the OS at every synchronize (~1.4 ms per compare)
+        HRT_CUDA(cudaMalloc(&s->cmp_d, sizeof(unsigned long long)));
+        cudaError_t he = cudaHostAlloc(&s->cmp_h, sizeof(unsigned long long), cudaHostAllocDefault);
+        if (he != cudaSuccess) {
+            cudaFree(s->cmp_d);
+            s->cmp_d = nullptr;
+            HRT_CUDA(he);
+        }
+    }
+    unsigned long long* d = s->cmp_d;
     HRT_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s->s));
     const uint64_t n16 = bytes / 16;
     const uint64_t nb = std::min<uint64_t>((uint64_t)hrt::sm_count(s->gpu) * 4, (n16 + 511) / 512 + 1);
     hrt::bytes_diff_kernel<<<(unsigned)nb, 512, 0, s->s>>>(
         reinterpret_cast<const uint8_t*>(a), reinterpret_cast<const uint8_t*>(b), n16, bytes, d);
-    cudaError_t le = cudaGetLastError();
-    unsigned long long h = 0;
-    HRT_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s->s));
-    cudaFreeAsync(d, s->s);
+    HRT_CUDA(cudaGetLastError());
+    HRT_CUDA(cudaMemcpyAsync(s->cmp_h, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s->s));
     HRT_CUDA(cudaStreamSynchronize(s->s));
-    HRT_CUDA(le);
-    *equal = h == 0;
+    *equal = *s->cmp_h == 0;
     return HRT_OK;
 }
 
