@@ -203,3 +203,21 @@ def test_run_segments_split_mixed_volume_runs_across_devices():
     assert seg(solver(3, 1), 0, 13) == [(0, 13)]      # one device: stream order suffices
     assert seg(solver(2, 2), 0, 13) == [(0, 13)]      # slabs share one counter array
     assert seg(solver(3, 2, k=1), 0, 13) == [(0, 13)]  # no two-step passes
+
+
+def test_device_view_cached_per_allocation():
+    """A copy's task-argument view is built once per allocation and rebuilt
+    when the copy moves to another allocation."""
+    from paper_2303_02543_b200.devices import DeviceAllocation, DeviceRegistry
+    from paper_2303_02543_b200.objects import DeviceCopy
+    from paper_2303_02543_b200.runtime import Runtime
+
+    rt = Runtime(DeviceRegistry())
+    obj = HeteroObject(1, (16,), dtype=np.float64)
+    obj.copies[0] = DeviceCopy(DeviceAllocation(0, 0, 128, ptr=4096))
+    v = rt.device_view(obj, 0)
+    assert rt.device_view(obj, 0) is v
+    assert (v.ptr, v.shape, v.dtype) == (4096, (16,), np.dtype(np.float64))
+    obj.copies[0].allocation = DeviceAllocation(0, 128, 128, ptr=8192)
+    w = rt.device_view(obj, 0)
+    assert w is not v and w.ptr == 8192
