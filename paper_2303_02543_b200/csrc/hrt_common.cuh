@@ -5,6 +5,8 @@
 #include <stdio.h>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hrt_b200.h"
 
 namespace hrt {
@@ -19,6 +21,16 @@ struct Stream {
     // allocated on first use, freed with the handle
     unsigned long long* cmp_d = nullptr;
     unsigned long long* cmp_h = nullptr;
+};
+
+// NVTX range over a host entry point (header-only NVTX 3: a null check when
+// no profiler is attached); shows the enqueue side of runs, uploads and
+// messages on an Nsight Systems timeline next to the kernels they launch
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 inline Stream* as_stream(void* h) { return reinterpret_cast<Stream*>(h); }

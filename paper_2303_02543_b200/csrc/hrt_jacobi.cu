@@ -4170,6 +4170,7 @@ int hrt_jacobi_plan_set_offsets(void* plan, const int64_t* offs3) {
 // -> buffer `parity` of every chunk (to_chunks=1), or back (0)
 int hrt_jacobi_plan_field_copy(void* plan, void* stream, double* field, int64_t FY, int64_t FZ,
                                int parity, int to_chunks) {
+    hrt::NvtxRange nvtx_("hrt_jacobi_plan_field_copy");
     HRT_CHECK_ARG(plan && stream && field, "null argument");
     Plan* p = reinterpret_cast<Plan*>(plan);
     HRT_CHECK_ARG(p->d_offs || p->nchunks == 0, "set the chunk offsets first");
@@ -4718,6 +4719,7 @@ int hrt_jacobi_plan_halo(void* plan, void* stream, int parity) {
 // with a residual the graph is re-instantiated per pair — use mode 0 then).
 int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint64_t* resid,
                         int mode) {
+    hrt::NvtxRange nvtx_("hrt_jacobi_plan_run");
     HRT_CHECK_ARG(plan && stream && n >= 0, "bad run arguments");
     Plan* p = reinterpret_cast<Plan*>(plan);
     int rc = use_device(p->gpu);
@@ -4773,6 +4775,7 @@ int hrt_jacobi_plan_run(void* plan, void* stream, int64_t first, int64_t n, uint
 // launch on `stream`; returns the summed device durations.  Synchronises.
 int hrt_jacobi_plan_run_timed(void* plan, void* stream, int64_t first, int64_t n, uint64_t* resid,
                               double* update_ms, double* halo_ms, double* total_ms) {
+    hrt::NvtxRange nvtx_("hrt_jacobi_plan_run_timed");
     HRT_CHECK_ARG(plan && stream && n >= 0, "bad run arguments");
     Plan* p = reinterpret_cast<Plan*>(plan);
     int rc = use_device(p->gpu);

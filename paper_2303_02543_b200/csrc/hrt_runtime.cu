@@ -635,6 +635,7 @@ int hrt_copy_sm_async(void* stream, void* dst, const void* src, uint64_t bytes, 
 // one per native call.
 int hrt_copy_ordered(void* stream, void* dst, const void* src, uint64_t bytes, int peer,
                      const uint64_t* waits, int nwait, int method, uint64_t* token) {
+    hrt::NvtxRange nvtx_("hrt_copy_ordered");
     HRT_CHECK_ARG(stream && token, "null argument");
     HRT_CHECK_ARG(nwait >= 0 && (nwait == 0 || waits), "bad wait list");
     HRT_CHECK_ARG(bytes == 0 || (dst && src), "null copy pointer");
