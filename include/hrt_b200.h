@@ -95,7 +95,9 @@ int hrt_host_register(void *ptr, uint64_t bytes);
 int hrt_host_unregister(void *ptr);
 int hrt_copy_async(void *stream, void *dst, const void *src, uint64_t bytes);   /* H2D/D2H/D2D (UVA) */
 /* *equal = 1 when n bytes at a and b (device/peer, 16-byte aligned) are
- * identical (ping-pong byte identity, pingpong.py:135-138).  Synchronises. */
+ * identical (ping-pong byte identity, pingpong.py:135-138).  Synchronises.
+ * Uses a result word owned by the stream handle: one caller per handle at
+ * a time. */
 int hrt_bytes_equal(void *stream, const void *a, const void *b, uint64_t bytes, int *equal);
 /* SM-driven copy kernel on stream's GPU; dst/src may be peer (NVLink)
  * addresses, 16-byte aligned.  blocks <= 0: automatic. */
